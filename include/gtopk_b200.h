@@ -1,0 +1,181 @@
+/*
+ * gtopk_b200.h -- C ABI of the B200-native gTop-k hot path (arXiv 1901.04359).
+ *
+ * The reference (pure Python + numpy, /root/reference/pkg/src/gtopk) has no
+ * FFI: its plug points are the Python functions re-exported by
+ * gtopk/__init__.py:3-44.  Each entry point below states the reference
+ * function it replaces (file:line); INTEGRATION.md shows the ctypes binding a
+ * maintainer adds on the reference side.
+ *
+ * Conventions
+ *  - Every pointer argument named d_* or documented "device" is a device
+ *    pointer on the current CUDA device; `stream` is a cudaStream_t (void* so
+ *    the header does not need cuda_runtime.h; NULL = legacy default stream).
+ *  - Sparse lists on the device are (int32 idx[cap], float val[cap],
+ *    int32 count) with strictly increasing indices; the count lives in device
+ *    memory so chains of kernels never synchronise with the host.
+ *  - Every call returns a host status code (GTK_OK or GTK_E*).  Data-dependent
+ *    errors (non-finite input, exchange timeout) are reported through a device
+ *    status word (uint32, GTK_DEV_* bits) that the host reads once at the
+ *    Python boundary and raises as the reference's exception type.
+ *  - m < 2^31 (device indices are int32; all BASELINE configs satisfy this).
+ */
+#ifndef GTOPK_B200_H_
+#define GTOPK_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* host status codes */
+#define GTK_OK 0
+#define GTK_EINVAL 1      /* -> ValueError        (sparse.py:144-145, collectives.py:199-203) */
+#define GTK_ENONFINITE 2  /* -> FloatingPointError (sparse.py:146-147) */
+#define GTK_EPROTO 3      /* -> ProtocolError     (transport.py:47-48) */
+#define GTK_ETIMEOUT 4    /* -> TransportError    (transport.py:262-268) */
+#define GTK_ECUDA 5       /* CUDA runtime failure */
+#define GTK_ENOMEM 6      /* workspace too small */
+#define GTK_EABORTED 7    /* -> TransportError("cluster aborted") (transport.py:256-257) */
+
+/* device status word bits */
+#define GTK_DEV_NONFINITE 0x1u  /* select input held NaN/Inf */
+#define GTK_DEV_FALLBACK 0x2u   /* select used the exact dense fallback (informational) */
+#define GTK_DEV_TIMEOUT 0x4u    /* peer flag wait timed out */
+#define GTK_DEV_ABORTED 0x8u    /* abort flag observed */
+#define GTK_DEV_PEER_FAILED 0x10u /* a peer's step failed (poisoned message received) */
+#define GTK_DEV_ERROR_MASK 0x1Du  /* every bit except the informational FALLBACK */
+
+/* gtk_select flags */
+#define GTK_SELECT_FORCE_EXACT 0x1 /* skip the sampled-threshold fast path (testing) */
+
+int gtk_version(void);
+const char* gtk_strerror(int code);
+/* last CUDA error string seen by the library on this thread ("" if none) */
+const char* gtk_last_cuda_error(void);
+
+/* ------------------------------------------------------------------------
+ * K1: fused residual-add + exact top-k select.
+ * Replaces optimizer.py:219-220 (`accumulated = residual + g;
+ * top_k_select(accumulated, k)`) and sparse.py:135-154 (top_k_select).
+ *   res_in  : device f32[m] residual, or NULL (then acc = grad: plain top_k_select)
+ *   grad    : device f32[m]
+ *   res_out : device f32[m]; receives acc with +0.0 at the k selected slots
+ *             (may alias res_in or grad)
+ *   sel_idx/sel_val : device int32[k] / f32[k], index-ascending, values bitwise acc
+ *   d_count : device int32, set to k
+ *   d_status: device uint32, OR-ed with GTK_DEV_* bits (caller zeroes it)
+ *   ws      : device workspace of gtk_select_workspace_bytes(m,k) bytes,
+ *             zeroed once with gtk_workspace_init before first use; one
+ *             workspace per stream (calls on one workspace must be ordered).
+ * ------------------------------------------------------------------------ */
+int gtk_select_workspace_bytes(int64_t m, int32_t k, size_t* bytes);
+int gtk_workspace_init(void* ws, size_t bytes, void* stream);
+int gtk_select(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
+               int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
+               size_t ws_bytes, int32_t flags, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K2: the sparse top-k merge operator ⊤.
+ * Replaces sparse.py:157-195 (top_op(a, b, k)); a = received, b = own
+ * (collectives.py:214).  Output may alias b (in-place accumulator update).
+ *   a_idx/a_val/d_na, b_idx/b_val/d_nb : device lists (counts on device)
+ *   cap = max entries either input may hold (<= k in gTopKAllReduce)
+ * ------------------------------------------------------------------------ */
+int gtk_merge_workspace_bytes(int32_t cap, int32_t k, size_t* bytes);
+int gtk_top_op(const int32_t* a_idx, const float* a_val, const int32_t* d_na, const int32_t* b_idx,
+               const float* b_val, const int32_t* d_nb, int32_t cap, int32_t k, int32_t* o_idx,
+               float* o_val, int32_t* d_no, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K3: scatter the global top-k into the model update and return the
+ * extra residuals.  Replaces optimizer.py:227-230 (extra residual) and
+ * optimizer.py:243 + :92-105 (densify, /P, momentum, w -= lr*u).
+ *   scaling: 0 = "average" (v / FLOAT(P)), 1 = "sum" (v), 2 = v * FLOAT(P)
+ *            (2 is gtopk_naive_step's "sum" on pre-averaged values, optimizer.py:293-296)
+ *   vel may be NULL when momentum == 0.  l_idx may be NULL (no extra residual).
+ *   Bitwise identical to the reference's dense update.
+ * ------------------------------------------------------------------------ */
+int gtk_update_workspace_bytes(int64_t m, size_t* bytes);
+/*   d_skip: optional device status word; if any GTK_DEV_* error bit is set
+ *           the kernels leave w/res/vel untouched (a failed step must not
+ *           change the state, optimizer.py:219-230). */
+int gtk_scatter_update(float* w, float* res, float* vel, const int32_t* g_idx, const float* g_val,
+                       const int32_t* d_gn, const int32_t* l_idx, const float* l_val,
+                       const int32_t* d_ln, int64_t m, float lr, float momentum, int32_t P,
+                       int32_t scaling, const uint32_t* d_skip, void* ws, size_t ws_bytes,
+                       void* stream);
+
+/* optimizer.py:92-99 with a dense update: u = divide_by > 0 ? upd / FLOAT(divide_by) : upd;
+ * if vel: vel = FLOAT(mom)*vel + u, u = vel;  w -= FLOAT(lr) * u.  (dense/topk baselines) */
+int gtk_dense_apply(float* w, float* vel, const float* upd, int64_t m, float lr, float momentum,
+                    int32_t divide_by, void* stream);
+
+/* sparse.py:198-202 densify: out = zeros(m); out[idx] = val */
+int gtk_densify(const int32_t* idx, const float* val, const int32_t* d_n, int64_t m, float* out,
+                void* stream);
+
+/* collectives.py:158-164 (TopKAllReduce accumulate): out = zeros(m);
+ * for r in 0..P-1: out[idx_r] += val_r;  if divide: out /= FLOAT(P).
+ * (divide = 0 is the unscaled rank-order sum of optimizer.py:176-183.)
+ * lists are packed [P][stride] with counts d_n[P]. */
+int gtk_topk_accumulate(const int32_t* idx, const float* val, const int32_t* d_n, int32_t P,
+                        int64_t stride, int64_t m, float* out, int32_t divide, void* stream);
+
+/* rank-ordered dense sum of P device vectors (in-process dense baseline;
+ * optimizer.py:108-115 summation order). srcs: device array of P pointers. */
+int gtk_dense_sum(const float* const* srcs, int32_t P, int64_t m, float* out, void* stream);
+
+/* ------------------------------------------------------------------------
+ * gTopKAllReduce exchange (collectives.py:188-219) over NVLink peer memory.
+ * One persistent cooperative kernel per rank runs every round of the
+ * schedule: push the current list into the partner's inbox (peer stores),
+ * signal with a system-scope release, wait on its own inbox flag, merge (⊤).
+ *
+ *  schedule (host array, nsteps entries of 4 int32: {send_to, recv_from,
+ *  merge, tag}); send_to/recv_from = -1 for none; merge=1 -> acc = ⊤(recv, acc),
+ *  merge=0 -> acc = recv (broadcast).
+ *  peer_inbox: host array of P device pointers (IPC-mapped) to each rank's
+ *  inbox region of gtk_exchange_inbox_bytes(k, nsteps) bytes.
+ *  peer_flags: host array of P device pointers to each rank's uint64 flags[nsteps*2].
+ * ------------------------------------------------------------------------ */
+int gtk_exchange_inbox_bytes(int32_t k, int32_t nsteps, size_t* bytes);
+int gtk_exchange_flags_bytes(int32_t nsteps, size_t* bytes);
+/* cudaMalloc'd + zeroed region (IPC handles need whole allocations) */
+int gtk_dev_alloc(size_t bytes, void** dptr);
+int gtk_dev_free(void* dptr);
+int gtk_ipc_get_handle(void* dptr, void* handle_out /* 64 bytes */);
+int gtk_ipc_open_handle(const void* handle /* 64 bytes */, void** dptr_out);
+int gtk_ipc_close_handle(void* dptr);
+/*  d_epoch: device uint64 call counter, zero-initialised, advanced by the
+ *         kernel itself (so the launch can be captured in a CUDA graph and
+ *         replayed); it stays identical on every rank.
+ *  acc_*: in = this rank's local selection (<= k entries), out = the global
+ *         top-k, identical on all ranks.
+ *  step_counts: optional device int32[nsteps][2] receiving the entry counts
+ *         sent/received per step (message accounting, 12 + 12*n bytes each).
+ *  ws: a merge workspace of gtk_merge_workspace_bytes(k, k) bytes.
+ *  d_abort: optional (host-mapped) flag polled while waiting. */
+int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
+                       void* const* peer_inbox, uint64_t* const* peer_flags, uint64_t* d_epoch,
+                       int32_t* acc_idx, float* acc_val, int32_t* d_acc_n, int32_t k,
+                       uint32_t* d_status, const uint32_t* d_abort, int64_t timeout_ns,
+                       int32_t* step_counts, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Profiling hooks (bench.py; not part of the reference interface).
+ * When enabled, CUDA events are recorded on the launching stream around:
+ * id 0 = K1 main HBM pass, 1 = whole select, 2 = exchange kernel,
+ * 3 = standalone merge, 4 = K3 update.  Skipped while a stream is captured.
+ * ------------------------------------------------------------------------ */
+int gtk_prof_enable(int on);
+int gtk_prof_read(int id, double* total_ms, int64_t* count); /* synchronises pending events */
+int gtk_prof_reset(void);
+int64_t gtk_launch_count(void); /* kernels launched by this library so far */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GTOPK_B200_H_ */

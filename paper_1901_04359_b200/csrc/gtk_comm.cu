@@ -1,0 +1,260 @@
+// gTopKAllReduce over NVLink 5 / NVSwitch peer memory (reference
+// collectives.py:188-219 + binomial_bcast :168-185), fused with the ⊤ merge.
+//
+// One persistent cooperative kernel per rank executes the rank's whole
+// schedule (butterfly for P = 2^n, reduce-tree + binomial broadcast otherwise):
+//
+//   step s:  [send]  every block copies its share of the current accumulator
+//                    (count, idx[], val[]) into the partner's inbox slot
+//                    (s, epoch & 1) with plain stores to the IPC-mapped peer
+//                    pointer -- posted writes over NVLink -- then fences at
+//                    system scope and bumps the partner's step flag with a
+//                    red.release.sys.add;
+//            [recv]  thread 0 of every block spins (ld.acquire.sys) on its own
+//                    step flag until it reaches epoch * G (one arrival per
+//                    sender block per call; the counters are monotonic so they
+//                    never need resetting), with a %globaltimer timeout;
+//            [merge] acc = ⊤(inbox, acc) with the same device merge as K2
+//                    (received-then-own, collectives.py:214), or acc = inbox
+//                    for a broadcast step.
+//
+// Inbox slots are double-buffered by call parity; every rank receives the
+// final list causally after all merges of the call, so a slot is never
+// overwritten while its reader is still merging.
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "gtk_internal.h"
+#include "gtk_merge.cuh"
+
+namespace gtk {
+
+constexpr int kMaxSteps = 64;
+constexpr int kMaxRanks = 64;
+
+struct Step {
+  int32_t send_to, recv_from, merge, tag;
+};
+
+struct ExchangeArgs {
+  int32_t rank, P, nsteps, k;
+  uint64_t* d_epoch;  // device call counter (identical on every rank): graph-replay safe
+  Step steps[kMaxSteps];
+  char* inbox[kMaxRanks];     // peer-mapped inbox bases (index = rank)
+  uint64_t* flags[kMaxRanks]; // peer-mapped flag arrays
+  int32_t* acc_idx;
+  float* acc_val;
+  int32_t* d_acc_n;
+  uint32_t* d_status;
+  const volatile uint32_t* d_abort;
+  int64_t timeout_ns;
+  int32_t* step_counts;  // [nsteps][2] (sent, received) entry counts, for stats
+  MergeArgs merge;       // workspace pointers; list pointers filled per step
+};
+
+__host__ __device__ inline size_t slot_bytes(int32_t k) {
+  return (16 + (size_t)k * 8 + 255) & ~size_t(255);
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  MergeSmem& S = *reinterpret_cast<MergeSmem*>(dsm);
+  __shared__ uint32_t s_n;
+  const unsigned G = gridDim.x, blk = blockIdx.x;
+  // every block reads the counter before anyone advances it (block 0 does so
+  // after the final grid barrier)
+  const uint64_t epoch = __ldcg((const unsigned long long*)a.d_epoch) + 1;
+  const uint32_t par = (uint32_t)(epoch & 1u);
+  const uint64_t target = epoch * (uint64_t)G;
+  // poison: a rank whose select failed (non-finite input) still runs every
+  // step so no peer hangs, but sends count = -1; receivers flag PEER_FAILED
+  // and forward the poison, so every rank fails the step and K3 is skipped.
+  const bool self_poison = (__ldcg(a.d_status) & GTK_DEV_NONFINITE) != 0;
+
+  for (int s = 0; s < a.nsteps; ++s) {
+    const Step st = a.steps[s];
+    if (st.send_to >= 0) {
+      char* slot = a.inbox[st.send_to] + ((size_t)s * 2 + par) * slot_bytes(a.k);
+      int32_t* r_n = (int32_t*)slot;
+      int32_t* r_idx = (int32_t*)(slot + 16);
+      float* r_val = (float*)(slot + 16 + (size_t)a.k * 4);
+      const bool poisoned = self_poison || (__ldcg(a.d_status) & GTK_DEV_PEER_FAILED);
+      uint32_t n = poisoned ? 0u : (uint32_t)__ldcg(a.d_acc_n);
+      if (n > (uint32_t)a.k) n = a.k;
+      const uint32_t per = (n + G - 1) / G;
+      const uint32_t e0 = min(n, blk * per), e1 = min(n, e0 + per);
+      for (uint32_t e = e0 + threadIdx.x; e < e1; e += kMergeThreads) {
+        r_idx[e] = __ldcg(a.acc_idx + e);
+        r_val[e] = __ldcg(a.acc_val + e);
+      }
+      if (blk == 0 && threadIdx.x == 0) {
+        *r_n = poisoned ? -1 : (int32_t)n;
+        if (a.step_counts) a.step_counts[2 * s] = (int32_t)n;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        red_release_sys_add_u64(a.flags[st.send_to] + s, 1ull);
+      }
+    }
+    if (st.recv_from >= 0) {
+      if (threadIdx.x == 0) {
+        const uint64_t t0 = globaltimer();
+        uint32_t spins = 0;
+        while (ld_acquire_sys_u64(a.flags[a.rank] + s) < target) {
+          if (((++spins) & 1023u) == 0) {
+            if (a.d_abort && *a.d_abort) {
+              atomicOr(a.d_status, GTK_DEV_ABORTED);
+              break;
+            }
+            if (a.timeout_ns > 0 && (int64_t)(globaltimer() - t0) > a.timeout_ns) {
+              atomicOr(a.d_status, GTK_DEV_TIMEOUT);
+              break;
+            }
+          }
+          __nanosleep(64);
+        }
+        __threadfence();
+      }
+      __syncthreads();
+      char* slot = a.inbox[a.rank] + ((size_t)s * 2 + par) * slot_bytes(a.k);
+      const int32_t* in_idx = (const int32_t*)(slot + 16);
+      const float* in_val = (const float*)(slot + 16 + (size_t)a.k * 4);
+      if (threadIdx.x == 0) {
+        int32_t n = __ldcg((const int32_t*)slot);
+        if (n < 0 && blk == 0) atomicOr(a.d_status, GTK_DEV_PEER_FAILED);
+        s_n = (uint32_t)(n < 0 ? 0 : (n > a.k ? a.k : n));  // clamp (garbage after a timeout)
+      }
+      __syncthreads();
+      const uint32_t n_in = s_n;
+      if (blk == 0 && threadIdx.x == 0 && a.step_counts) a.step_counts[2 * s + 1] = (int32_t)n_in;
+      if (st.merge) {
+        uint32_t n_own = self_poison ? 0u : (uint32_t)__ldcg(a.d_acc_n);
+        if (n_own > (uint32_t)a.k) n_own = a.k;
+        grid_sync(&a.merge.ews->bar, G);  // everyone has read the counts
+        MergeArgs m = a.merge;
+        m.a_idx = in_idx;
+        m.a_val = in_val;
+        m.b_idx = a.acc_idx;
+        m.b_val = a.acc_val;
+        m.o_idx = a.acc_idx;
+        m.o_val = a.acc_val;
+        m.d_no = a.d_acc_n;
+        merge_device(m, n_in, n_own, G, S);
+      } else {
+        const uint32_t per = (n_in + G - 1) / G;
+        const uint32_t e0 = min(n_in, blk * per), e1 = min(n_in, e0 + per);
+        for (uint32_t e = e0 + threadIdx.x; e < e1; e += kMergeThreads) {
+          a.acc_idx[e] = __ldcg(in_idx + e);
+          a.acc_val[e] = __ldcg(in_val + e);
+        }
+        if (blk == 0 && threadIdx.x == 0) *a.d_acc_n = (int32_t)n_in;
+      }
+    }
+    grid_sync(&a.merge.ews->bar, G);
+  }
+  if (blk == 0 && threadIdx.x == 0) *a.d_epoch = epoch;
+}
+
+}  // namespace gtk
+
+using namespace gtk;
+
+extern "C" int gtk_exchange_inbox_bytes(int32_t k, int32_t nsteps, size_t* bytes) {
+  if (!bytes || k < 1 || nsteps < 0 || nsteps > kMaxSteps) return GTK_EINVAL;
+  *bytes = slot_bytes(k) * 2 * (size_t)(nsteps > 0 ? nsteps : 1);
+  return GTK_OK;
+}
+
+extern "C" int gtk_exchange_flags_bytes(int32_t nsteps, size_t* bytes) {
+  if (!bytes || nsteps < 0 || nsteps > kMaxSteps) return GTK_EINVAL;
+  *bytes = sizeof(uint64_t) * (size_t)(nsteps > 0 ? nsteps : 1);
+  return GTK_OK;
+}
+
+extern "C" int gtk_dev_alloc(size_t bytes, void** dptr) {
+  if (!dptr || bytes == 0) return GTK_EINVAL;
+  GTK_CUDA(cudaMalloc(dptr, bytes));
+  GTK_CUDA(cudaMemset(*dptr, 0, bytes));
+  return GTK_OK;
+}
+
+extern "C" int gtk_dev_free(void* dptr) {
+  if (dptr) GTK_CUDA(cudaFree(dptr));
+  return GTK_OK;
+}
+
+extern "C" int gtk_ipc_get_handle(void* dptr, void* handle_out) {
+  if (!dptr || !handle_out) return GTK_EINVAL;
+  cudaIpcMemHandle_t h;
+  GTK_CUDA(cudaIpcGetMemHandle(&h, dptr));
+  static_assert(sizeof(h) == 64, "ipc handle size");
+  std::memcpy(handle_out, &h, sizeof(h));
+  return GTK_OK;
+}
+
+extern "C" int gtk_ipc_open_handle(const void* handle, void** dptr_out) {
+  if (!handle || !dptr_out) return GTK_EINVAL;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  GTK_CUDA(cudaIpcOpenMemHandle(dptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return GTK_OK;
+}
+
+extern "C" int gtk_ipc_close_handle(void* dptr) {
+  if (!dptr) return GTK_EINVAL;
+  GTK_CUDA(cudaIpcCloseMemHandle(dptr));
+  return GTK_OK;
+}
+
+extern "C" int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
+                                  void* const* peer_inbox, uint64_t* const* peer_flags, uint64_t* d_epoch,
+                                  int32_t* acc_idx, float* acc_val, int32_t* d_acc_n, int32_t k,
+                                  uint32_t* d_status, const uint32_t* d_abort, int64_t timeout_ns,
+                                  int32_t* step_counts, void* ws, size_t ws_bytes, void* stream) {
+  if (P < 1 || P > kMaxRanks || rank < 0 || rank >= P || nsteps < 0 || nsteps > kMaxSteps || k < 1)
+    return GTK_EINVAL;
+  if (!acc_idx || !acc_val || !d_acc_n || !d_status || !ws || !d_epoch) return GTK_EINVAL;
+  if (nsteps > 0 && (!schedule || !peer_inbox || !peer_flags)) return GTK_EINVAL;
+  const MergeLayout L = merge_layout(k);
+  if (ws_bytes < L.total) return GTK_ENOMEM;
+  if (nsteps == 0) return GTK_OK;
+  ExchangeArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.rank = rank;
+  a.P = P;
+  a.nsteps = nsteps;
+  a.k = k;
+  a.d_epoch = d_epoch;
+  for (int s = 0; s < nsteps; ++s) {
+    a.steps[s] = Step{schedule[4 * s], schedule[4 * s + 1], schedule[4 * s + 2], schedule[4 * s + 3]};
+    if (a.steps[s].send_to >= P || a.steps[s].recv_from >= P) return GTK_EINVAL;
+  }
+  for (int r = 0; r < P; ++r) {
+    a.inbox[r] = (char*)peer_inbox[r];
+    a.flags[r] = peer_flags[r];
+  }
+  a.acc_idx = acc_idx;
+  a.acc_val = acc_val;
+  a.d_acc_n = d_acc_n;
+  a.d_status = d_status;
+  a.d_abort = (const volatile uint32_t*)d_abort;
+  a.timeout_ns = timeout_ns;
+  a.step_counts = step_counts;
+  char* base = (char*)ws;
+  a.merge = MergeArgs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, (uint32_t)k, nullptr, nullptr,
+                      nullptr, (MergeCtl*)(base + L.ctl), (EngineWS*)(base + L.engine),
+                      (int32_t*)(base + L.u_idx), (float*)(base + L.u_val)};
+  int G = merge_grid_for((const void*)exchange_kernel, k);
+  if (G <= 0) return GTK_ECUDA;
+  void* args[] = {&a};
+  ProfScope prof(kProfExchange, (cudaStream_t)stream);
+  return coop_launch((const void*)exchange_kernel, G, kMergeThreads, args, sizeof(MergeSmem), (cudaStream_t)stream);
+}

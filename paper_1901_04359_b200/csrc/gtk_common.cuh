@@ -1,0 +1,152 @@
+// Common device helpers for the gTop-k B200 library (sm_100a).
+//
+// Key convention (SURVEY.md §8a "key equivalence"): the selection key of an
+// fp32 value is its bit pattern with the sign cleared, key = bits & 0x7FFFFFFF.
+// For finite inputs this is monotone in |x|, so "k largest |g|, lower index
+// wins ties" (reference sparse.py:148-150) == "k largest key, lower index wins".
+// Non-finite values have key >= 0x7F800000.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/gtopk_b200.h"
+
+namespace gtk {
+
+constexpr uint32_t kKeyMask = 0x7FFFFFFFu;
+constexpr uint32_t kInfKey = 0x7F800000u;
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint32_t key_of(float x) { return __float_as_uint(x) & kKeyMask; }
+
+// Merge-side key (reference sparse.py:190 lexsort on -|v|): NaN magnitudes sort
+// LAST in numpy, below every nonzero finite or infinite value -> key 0.
+__device__ __forceinline__ uint32_t merge_key_of(float x) {
+  uint32_t k = __float_as_uint(x) & kKeyMask;
+  return k > kInfKey ? 0u : k;
+}
+
+// fp32 add with x86 SSE NaN semantics (the reference runs numpy on x86): the
+// result of a NaN-producing add of non-NaN operands is the "real indefinite"
+// 0xFFC00000; a NaN operand propagates quieted (first operand wins).
+__device__ __forceinline__ float add_x86(float a, float b) {
+  const float r = __fadd_rn(a, b);
+  if (r == r) return r;
+  const uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
+  if ((ua & kKeyMask) > kInfKey) return __uint_as_float(ua | 0x00400000u);
+  if ((ub & kKeyMask) > kInfKey) return __uint_as_float(ub | 0x00400000u);
+  return __uint_as_float(0xFFC00000u);
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned warp_id() { return threadIdx.x >> 5; }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint32_t warp_sum(uint32_t v) { return __reduce_add_sync(kFull, v); }
+
+// ---- memory-order primitives (PTX ISA memory consistency model) ----------
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_gpu_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_sys_add_u64(uint64_t* p, uint64_t v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// streaming (evict-first) 128-bit global accesses for the single-use m-length
+// arrays of the select pass.
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+  return __ldcs(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ void st_stream4(float* p, float4 v) {
+  __stcs(reinterpret_cast<float4*>(p), v);
+}
+
+// ---- grid-wide barrier for cooperative launches ---------------------------
+// Generation barrier; count returns to 0 after every use so the workspace
+// needs a single zero-initialisation.
+struct GridBarrier {
+  uint32_t count;
+  uint32_t gen;
+};
+
+__device__ __forceinline__ void grid_sync(GridBarrier* b, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t g = ld_acquire_gpu(&b->gen);
+    __threadfence();
+    const uint32_t prev = atomicAdd(&b->count, 1u);
+    if (prev == nblocks - 1) {
+      b->count = 0;
+      __threadfence();
+      st_release_gpu(&b->gen, g + 1);
+    } else {
+      while (ld_acquire_gpu(&b->gen) == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Block-wide exclusive scan of one uint32 per thread (NT threads, NT % 32 == 0).
+// `scratch` needs NT/32 + 1 words. Returns the exclusive prefix; *total gets the sum.
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* scratch, uint32_t* total) {
+  constexpr int NW = NT / 32;
+  const unsigned lane = lane_id(), w = warp_id();
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= (unsigned)o) x += y;
+  }
+  if (lane == 31) scratch[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t s = lane < (unsigned)NW ? scratch[lane] : 0u;
+    uint32_t t = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(kFull, t, o);
+      if (lane >= (unsigned)o) t += y;
+    }
+    if (lane < (unsigned)NW) scratch[lane] = t - s;
+    if (lane == 31) scratch[NW] = t;
+  }
+  __syncthreads();
+  const uint32_t res = scratch[w] + x - v;
+  *total = scratch[NW];
+  __syncthreads();
+  return res;
+}
+
+__host__ __device__ __forceinline__ uint32_t ceil_log2_u64(uint64_t x) {
+  uint32_t s = 0;
+  while ((1ull << s) < x) ++s;
+  return s;
+}
+
+}  // namespace gtk

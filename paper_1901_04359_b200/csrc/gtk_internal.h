@@ -1,0 +1,52 @@
+// Host-side helpers shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "../../include/gtopk_b200.h"
+
+namespace gtk {
+
+void set_last_cuda_error(cudaError_t e);
+int num_sms();
+// max co-resident blocks of `func` (cooperative launch limit) on the current device
+int coop_grid(const void* func, int threads, size_t smem);
+int coop_launch(const void* func, int grid, int threads, void** args, size_t smem, cudaStream_t st);
+// opt a kernel into > 48 KB of dynamic shared memory (once per device); false on error
+bool ensure_dyn_smem(const void* func, size_t bytes);
+// blocks for a cooperative ⊤-merge kernel over lists of <= cap entries
+int merge_grid_for(const void* func, int32_t cap);
+
+// ---- profiling hooks (bench.py): CUDA events around a launch, recorded on the
+// launching stream, only when enabled and the stream is not being captured ----
+enum ProfId { kProfSelectMain = 0, kProfSelect = 1, kProfExchange = 2, kProfMerge = 3, kProfUpdate = 4, kProfN = 8 };
+void prof_record(int id, cudaStream_t st, bool begin);
+void count_launch(int n = 1);
+
+struct ProfScope {
+  int id;
+  cudaStream_t st;
+  ProfScope(int i, cudaStream_t s) : id(i), st(s) { prof_record(id, st, true); }
+  ~ProfScope() { prof_record(id, st, false); }
+};
+
+}  // namespace gtk
+
+#define GTK_CHECK_LAUNCH()                        \
+  do {                                            \
+    cudaError_t _e = cudaGetLastError();          \
+    if (_e != cudaSuccess) {                      \
+      gtk::set_last_cuda_error(_e);               \
+      return GTK_ECUDA;                           \
+    }                                             \
+    gtk::count_launch();                          \
+  } while (0)
+
+#define GTK_CUDA(call)                            \
+  do {                                            \
+    cudaError_t _e = (call);                      \
+    if (_e != cudaSuccess) {                      \
+      gtk::set_last_cuda_error(_e);               \
+      return GTK_ECUDA;                           \
+    }                                             \
+  } while (0)

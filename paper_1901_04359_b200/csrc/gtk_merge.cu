@@ -1,0 +1,61 @@
+// K2: the sparse top-k merge operator ⊤ (reference sparse.py:157-195) as one
+// cooperative launch; the algorithm lives in gtk_merge.cuh.
+#include <cuda_runtime.h>
+
+#include "gtk_internal.h"
+#include "gtk_merge.cuh"
+
+namespace gtk {
+
+__global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  MergeSmem& S = *reinterpret_cast<MergeSmem*>(dsm);
+  const uint32_t na = (uint32_t)__ldcg(a.d_na), nb = (uint32_t)__ldcg(a.d_nb);
+  merge_device(a, na, nb, gridDim.x, S);
+}
+
+// blocks for a merge of two lists of <= cap entries: ~2K merged slots per
+// block (slices stay in shared memory), capped at one block per SM
+int merge_grid_for(const void* func, int32_t cap) {
+  if (!ensure_dyn_smem(func, sizeof(MergeSmem))) return 0;
+  const int want = (int)((2LL * cap + kMergeSub - 1) / kMergeSub);
+  int g = coop_grid(func, kMergeThreads, sizeof(MergeSmem));
+  if (g <= 0) return 0;
+  const int lim = num_sms();
+  if (g > lim) g = lim;
+  if (want < g) g = want < 1 ? 1 : want;
+  if (g > kMaxBlocks) g = kMaxBlocks;
+  return g;
+}
+
+int launch_merge(const MergeArgs& args, int32_t cap, cudaStream_t st) {
+  const int G = merge_grid_for((const void*)merge_kernel, cap);
+  if (G <= 0) return GTK_ECUDA;
+  MergeArgs a = args;
+  void* p[] = {&a};
+  ProfScope prof(kProfMerge, st);
+  return coop_launch((const void*)merge_kernel, G, kMergeThreads, p, sizeof(MergeSmem), st);
+}
+
+}  // namespace gtk
+
+using namespace gtk;
+
+extern "C" int gtk_merge_workspace_bytes(int32_t cap, int32_t k, size_t* bytes) {
+  if (!bytes || cap < 0 || k < 1) return GTK_EINVAL;
+  *bytes = merge_layout(cap < 1 ? 1 : cap).total;
+  return GTK_OK;
+}
+
+extern "C" int gtk_top_op(const int32_t* a_idx, const float* a_val, const int32_t* d_na, const int32_t* b_idx,
+                          const float* b_val, const int32_t* d_nb, int32_t cap, int32_t k, int32_t* o_idx,
+                          float* o_val, int32_t* d_no, void* ws, size_t ws_bytes, void* stream) {
+  if (!d_na || !d_nb || !o_idx || !o_val || !d_no || !ws || cap < 0 || k < 1) return GTK_EINVAL;
+  const MergeLayout L = merge_layout(cap < 1 ? 1 : cap);
+  if (ws_bytes < L.total) return GTK_ENOMEM;
+  char* base = (char*)ws;
+  MergeArgs args{a_idx, a_val, d_na, b_idx, b_val, d_nb, (uint32_t)k, o_idx, o_val, d_no,
+                 (MergeCtl*)(base + L.ctl), (EngineWS*)(base + L.engine), (int32_t*)(base + L.u_idx),
+                 (float*)(base + L.u_val)};
+  return launch_merge(args, cap < 1 ? 1 : cap, (cudaStream_t)stream);
+}

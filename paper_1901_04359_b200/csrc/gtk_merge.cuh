@@ -1,0 +1,245 @@
+// Device-side ⊤ merge (K2, reference sparse.py:157-195) shared by the
+// standalone merge launch (gtk_merge.cu) and the fused NVLink exchange kernel
+// (gtk_comm.cu).  Must run inside a cooperative launch of G blocks x
+// kMergeThreads with sizeof(MergeSmem) bytes of dynamic shared memory.
+//
+// phase 0: the merged sequence of A (received) and B (own) -- A first on equal
+//          indices -- is cut into G contiguous diagonal slices (merge path).
+//          Every block finds the A/B split of each of its 2048-slot
+//          sub-chunk boundaries in parallel (one warp per boundary, 33-ary
+//          search), stages the inputs in shared memory and builds its slice of
+//          union slots directly in shared memory: a shared index is summed once
+//          (a + b with x86 NaN semantics -- fp32 add is commutative, so the
+//          reference's received-then-own order, collectives.py:214, is met),
+//          exact zeros (+0/-0) become empty slots (sparse.py:184-186), and a
+//          2048-bin histogram of the top key bits is accumulated.
+// phase 1: the exact engine keeps the k largest by (|v| desc, idx asc), NaN
+//          magnitudes last (numpy lexsort, sparse.py:190), and compacts them in
+//          index order -- already index-sorted (sparse.py:194), no sort.
+// The output may alias B (in-place accumulator): every input read happens
+// before the first grid barrier.  All list loads are ld.global.cg, so lists
+// written by a peer GPU earlier in the same kernel are read correctly.
+#pragma once
+
+#include "gtk_engine.cuh"
+
+namespace gtk {
+
+constexpr int kMergeThreads = 512;
+constexpr int kMergeSub = 2048;        // merged slots staged per sub-chunk
+constexpr int kMergeSliceCap = 4096;   // slice slots kept in shared memory
+constexpr int kMergeMaxSplits = 65;    // sub-chunk boundaries per block (slice <= 128K)
+
+struct MergeCtl {
+  uint32_t n_valid;
+  uint32_t pad[63];
+};
+
+struct MergeLayout {
+  size_t ctl, engine, u_idx, u_val, total;
+};
+
+static inline MergeLayout merge_layout(int32_t cap) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  MergeLayout L{};
+  size_t off = 0;
+  L.ctl = off;
+  off = al(off + sizeof(MergeCtl));
+  L.engine = off;
+  off = al(off + sizeof(EngineWS));
+  L.u_idx = off;
+  off = al(off + sizeof(int32_t) * 2 * (size_t)cap);
+  L.u_val = off;
+  off = al(off + sizeof(float) * 2 * (size_t)cap);
+  L.total = off;
+  return L;
+}
+
+struct MergeArgs {
+  const int32_t* a_idx;
+  const float* a_val;
+  const int32_t* d_na;
+  const int32_t* b_idx;
+  const float* b_val;
+  const int32_t* d_nb;
+  uint32_t k;
+  int32_t* o_idx;
+  float* o_val;
+  int32_t* d_no;
+  MergeCtl* ctl;
+  EngineWS* ews;
+  int32_t* u_idx;  // global slot scratch for slices larger than kMergeSliceCap
+  float* u_val;
+};
+
+struct MergeSmem {
+  EngineSmem<kMergeThreads> esm;
+  int32_t slice_idx[kMergeSliceCap];
+  float slice_val[kMergeSliceCap];
+  int32_t sAi[kMergeSub], sBi[kMergeSub];
+  float sAv[kMergeSub], sBv[kMergeSub];
+  uint32_t split[kMergeMaxSplits];
+  uint32_t s_valid;
+};
+
+// number of A elements among the first d merged elements (A before B on ties);
+// executed by one full warp, result returned to every lane.
+static __device__ __forceinline__ uint32_t merge_path_warp(const int32_t* A, uint32_t na, const int32_t* B,
+                                                           uint32_t nb, uint32_t d) {
+  uint32_t L = d > nb ? d - nb : 0u;
+  uint32_t H = d < na ? d : na;
+  const unsigned lane = lane_id();
+  while (L < H) {
+    const uint32_t n = H - L;
+    if (n <= 32) {
+      bool q = false;
+      if (lane < n) {
+        const uint32_t i = L + lane;
+        q = __ldcg(A + i) <= __ldcg(B + (d - 1 - i));
+      }
+      L += __popc(__ballot_sync(kFull, q));
+      break;
+    }
+    const uint32_t p = L + (uint32_t)(((uint64_t)n * (lane + 1)) / 33);
+    const bool q = __ldcg(A + p) <= __ldcg(B + (d - 1 - p));
+    const unsigned bal = __ballot_sync(kFull, q);
+    const int t = __popc(bal);
+    const uint32_t p_prev = __shfl_sync(kFull, p, t > 0 ? t - 1 : 0);
+    const uint32_t p_t = __shfl_sync(kFull, p, t < 32 ? t : 31);
+    if (t == 0) {
+      H = p_t;
+    } else {
+      L = p_prev + 1;
+      if (t < 32) H = p_t;
+    }
+  }
+  return L;
+}
+
+static __device__ __forceinline__ uint32_t lower_bound_s(const int32_t* s, uint32_t n, int32_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (s[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+static __device__ __forceinline__ uint32_t upper_bound_s(const int32_t* s, uint32_t n, int32_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (s[mid] <= x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// na/nb are passed by value: the caller read them before any output write.
+static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t na, uint32_t nb, unsigned G,
+                                                    MergeSmem& S) {
+  EngineSmem<kMergeThreads>& esm = S.esm;
+  const unsigned blk = blockIdx.x;
+  const uint32_t N = na + nb;
+  if (N == 0) {
+    if (blk == 0 && threadIdx.x == 0) *a.d_no = 0;
+    grid_sync(&a.ews->bar, G);  // callers may reuse the inputs right after
+    return;
+  }
+  for (int b = threadIdx.x; b < kHistLen; b += kMergeThreads) esm.hist[b] = 0;
+  if (threadIdx.x == 0) S.s_valid = 0;
+
+  uint32_t d0, d1;
+  slice_of(N, G, blk, d0, d1);
+  const uint32_t L = d1 - d0;
+  const bool in_smem = L <= (uint32_t)kMergeSliceCap;
+  const uint32_t nsub = (L + kMergeSub - 1) / kMergeSub;
+  // all sub-chunk boundaries of the slice, one warp each, in parallel
+  for (uint32_t j = warp_id(); j <= nsub; j += kMergeThreads / 32) {
+    const uint32_t d = min(d1, d0 + j * kMergeSub);
+    const uint32_t i = merge_path_warp(a.a_idx, na, a.b_idx, nb, d);
+    if (lane_id() == 0) S.split[j] = i;
+  }
+  __syncthreads();
+  uint32_t my_valid = 0;
+  for (uint32_t j = 0; j < nsub; ++j) {
+    const uint32_t sub = d0 + j * kMergeSub, sub_end = min(d1, sub + kMergeSub);
+    const uint32_t ia = S.split[j], ib = S.split[j + 1];
+    const uint32_t ja = sub - ia, jb = sub_end - ib;
+    const uint32_t la = ib - ia, lb = jb - ja;
+    for (uint32_t t = threadIdx.x; t < la; t += kMergeThreads) {
+      S.sAi[t] = __ldcg(a.a_idx + ia + t);
+      S.sAv[t] = __ldcg(a.a_val + ia + t);
+    }
+    for (uint32_t t = threadIdx.x; t < lb; t += kMergeThreads) {
+      S.sBi[t] = __ldcg(a.b_idx + ja + t);
+      S.sBv[t] = __ldcg(a.b_val + ja + t);
+    }
+    const int32_t prevA = ia > 0 ? __ldcg(a.a_idx + ia - 1) : -1;
+    const int32_t nextB = jb < nb ? __ldcg(a.b_idx + jb) : -1;
+    const float nextBv = jb < nb ? __ldcg(a.b_val + jb) : 0.0f;
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < la; t += kMergeThreads) {
+      const int32_t x = S.sAi[t];
+      const uint32_t r = lower_bound_s(S.sBi, lb, x);
+      float v = S.sAv[t];
+      if (r < lb) {
+        if (S.sBi[r] == x) v = add_x86(v, S.sBv[r]);
+      } else if (nextB == x) {
+        v = add_x86(v, nextBv);
+      }
+      const uint32_t slot = sub + t + r;
+      const bool valid = v != 0.0f;
+      if (in_smem) {
+        S.slice_idx[slot - d0] = valid ? x : -1;
+        S.slice_val[slot - d0] = v;
+      } else {
+        a.u_idx[slot] = valid ? x : -1;
+        a.u_val[slot] = v;
+      }
+      if (valid) {
+        ++my_valid;
+        atomicAdd(&esm.hist[merge_key_of(v) >> 20], 1u);
+      }
+    }
+    for (uint32_t t = threadIdx.x; t < lb; t += kMergeThreads) {
+      const int32_t x = S.sBi[t];
+      const uint32_t r = upper_bound_s(S.sAi, la, x);
+      const bool dup = r > 0 ? (S.sAi[r - 1] == x) : (prevA == x);
+      const float v = S.sBv[t];
+      const uint32_t slot = sub + t + r;
+      const bool valid = !dup && v != 0.0f;
+      if (in_smem) {
+        S.slice_idx[slot - d0] = valid ? x : -1;
+        S.slice_val[slot - d0] = v;
+      } else {
+        a.u_idx[slot] = valid ? x : -1;
+        a.u_val[slot] = v;
+      }
+      if (valid) {
+        ++my_valid;
+        atomicAdd(&esm.hist[merge_key_of(v) >> 20], 1u);
+      }
+    }
+    __syncthreads();
+  }
+  my_valid = warp_sum(my_valid);
+  if (lane_id() == 0 && my_valid) atomicAdd(&S.s_valid, my_valid);
+  __syncthreads();
+  for (int b = threadIdx.x; b < kHistLen; b += kMergeThreads) {
+    const uint32_t c = esm.hist[b];
+    if (c) atomicAdd(&a.ews->hist[0][b], c);
+  }
+  if (threadIdx.x == 0 && S.s_valid) atomicAdd(&a.ctl->n_valid, S.s_valid);
+  grid_sync(&a.ews->bar, G);
+
+  const uint32_t n_valid = __ldcg(&a.ctl->n_valid);
+  const bool keep_all = n_valid <= a.k;
+  const SliceSrc src{S.slice_idx, S.slice_val, a.u_idx, a.u_val, d0, in_smem, true};
+  const Sink out{a.o_idx, a.o_val, a.d_no, nullptr};
+  engine_run<kMergeThreads>(src, d0, d1, keep_all ? n_valid : a.k, keep_all, 0u, 20u, true, a.ews, esm, out, G);
+  // every block read n_valid before the engine's first barrier
+  if (blk == 0 && threadIdx.x == 0) a.ctl->n_valid = 0;
+}
+
+}  // namespace gtk

@@ -1,0 +1,240 @@
+// K3: global top-k -> model update + extra residuals (reference
+// optimizer.py:227-230, :243, :92-105), plus the densify / TopKAllReduce /
+// dense-sum helpers of the baselines (sparse.py:198-202, collectives.py:158-164,
+// optimizer.py:108-115).
+//
+// Bit-exactness of the sparse update: the reference computes
+// u = densify(g)/FLOAT(P) densely and w -= FLOAT(lr)*u.  At untouched slots
+// u = +0, FLOAT(lr)*(+0) = +0 for finite lr with the sign bit clear, and
+// w - (+0) == w bitwise (including w = -0), so only the k touched slots change.
+// For any other lr (negative, -0, inf, nan) or momentum > 0 the dense kernel
+// runs instead.  All arithmetic uses explicit _rn intrinsics (no FMA
+// contraction), matching numpy's single-op fp32 rounding.
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "gtk_common.cuh"
+#include "gtk_internal.h"
+
+namespace gtk {
+
+constexpr int kUpdThreads = 256;
+constexpr int kDenseTile = 4096;  // elements per block in the dense update
+
+__device__ __forceinline__ bool sorted_contains(const int32_t* a, uint32_t n, int32_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    const int32_t y = __ldg(a + mid);
+    if (y < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo < n && __ldg(a + lo) == x;
+}
+
+__device__ __forceinline__ float scale_u(float v, float Pf, int scaling) {
+  return scaling == 0 ? __fdiv_rn(v, Pf) : (scaling == 2 ? __fmul_rn(v, Pf) : v);
+}
+
+// sparse path: global entries update w; local entries outside the global set
+// return to the residual.
+__device__ __forceinline__ bool skipped(const uint32_t* d_skip) {
+  return d_skip && (__ldcg(d_skip) & GTK_DEV_ERROR_MASK);
+}
+
+__global__ void __launch_bounds__(kUpdThreads)
+    scatter_update_kernel(float* w, float* res, const int32_t* g_idx, const float* g_val, const int32_t* d_gn,
+                          const int32_t* l_idx, const float* l_val, const int32_t* d_ln, float lr, float Pf,
+                          int scaling, int do_weights, const uint32_t* d_skip) {
+  if (skipped(d_skip)) return;
+  const uint32_t gn = (uint32_t)__ldg(d_gn);
+  const uint32_t ln = l_idx ? (uint32_t)__ldg(d_ln) : 0u;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (do_weights) {
+    for (uint32_t e = tid; e < gn; e += stride) {
+      const int32_t i = __ldg(g_idx + e);
+      const float u = scale_u(__ldg(g_val + e), Pf, scaling);
+      w[i] = __fsub_rn(w[i], __fmul_rn(lr, u));
+    }
+  }
+  for (uint32_t e = tid; e < ln; e += stride) {
+    const int32_t i = __ldg(l_idx + e);
+    if (!sorted_contains(g_idx, gn, i)) res[i] = __fadd_rn(res[i], __ldg(l_val + e));
+  }
+}
+
+// dense path (momentum > 0 or an lr for which the sparse form is not exact):
+// each block stages the global entries of its tile into shared memory.
+__global__ void __launch_bounds__(kUpdThreads)
+    dense_update_kernel(float* w, float* vel, const int32_t* g_idx, const float* g_val, const int32_t* d_gn,
+                        uint32_t m, float lr, float mom, float Pf, int scaling, const uint32_t* d_skip) {
+  __shared__ float su[kDenseTile];
+  __shared__ uint32_t s_rng[2];
+  if (skipped(d_skip)) return;
+  const uint32_t gn = (uint32_t)__ldg(d_gn);
+  const uint32_t t0 = blockIdx.x * kDenseTile;
+  const uint32_t t1 = min(m, t0 + kDenseTile);
+  for (int j = threadIdx.x; j < kDenseTile; j += kUpdThreads) su[j] = 0.0f;
+  if (threadIdx.x < 2) {
+    const int32_t x = (int32_t)(threadIdx.x == 0 ? t0 : t1);
+    uint32_t lo = 0, hi = gn;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(g_idx + mid) < x) lo = mid + 1;
+      else hi = mid;
+    }
+    s_rng[threadIdx.x] = lo;
+  }
+  __syncthreads();
+  for (uint32_t e = s_rng[0] + threadIdx.x; e < s_rng[1]; e += kUpdThreads)
+    su[__ldg(g_idx + e) - t0] = scale_u(__ldg(g_val + e), Pf, scaling);
+  __syncthreads();
+  for (uint32_t e = t0 + threadIdx.x; e < t1; e += kUpdThreads) {
+    float u = su[e - t0];
+    if (vel) {
+      const float v2 = __fadd_rn(__fmul_rn(mom, vel[e]), u);
+      vel[e] = v2;
+      u = v2;
+    }
+    w[e] = __fsub_rn(w[e], __fmul_rn(lr, u));
+  }
+}
+
+__global__ void dense_apply_kernel(float* w, float* vel, const float* upd, uint32_t m, float lr, float mom,
+                                   float Pf, int divide) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+    float u = upd[e];
+    if (divide) u = __fdiv_rn(u, Pf);
+    if (vel) {
+      u = __fadd_rn(__fmul_rn(mom, vel[e]), u);
+      vel[e] = u;
+    }
+    w[e] = __fsub_rn(w[e], __fmul_rn(lr, u));
+  }
+}
+
+__global__ void scatter_kernel(const int32_t* idx, const float* val, const int32_t* d_n, float* out) {
+  const uint32_t n = (uint32_t)__ldg(d_n);
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
+    out[__ldg(idx + e)] = __ldg(val + e);
+}
+
+__global__ void scatter_add_kernel(const int32_t* idx, const float* val, const int32_t* d_n, float* out) {
+  const uint32_t n = (uint32_t)__ldg(d_n);
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int32_t i = __ldg(idx + e);
+    out[i] = __fadd_rn(out[i], __ldg(val + e));
+  }
+}
+
+__global__ void divide_kernel(float* out, uint32_t m, float Pf) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x)
+    out[e] = __fdiv_rn(out[e], Pf);
+}
+
+__global__ void dense_sum_kernel(const float* const* srcs, int P, uint32_t m, float* out) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+    float acc = 0.0f;
+    for (int r = 0; r < P; ++r) acc = __fadd_rn(acc, srcs[r][e]);
+    out[e] = acc;
+  }
+}
+
+static int grid_for(uint64_t n, int threads) {
+  uint64_t g = (n + threads - 1) / threads;
+  const uint64_t cap = (uint64_t)num_sms() * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace gtk
+
+using namespace gtk;
+
+extern "C" int gtk_update_workspace_bytes(int64_t m, size_t* bytes) {
+  if (!bytes || m < 1) return GTK_EINVAL;
+  *bytes = 0;
+  return GTK_OK;
+}
+
+extern "C" int gtk_scatter_update(float* w, float* res, float* vel, const int32_t* g_idx, const float* g_val,
+                                  const int32_t* d_gn, const int32_t* l_idx, const float* l_val,
+                                  const int32_t* d_ln, int64_t m, float lr, float momentum, int32_t P,
+                                  int32_t scaling, const uint32_t* d_skip, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  (void)ws;
+  (void)ws_bytes;
+  if (!w || !g_idx || !g_val || !d_gn || m < 1 || m >= (int64_t(1) << 31) || P < 1) return GTK_EINVAL;
+  if (scaling < 0 || scaling > 2) return GTK_EINVAL;
+  if (l_idx && (!l_val || !d_ln || !res)) return GTK_EINVAL;
+  if (momentum > 0.0f && !vel) return GTK_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const float Pf = (float)P;
+  const bool sparse_exact = momentum == 0.0f && std::isfinite(lr) && !std::signbit(lr);
+  ProfScope prof(kProfUpdate, st);
+  if (!sparse_exact) {
+    const int tiles = (int)((m + kDenseTile - 1) / kDenseTile);
+    dense_update_kernel<<<tiles, kUpdThreads, 0, st>>>(w, momentum > 0.0f ? vel : nullptr, g_idx, g_val, d_gn,
+                                                        (uint32_t)m, lr, momentum, Pf, scaling, d_skip);
+    GTK_CHECK_LAUNCH();
+    if (l_idx) {
+      scatter_update_kernel<<<num_sms() * 2, kUpdThreads, 0, st>>>(w, res, g_idx, g_val, d_gn, l_idx, l_val, d_ln,
+                                                                    lr, Pf, scaling, 0, d_skip);
+      GTK_CHECK_LAUNCH();
+    }
+    return GTK_OK;
+  }
+  // k-length work: one launch updates w at the global entries and returns the
+  // local entries that missed the global set to the residual
+  scatter_update_kernel<<<num_sms() * 2, kUpdThreads, 0, st>>>(w, res, g_idx, g_val, d_gn, l_idx, l_val, d_ln, lr,
+                                                                Pf, scaling, 1, d_skip);
+  GTK_CHECK_LAUNCH();
+  return GTK_OK;
+}
+
+extern "C" int gtk_dense_apply(float* w, float* vel, const float* upd, int64_t m, float lr, float momentum,
+                               int32_t divide_by, void* stream) {
+  if (!w || !upd || m < 1 || m >= (int64_t(1) << 31) || divide_by < 0) return GTK_EINVAL;
+  if (momentum > 0.0f && !vel) return GTK_EINVAL;
+  dense_apply_kernel<<<grid_for(m, 256), 256, 0, (cudaStream_t)stream>>>(
+      w, momentum > 0.0f ? vel : nullptr, upd, (uint32_t)m, lr, momentum, (float)divide_by, divide_by > 0);
+  GTK_CHECK_LAUNCH();
+  return GTK_OK;
+}
+
+extern "C" int gtk_densify(const int32_t* idx, const float* val, const int32_t* d_n, int64_t m, float* out,
+                           void* stream) {
+  if (!idx || !val || !d_n || !out || m < 1 || m >= (int64_t(1) << 31)) return GTK_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  GTK_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)m, st));
+  scatter_kernel<<<num_sms() * 2, 256, 0, st>>>(idx, val, d_n, out);
+  GTK_CHECK_LAUNCH();
+  return GTK_OK;
+}
+
+extern "C" int gtk_topk_accumulate(const int32_t* idx, const float* val, const int32_t* d_n, int32_t P,
+                                   int64_t stride, int64_t m, float* out, int32_t divide, void* stream) {
+  if (!idx || !val || !d_n || !out || P < 1 || m < 1 || m >= (int64_t(1) << 31) || stride < 0)
+    return GTK_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  GTK_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)m, st));
+  for (int r = 0; r < P; ++r) {  // rank order 0..P-1 (collectives.py:162-163)
+    scatter_add_kernel<<<num_sms() * 2, 256, 0, st>>>(idx + r * stride, val + r * stride, d_n + r, out);
+    GTK_CHECK_LAUNCH();
+  }
+  if (divide) {
+    divide_kernel<<<grid_for(m, 256), 256, 0, st>>>(out, (uint32_t)m, (float)P);
+    GTK_CHECK_LAUNCH();
+  }
+  return GTK_OK;
+}
+
+extern "C" int gtk_dense_sum(const float* const* srcs, int32_t P, int64_t m, float* out, void* stream) {
+  if (!srcs || !out || P < 1 || m < 1 || m >= (int64_t(1) << 31)) return GTK_EINVAL;
+  dense_sum_kernel<<<grid_for(m, 256), 256, 0, (cudaStream_t)stream>>>(srcs, P, (uint32_t)m, out);
+  GTK_CHECK_LAUNCH();
+  return GTK_OK;
+}

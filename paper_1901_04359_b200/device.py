@@ -1,0 +1,212 @@
+"""Device-side plumbing: sparse lists in HBM, workspaces, and thin wrappers
+over the C-ABI kernels (`_lib`).  PyTorch is used only for device memory and
+streams; every computation is a kernel of `libgtopk_b200.so`.
+
+Device sparse list layout (one per rank per buffer): int32 idx[cap],
+float32 val[cap], int32 count[1] -- index-ascending, count on the device so a
+chain select -> merge rounds -> update never synchronises with the host.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+
+U64 = np.uint64
+F32 = np.float32
+
+
+def require_cuda() -> None:
+    _lib.load()
+    if not torch.cuda.is_available():
+        raise _lib.NativeLibraryError(
+            "no CUDA device visible: the gTop-k hot path runs only on the GPU (no CPU fallback)"
+        )
+
+
+def default_device() -> torch.device:
+    require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def P(t) -> ctypes.c_void_p:
+    """Raw device pointer of a tensor (or NULL)."""
+    return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+def stream_of(device: torch.device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class DeviceList:
+    """Index-sorted sparse list resident on one GPU."""
+
+    __slots__ = ("dim", "cap", "idx", "val", "count", "device")
+
+    def __init__(self, dim: int, cap: int, device: torch.device):
+        self.dim = int(dim)
+        self.cap = int(max(cap, 1))
+        self.device = device
+        self.idx = torch.empty(self.cap, dtype=torch.int32, device=device)
+        self.val = torch.empty(self.cap, dtype=torch.float32, device=device)
+        self.count = torch.zeros(1, dtype=torch.int32, device=device)
+
+    @classmethod
+    def from_host(cls, dim, indices, values, device, cap=None) -> "DeviceList":
+        indices = np.asarray(indices)
+        n = int(indices.size)
+        lst = cls(dim, max(n, cap or 0, 1), device)
+        if n:
+            lst.idx[:n].copy_(torch.from_numpy(indices.astype(np.int32)), non_blocking=False)
+            lst.val[:n].copy_(torch.from_numpy(np.asarray(values, dtype=F32)), non_blocking=False)
+        lst.count.fill_(n)
+        return lst
+
+    def nnz(self) -> int:
+        return int(self.count.item())
+
+    def to_host(self):
+        n = self.nnz()
+        idx = self.idx[:n].cpu().numpy().astype(U64)
+        val = self.val[:n].cpu().numpy().astype(F32)
+        return idx, val
+
+    def copy_from(self, other: "DeviceList") -> None:
+        n = min(self.cap, other.cap)
+        self.idx[:n].copy_(other.idx[:n], non_blocking=True)
+        self.val[:n].copy_(other.val[:n], non_blocking=True)
+        self.count.copy_(other.count, non_blocking=True)
+
+    def clone(self, cap=None) -> "DeviceList":
+        out = DeviceList(self.dim, cap or self.cap, self.device)
+        out.copy_from(self)
+        return out
+
+
+# ---------------------------------------------------------------------------
+# workspaces: one cache per host thread (one stream per worker thread), so
+# concurrent ranks in one process never share a workspace.
+# ---------------------------------------------------------------------------
+
+_tls = threading.local()
+
+
+def _cache() -> dict:
+    c = getattr(_tls, "ws", None)
+    if c is None:
+        c = _tls.ws = {}
+    return c
+
+
+def _new_ws(nbytes: int, device) -> torch.Tensor:
+    buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+    _lib.call("gtk_workspace_init", P(buf), ctypes.c_size_t(buf.numel()), stream_of(device))
+    return buf
+
+
+def select_workspace(m: int, k: int, device) -> torch.Tensor:
+    key = ("select", device.index, m, k)
+    c = _cache()
+    ws = c.get(key)
+    if ws is None:
+        n = ctypes.c_size_t()
+        _lib.call("gtk_select_workspace_bytes", m, k, ctypes.byref(n))
+        ws = c[key] = _new_ws(n.value, device)
+    return ws
+
+
+def merge_workspace(cap: int, k: int, device) -> torch.Tensor:
+    key = ("merge", device.index, cap)
+    c = _cache()
+    ws = c.get(key)
+    if ws is None:
+        n = ctypes.c_size_t()
+        _lib.call("gtk_merge_workspace_bytes", cap, k, ctypes.byref(n))
+        ws = c[key] = _new_ws(n.value, device)
+    return ws
+
+
+# ---------------------------------------------------------------------------
+# kernel wrappers
+# ---------------------------------------------------------------------------
+
+
+def select(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, out: DeviceList,
+           status: torch.Tensor, force_exact: bool = False) -> None:
+    """K1: res_out = res_in + grad (or grad), out = exact top-k of it, res_out
+    zeroed at the winners.  Stream-ordered, no host sync."""
+    m = grad.numel()
+    dev = grad.device
+    ws = select_workspace(m, k, dev)
+    _lib.call(
+        "gtk_select", P(res_in), P(grad), P(res_out), m, k, P(out.idx), P(out.val), P(out.count),
+        P(status), P(ws), ctypes.c_size_t(ws.numel()),
+        _lib.SELECT_FORCE_EXACT if force_exact else 0, stream_of(dev),
+    )
+
+
+def top_op(a: DeviceList, b: DeviceList, k: int, out: DeviceList) -> None:
+    """K2: out = ⊤(a, b, k) (a = received, b = own).  out may be b."""
+    dev = b.device
+    cap = max(a.cap, b.cap)
+    ws = merge_workspace(cap, k, dev)
+    _lib.call(
+        "gtk_top_op", P(a.idx), P(a.val), P(a.count), P(b.idx), P(b.val), P(b.count), cap, k,
+        P(out.idx), P(out.val), P(out.count), P(ws), ctypes.c_size_t(ws.numel()), stream_of(dev),
+    )
+
+
+def scatter_update(w, res, vel, glist: DeviceList, llist, m, lr, momentum, P_, scaling, skip=None) -> None:
+    """K3: weights update from the global list + extra residual from the local
+    list; a no-op on device if the status word `skip` carries an error bit."""
+    dev = w.device
+    _lib.call(
+        "gtk_scatter_update", P(w), P(res), P(vel), P(glist.idx), P(glist.val), P(glist.count),
+        P(llist.idx if llist is not None else None), P(llist.val if llist is not None else None),
+        P(llist.count if llist is not None else None), m, ctypes.c_float(lr),
+        ctypes.c_float(momentum), P_, scaling, P(skip), None, ctypes.c_size_t(0), stream_of(dev),
+    )
+
+
+def dense_apply(w, vel, upd, lr, momentum, divide_by: int = 0) -> None:
+    """optimizer.py:92-99 with a dense update vector (baselines)."""
+    _lib.call("gtk_dense_apply", P(w), P(vel if momentum > 0 else None), P(upd), w.numel(),
+              ctypes.c_float(lr), ctypes.c_float(momentum), int(divide_by), stream_of(w.device))
+
+
+def densify(lst: DeviceList, m: int, out: torch.Tensor) -> None:
+    _lib.call("gtk_densify", P(lst.idx), P(lst.val), P(lst.count), m, P(out), stream_of(out.device))
+
+
+def topk_accumulate(idx: torch.Tensor, val: torch.Tensor, counts: torch.Tensor, P_: int,
+                    stride: int, m: int, out: torch.Tensor, divide: bool = True) -> None:
+    _lib.call(
+        "gtk_topk_accumulate", P(idx), P(val), P(counts), P_, stride, m, P(out), 1 if divide else 0,
+        stream_of(out.device),
+    )
+
+
+def dense_sum(srcs, m: int, out: torch.Tensor) -> None:
+    ptrs = torch.tensor([t.data_ptr() for t in srcs], dtype=torch.int64, device=out.device)
+    _lib.call("gtk_dense_sum", P(ptrs), len(srcs), m, P(out), stream_of(out.device))
+    # keep the pointer table alive until the kernel has consumed it
+    torch.cuda.current_stream(out.device).synchronize()
+
+
+def raise_status(word: int) -> None:
+    """Raise the reference exception for a device status word."""
+    from .transport import TransportError
+
+    if word & _lib.DEV_NONFINITE:
+        raise FloatingPointError("non-finite values in dense input")
+    if word & _lib.DEV_ABORTED:
+        raise TransportError("cluster aborted")
+    if word & _lib.DEV_TIMEOUT:
+        raise TransportError("peer exchange timed out")
+    if word & _lib.DEV_PEER_FAILED:
+        raise TransportError("a peer rank failed during the exchange")

@@ -1,0 +1,257 @@
+"""One process per GPU (torchrun): the NVLink backend of the collectives.
+
+`init_dist_cluster()` returns this rank's `DistEndpoint`.  torch.distributed
+is the plumbing only:
+  * NCCL carries the baselines (TopKAllReduce's allgather, the dense
+    allreduce -- collectives.py:88-165),
+  * a gloo group carries host bytes (Endpoint.send/recv, the CUDA IPC handle
+    exchange, barriers).
+gTopKAllReduce itself is ONE kernel per rank (`gtk_gtopk_exchange`): it
+pushes its accumulator into the partner's IPC-mapped inbox over NVLink,
+signals with a system-scope release, waits on its own flag and merges (⊤),
+for every round of the schedule -- recursive-doubling butterfly for P = 2^n
+(bitwise equal to the reference's tree + broadcast), the reference's exact
+tree + binomial broadcast otherwise (collectives.py:206-217).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from . import collectives as _coll
+from . import device as _dev
+from .device import DeviceList, P
+from .transport import DEFAULT_TIMEOUT, Endpoint, TransportError, TransportStats, sparse_msg_bytes
+
+
+def _schedule(rank: int, world: int, mode: str):
+    if mode == "auto":
+        mode = "butterfly" if world & (world - 1) == 0 else "tree"
+    if mode == "butterfly":
+        return _coll.butterfly_schedule(rank, world), mode
+    return _coll.tree_schedule(rank, world), mode
+
+
+class _ExchangePlan:
+    """Per-k resources of the fused exchange: own inbox/flags (cudaMalloc,
+    IPC-exported), the peers' mapped pointers, accumulator and workspace."""
+
+    def __init__(self, group: "DistDeviceGroup", k: int):
+        lib = _lib.load()
+        self.k = k
+        steps, self.mode = _schedule(group.rank, group.world, group.mode)
+        self.nsteps = len(steps)
+        self.steps = steps
+        sched = np.array([[s, r, mg, j] for j, (s, r, mg) in enumerate(steps)], dtype=np.int32).reshape(-1)
+        self.schedule = (ctypes.c_int32 * max(len(sched), 1))(*sched.tolist())
+        n_in, n_fl = ctypes.c_size_t(), ctypes.c_size_t()
+        _lib.check(lib.gtk_exchange_inbox_bytes(k, self.nsteps, ctypes.byref(n_in)))
+        _lib.check(lib.gtk_exchange_flags_bytes(self.nsteps, ctypes.byref(n_fl)))
+        self.inbox, self.flags = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(lib.gtk_dev_alloc(n_in.value, ctypes.byref(self.inbox)))
+        _lib.check(lib.gtk_dev_alloc(n_fl.value, ctypes.byref(self.flags)))
+        handles = np.zeros(128, dtype=np.uint8)
+        _lib.check(lib.gtk_ipc_get_handle(self.inbox, handles[:64].ctypes.data_as(ctypes.c_void_p)))
+        _lib.check(lib.gtk_ipc_get_handle(self.flags, handles[64:].ctypes.data_as(ctypes.c_void_p)))
+        allh = [torch.zeros(128, dtype=torch.uint8) for _ in range(group.world)]
+        dist.all_gather(allh, torch.from_numpy(handles), group=group.gloo)
+        W = group.world
+        self.peer_inbox = (ctypes.c_void_p * W)()
+        self.peer_flags = (ctypes.c_void_p * W)()
+        self._opened = []
+        for r in range(W):
+            if r == group.rank:
+                self.peer_inbox[r] = self.inbox.value
+                self.peer_flags[r] = self.flags.value
+                continue
+            h = allh[r].numpy()
+            pi, pf = ctypes.c_void_p(), ctypes.c_void_p()
+            _lib.check(lib.gtk_ipc_open_handle(h[:64].ctypes.data_as(ctypes.c_void_p), ctypes.byref(pi)))
+            _lib.check(lib.gtk_ipc_open_handle(h[64:].ctypes.data_as(ctypes.c_void_p), ctypes.byref(pf)))
+            self.peer_inbox[r] = pi.value
+            self.peer_flags[r] = pf.value
+            self._opened += [pi, pf]
+        dev = group.device
+        self.acc = DeviceList(group.dim_hint, k, dev)
+        self.ws = _dev.merge_workspace(k, k, dev)
+        self.step_counts = torch.zeros(max(2 * self.nsteps, 2), dtype=torch.int32, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.epoch = torch.zeros(1, dtype=torch.int64, device=dev)  # advanced by the kernel
+        dist.barrier(group=group.gloo)  # every rank mapped every peer before first use
+
+    def close(self):
+        lib = _lib.load()
+        for p in self._opened:
+            lib.gtk_ipc_close_handle(p)
+        self._opened = []
+        lib.gtk_dev_free(self.inbox)
+        lib.gtk_dev_free(self.flags)
+
+
+class DistDeviceGroup:
+    """Device collectives for one rank of a torchrun job."""
+
+    def __init__(self, rank: int, world: int, device: torch.device, gloo, timeout: float,
+                 mode: str = "auto"):
+        self.rank = rank
+        self.world = world
+        self.P = world
+        self.device = device
+        self.gloo = gloo
+        self.timeout = timeout
+        self.mode = mode
+        self.dim_hint = 0
+        self._plans: dict[int, _ExchangePlan] = {}
+        self.aborted = False
+        self._abort_host = None
+
+    def abort(self) -> None:
+        self.aborted = True
+
+    def plan(self, k: int, dim: int) -> _ExchangePlan:
+        p = self._plans.get(k)
+        if p is None:
+            self.dim_hint = dim
+            p = self._plans[k] = _ExchangePlan(self, k)
+        p.acc.dim = dim
+        return p
+
+    # -- gTopKAllReduce ----------------------------------------------------
+    def gtopk(self, ep: Endpoint, lst: DeviceList, k: int, status: torch.Tensor | None = None) -> DeviceList:
+        """Fused NVLink exchange; returns the plan's accumulator (valid until
+        the next gtopk call with the same k)."""
+        if self.aborted:
+            raise TransportError("cluster aborted")
+        plan = self.plan(k, lst.dim)
+        if lst is not plan.acc:
+            plan.acc.copy_from(lst)
+        if self.world == 1:
+            return plan.acc
+        st = status if status is not None else plan.status
+        if status is None:
+            st.zero_()
+        _lib.call(
+            "gtk_gtopk_exchange", self.rank, self.world, plan.schedule, plan.nsteps, plan.peer_inbox,
+            plan.peer_flags, P(plan.epoch), P(plan.acc.idx), P(plan.acc.val), P(plan.acc.count),
+            k, P(st), None, ctypes.c_int64(int(self.timeout * 1e9)), P(plan.step_counts), P(plan.ws),
+            ctypes.c_size_t(plan.ws.numel()), _dev.stream_of(self.device),
+        )
+        counts = plan.step_counts.clone()  # snapshot for lazy byte accounting
+        for j, (s, r, _mg) in enumerate(plan.steps):
+            if s >= 0:
+                ep.stats.add_sparse(counts[2 * j:2 * j + 1], sent=True)
+            if r >= 0:
+                ep.stats.add_sparse(counts[2 * j + 1:2 * j + 2], sent=False)
+        if status is None:
+            word = int(st.item())
+            _dev.raise_status(word)
+        return plan.acc
+
+    # -- TopKAllReduce baseline: NCCL allgather + rank-order accumulation -----
+    def topk(self, ep: Endpoint, lst: DeviceList, divide: bool = True) -> torch.Tensor:
+        W = self.world
+        cnts = torch.empty(W, dtype=torch.int32, device=self.device)
+        dist.all_gather_into_tensor(cnts, lst.count)
+        cap = max(int(cnts.max().item()), 1)
+        idx = torch.zeros(W * cap, dtype=torch.int32, device=self.device)
+        val = torch.zeros(W * cap, dtype=torch.float32, device=self.device)
+        mi = torch.zeros(cap, dtype=torch.int32, device=self.device)
+        mv = torch.zeros(cap, dtype=torch.float32, device=self.device)
+        n = min(cap, lst.cap)
+        mi[:n].copy_(lst.idx[:n])
+        mv[:n].copy_(lst.val[:n])
+        dist.all_gather_into_tensor(idx, mi)
+        dist.all_gather_into_tensor(val, mv)
+        out = torch.empty(lst.dim, dtype=torch.float32, device=self.device)
+        _dev.topk_accumulate(idx, val, cnts, W, cap, lst.dim, out, divide=divide)
+        for s in range(W - 1):
+            ep.stats.add_sparse(cnts[(self.rank - s) % W:(self.rank - s) % W + 1], sent=True)
+            ep.stats.add_sparse(cnts[(self.rank - s - 1) % W:(self.rank - s - 1) % W + 1], sent=False)
+        return out
+
+    # -- dense baseline: NCCL allreduce (sum) -----------------------------------
+    def dense(self, ep: Endpoint, g: torch.Tensor) -> torch.Tensor:
+        W = self.world
+        m = torch.tensor([g.numel()], dtype=torch.int64)
+        ms = [torch.zeros(1, dtype=torch.int64) for _ in range(W)]
+        dist.all_gather(ms, m, group=self.gloo)
+        if any(int(x) != g.numel() for x in ms):
+            from .transport import ProtocolError
+
+            raise ProtocolError("ring chunk size mismatch across ranks")
+        out = g.clone()
+        if W > 1:
+            dist.all_reduce(out, op=dist.ReduceOp.SUM)
+        chunk = -(-g.numel() // W)
+        ep.stats.msgs_sent += 2 * (W - 1)
+        ep.stats.msgs_recv += 2 * (W - 1)
+        ep.stats.bytes_sent += 2 * (W - 1) * chunk * 4
+        ep.stats.bytes_recv += 2 * (W - 1) * chunk * 4
+        return out
+
+    def close(self) -> None:
+        for p in self._plans.values():
+            p.close()
+        self._plans.clear()
+
+
+class DistEndpoint(Endpoint):
+    """Endpoint of one torchrun rank; byte messages travel over gloo."""
+
+    def __init__(self, rank: int, world_size: int, group, gloo, timeout: float = DEFAULT_TIMEOUT):
+        super().__init__(rank, world_size, timeout)
+        self.group = group
+        self._gloo = gloo
+
+    def _send_impl(self, dest, tag, payload):
+        if self.group is not None and self.group.aborted:
+            raise TransportError("endpoint aborted")
+        n = torch.tensor([len(payload)], dtype=torch.int64)
+        dist.send(n, dest, group=self._gloo, tag=tag)
+        if len(payload):
+            dist.send(torch.frombuffer(bytearray(payload), dtype=torch.uint8), dest, group=self._gloo, tag=tag)
+
+    def _recv_impl(self, source, tag):
+        n = torch.zeros(1, dtype=torch.int64)
+        dist.recv(n, source, group=self._gloo, tag=tag)
+        if int(n) == 0:
+            return b""
+        buf = torch.empty(int(n), dtype=torch.uint8)
+        dist.recv(buf, source, group=self._gloo, tag=tag)
+        return bytes(buf.numpy().tobytes())
+
+    def abort(self):
+        if self.group is not None:
+            self.group.abort()
+
+    def close(self):
+        if self.group is not None and hasattr(self.group, "close"):
+            self.group.close()
+
+
+def init_dist_cluster(timeout: float = DEFAULT_TIMEOUT, mode: str = "auto", device_collectives: bool = True):
+    """Join the torchrun job (RANK/WORLD_SIZE/LOCAL_RANK/MASTER_* env) and
+    return this rank's endpoint.  mode: "auto" | "butterfly" | "tree"."""
+    backend = "nccl" if (device_collectives and torch.cuda.is_available()) else "gloo"
+    if not dist.is_initialized():
+        if backend == "nccl":
+            local = int(os.environ.get("LOCAL_RANK", "0"))
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    gloo = dist.new_group(backend="gloo") if backend == "nccl" else dist.group.WORLD
+    group = None
+    if device_collectives:
+        if not torch.cuda.is_available():
+            raise _lib.NativeLibraryError("device collectives need a CUDA device")
+        local = int(os.environ.get("LOCAL_RANK", str(rank % torch.cuda.device_count())))
+        group = DistDeviceGroup(rank, world, torch.device("cuda", local), gloo, timeout, mode)
+    return DistEndpoint(rank, world, group, gloo, timeout)

@@ -1,0 +1,210 @@
+"""GPU parity of the kernels K1 (select) and K2 (merge) through the C ABI,
+against golden vectors produced by the reference itself and the numpy oracle.
+Bar: bit-exact indices, values and residuals."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import cuda_ok, load_golden
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA GPU")]
+
+F32 = np.float32
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def gk():
+    import paper_1901_04359_b200 as gk
+
+    return gk
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import paper_1901_04359_b200.device as dev
+
+    return dev
+
+
+def _device_select(dev, g, k, res_in=None, force_exact=False):
+    import torch
+
+    d = torch.device("cuda", 0)
+    gd = torch.from_numpy(np.ascontiguousarray(g, F32)).to(d)
+    rd = None if res_in is None else torch.from_numpy(np.ascontiguousarray(res_in, F32)).to(d)
+    out_res = torch.empty_like(gd)
+    lst = dev.DeviceList(g.size, k, d)
+    st = torch.zeros(1, dtype=torch.int32, device=d)
+    dev.select(rd, gd, out_res, k, lst, st, force_exact=force_exact)
+    word = int(st.item())
+    i, v = lst.to_host()
+    return i, v, out_res.cpu().numpy(), word
+
+
+def test_select_golden_small(gk):
+    z = load_golden("select_small.npz")
+    for c in range(int(z["n"])):
+        g, k = z[f"c{c}_g"], int(z[f"c{c}_k"])
+        sel, res = gk.top_k_select(g, k)
+        assert np.array_equal(sel.indices, z[f"c{c}_idx"]), c
+        assert np.array_equal(sel.values.view(np.uint32), z[f"c{c}_val"].view(np.uint32)), c
+        if f"c{c}_res" in z:
+            assert np.array_equal(res.view(np.uint32), z[f"c{c}_res"].view(np.uint32)), c
+        else:
+            assert sha(res) == str(z[f"c{c}_res_sha"]), c
+
+
+def test_select_golden_small_forced_exact_fallback(dev):
+    """The dense exact fallback (engine over all m) must agree too."""
+    z = load_golden("select_small.npz")
+    for c in range(0, int(z["n"]), 3):
+        g, k = z[f"c{c}_g"], int(z[f"c{c}_k"])
+        i, v, res, word = _device_select(dev, g, k, force_exact=True)
+        assert word & 0x2, "fallback flag expected"
+        assert np.array_equal(i, z[f"c{c}_idx"]), c
+        assert np.array_equal(v.view(np.uint32), z[f"c{c}_val"].view(np.uint32)), c
+
+
+def test_select_golden_large(gk):
+    z = load_golden("select_large.npz")
+    for name in ("cfg1", "resnet20"):
+        m, k, P = int(z[f"{name}_m"]), int(z[f"{name}_k"]), int(z[f"{name}_P"])
+        rng = np.random.default_rng(0)
+        for r in range(P):
+            g = rng.standard_normal(m).astype(F32)
+            sel, res = gk.top_k_select(g, k)
+            assert np.array_equal(sel.indices, z[f"{name}_r{r}_idx"])
+            assert np.array_equal(sel.values, z[f"{name}_r{r}_val"])
+            assert sha(res) == str(z[f"{name}_r{r}_res_sha"])
+
+
+@pytest.mark.parametrize("kind", ["normal", "int", "layered", "spiky"])
+def test_fused_residual_select_vs_oracle(dev, kind):
+    from oracle import gtopk_oracle as orc
+
+    rng = np.random.default_rng(7)
+    for m, k in ((1, 1), (5, 3), (4097, 40), (100_003, 100), (300_000, 3000), (2_000_000, 2000)):
+        if kind == "normal":
+            g = rng.standard_normal(m).astype(F32)
+            r = (0.1 * rng.standard_normal(m)).astype(F32)
+        elif kind == "int":
+            g = rng.integers(-3, 4, m).astype(F32)
+            r = rng.integers(-1, 2, m).astype(F32)
+        elif kind == "layered":
+            g = rng.standard_normal(m).astype(F32)
+            g[: m // 7] *= F32(1000.0)
+            r = np.zeros(m, F32)
+        else:  # all mass concentrated in one short region
+            g = (1e-3 * rng.standard_normal(m)).astype(F32)
+            s = m // 2
+            g[s:s + 4 * k] = rng.standard_normal(min(4 * k, m - s)).astype(F32) * 100
+            r = np.zeros(m, F32)
+        acc = r + g
+        wi, wv, wres = orc.top_k_select(acc, k)
+        i, v, res, _ = _device_select(dev, g, k, res_in=r)
+        assert np.array_equal(i, wi), (kind, m, k)
+        assert np.array_equal(v.view(np.uint32), wv.view(np.uint32)), (kind, m, k)
+        assert np.array_equal(res.view(np.uint32), wres.view(np.uint32)), (kind, m, k)
+
+
+def test_select_nonfinite_raises(gk):
+    with pytest.raises(FloatingPointError):
+        gk.top_k_select(np.array([1.0, np.nan], F32), 1)
+    with pytest.raises(FloatingPointError):
+        gk.top_k_select(np.array([np.inf, 0.0], F32), 1)
+    g = np.random.default_rng(1).standard_normal(1_000_000).astype(F32)
+    g[777_777] = np.inf
+    with pytest.raises(FloatingPointError):
+        gk.top_k_select(g, 1000)
+
+
+def test_select_errors(gk):
+    with pytest.raises(ValueError):
+        gk.top_k_select([1.0, 2.0], 0)
+    with pytest.raises(ValueError):
+        gk.top_k_select([1.0, 2.0], 3)
+
+
+def test_select_full_size_properties(dev):
+    """BASELINE headline size m=25.6M, rho=0.001: size-independent properties
+    (exact count, index order, partition identity, optimality with the index
+    tie-break) checked on the device."""
+    import torch
+
+    d = torch.device("cuda", 0)
+    m, k = 25_600_000, 25_600
+    gen = torch.Generator(device=d).manual_seed(3)
+    g = torch.randn(m, device=d, generator=gen)
+    r = 0.1 * torch.randn(m, device=d, generator=gen)
+    out_res = torch.empty_like(g)
+    lst = dev.DeviceList(m, k, d)
+    st = torch.zeros(1, dtype=torch.int32, device=d)
+    for _ in range(3):  # repeated calls reuse the workspace
+        dev.select(r, g, out_res, k, lst, st)
+    assert int(st.item()) & ~0x2 == 0
+    assert lst.nnz() == k
+    idx = lst.idx[:k].long()
+    val = lst.val[:k]
+    assert bool((idx[1:] > idx[:-1]).all())
+    acc = r + g
+    assert torch.equal(val, acc[idx])
+    back = out_res.clone()
+    back[idx] = val
+    assert torch.equal(back.view(torch.int32), acc.view(torch.int32))
+    assert bool((out_res[idx] == 0).all())
+    key = acc.view(torch.int32) & 0x7FFFFFFF
+    tau = int(key[idx].min())
+    mask = torch.zeros(m, dtype=torch.bool, device=d)
+    mask[idx] = True
+    assert int((key[~mask] > tau).sum()) == 0
+    eq_out = torch.nonzero((key == tau) & ~mask).flatten()
+    eq_in = torch.nonzero((key == tau) & mask).flatten()
+    if eq_out.numel() and eq_in.numel():
+        assert int(eq_out.min()) > int(eq_in.max())
+
+
+def test_top_op_golden(gk):
+    z = load_golden("top_op.npz")
+    for c in range(int(z["n"])):
+        m, k = int(z[f"c{c}_m"]), int(z[f"c{c}_k"])
+        a = gk.SparseVector(m, z[f"c{c}_a_idx"], z[f"c{c}_a_val"])
+        b = gk.SparseVector(m, z[f"c{c}_b_idx"], z[f"c{c}_b_val"])
+        o = gk.top_op(a, b, k)
+        assert np.array_equal(o.indices, z[f"c{c}_o_idx"]), c
+        assert np.array_equal(o.values.view(np.uint32), z[f"c{c}_o_val"].view(np.uint32)), c
+
+
+def test_top_op_known_answers(gk):
+    sv = gk.SparseVector.from_pairs
+    a = sv(6, [(1, 0.5), (3, -2.0)])
+    b = sv(6, [(1, 0.6), (4, 1.0)])
+    assert gk.top_op(a, b, 2) == sv(6, [(1, np.float32(0.5) + np.float32(0.6)), (3, -2.0)])
+    a = sv(8, [(0, 1.0), (5, -3.0)])
+    assert gk.top_op(a, gk.SparseVector.empty(8), 2) == a
+    assert gk.top_op(gk.SparseVector.empty(8), a, 2) == a
+    assert gk.top_op(sv(3, [(0, 1.0)]), sv(3, [(0, -1.0)]), 1) == gk.SparseVector.empty(3)
+    with pytest.raises(ValueError):
+        gk.top_op(sv(3, [(0, 1.0)]), sv(4, [(0, 1.0)]), 1)
+
+
+@pytest.mark.parametrize("k", [1, 7, 1000, 25_600, 100_000])
+def test_top_op_large_vs_oracle(gk, k):
+    from oracle import gtopk_oracle as orc
+
+    rng = np.random.default_rng(k)
+    m = max(4 * k, 1000)
+    ga = rng.standard_normal(m).astype(F32)
+    gb = rng.standard_normal(m).astype(F32)
+    gb[: m // 3] = -ga[: m // 3]  # cancellation on a third of the shared indices
+    ai, av, _ = orc.top_k_select(ga, k)
+    bi, bv, _ = orc.top_k_select(gb, k)
+    wi, wv = orc.top_op(ai, av, bi, bv, k)
+    o = gk.top_op(gk.SparseVector(m, ai, av), gk.SparseVector(m, bi, bv), k)
+    assert np.array_equal(o.indices, wi)
+    assert np.array_equal(o.values.view(np.uint32), wv.view(np.uint32))
