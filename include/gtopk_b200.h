@@ -12,8 +12,12 @@
  *    pointer on the current CUDA device; `stream` is a cudaStream_t (void* so
  *    the header does not need cuda_runtime.h; NULL = legacy default stream).
  *  - Sparse lists on the device are (int32 idx[cap], float val[cap],
- *    int32 count) with strictly increasing indices; the count lives in device
- *    memory so chains of kernels never synchronise with the host.
+ *    int32 count[2]) with strictly increasing indices.  count[0] is the
+ *    entry count; count[1] is a k-th-key hint written by select/merge (the
+ *    key = bits & 0x7FFFFFFF of the list's k-th largest |value|, 0 = none)
+ *    that lets a later merge histogram a narrow window in one round -- it
+ *    never changes results.  Counts live in device memory so chains of
+ *    kernels never synchronise with the host.
  *  - Every call returns a host status code (GTK_OK or GTK_E*).  Data-dependent
  *    errors (non-finite input, exchange timeout) are reported through a device
  *    status word (uint32, GTK_DEV_* bits) that the host reads once at the
@@ -156,13 +160,16 @@ int gtk_ipc_close_handle(void* dptr);
  *         top-k, identical on all ranks.
  *  step_counts: optional device int32[nsteps][2] receiving the entry counts
  *         sent/received per step (message accounting, 12 + 12*n bytes each).
+ *  in_*: optional input list; when given the kernel first copies it into acc
+ *         (so the caller's local selection stays intact for K3).
  *  ws: a merge workspace of gtk_merge_workspace_bytes(k, k) bytes.
  *  d_abort: optional (host-mapped) flag polled while waiting. */
 int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
                        void* const* peer_inbox, uint64_t* const* peer_flags, uint64_t* d_epoch,
                        int32_t* acc_idx, float* acc_val, int32_t* d_acc_n, int32_t k,
                        uint32_t* d_status, const uint32_t* d_abort, int64_t timeout_ns,
-                       int32_t* step_counts, void* ws, size_t ws_bytes, void* stream);
+                       int32_t* step_counts, const int32_t* in_idx, const float* in_val,
+                       const int32_t* d_in_n, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
  * Profiling hooks (bench.py; not part of the reference interface).
@@ -173,6 +180,9 @@ int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedule, int32_t
 int gtk_prof_enable(int on);
 int gtk_prof_read(int id, double* total_ms, int64_t* count); /* synchronises pending events */
 int gtk_prof_reset(void);
+/* pairs recorded during stream capture are event-record graph nodes; after a
+ * synchronised replay this returns the sum of their current durations */
+int gtk_prof_graph_read(int id, double* ms, int64_t* count);
 int64_t gtk_launch_count(void); /* kernels launched by this library so far */
 
 #ifdef __cplusplus

@@ -59,6 +59,7 @@ EXPORTS = (
     "gtk_prof_enable",
     "gtk_prof_read",
     "gtk_prof_reset",
+    "gtk_prof_graph_read",
     "gtk_launch_count",
 )
 
@@ -95,12 +96,13 @@ _SIGS = {
     "gtk_ipc_open_handle": ([_P, ctypes.POINTER(_P)], _I32),
     "gtk_ipc_close_handle": ([_P], _I32),
     "gtk_gtopk_exchange": (
-        [_I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _SZ, _P],
+        [_I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P],
         _I32,
     ),
     "gtk_prof_enable": ([_I32], _I32),
     "gtk_prof_read": ([_I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)], _I32),
     "gtk_prof_reset": ([], _I32),
+    "gtk_prof_graph_read": ([_I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)], _I32),
     "gtk_launch_count": ([], _I64),
 }
 
@@ -115,6 +117,14 @@ def prof_read(pid: int):
     """(total_ms, count) of a profiled launch site (synchronises)."""
     tot, cnt = ctypes.c_double(), _I64()
     check(load().gtk_prof_read(pid, ctypes.byref(tot), ctypes.byref(cnt)), "gtk_prof_read")
+    return tot.value, cnt.value
+
+
+def prof_graph_read(pid: int):
+    """(ms, count) of the graph-captured pairs of a launch site, as of the
+    last (synchronised) replay."""
+    tot, cnt = ctypes.c_double(), _I64()
+    check(load().gtk_prof_graph_read(pid, ctypes.byref(tot), ctypes.byref(cnt)), "gtk_prof_graph_read")
     return tot.value, cnt.value
 
 _lock = threading.Lock()

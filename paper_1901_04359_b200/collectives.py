@@ -183,7 +183,7 @@ def _local_gtopk_leader(ops):
         half, span = 1 << (j - 1), 1 << j
         for r in range(0, P, span):
             if r + half < P:
-                log[nmsg:nmsg + 1].copy_(acc[r + half].count)
+                log[nmsg:nmsg + 1].copy_(acc[r + half].n)
                 sends.append((r + half, r, nmsg))
                 nmsg += 1
                 _dev.top_op(acc[r + half], acc[r], k, acc[r])
@@ -199,8 +199,8 @@ def _local_gtopk_leader(ops):
         half = 1 << (j - 1)
         for rel in range(P):
             if rel < half and rel + half < P:
-                ops[rel][0].stats.add_sparse(final.count, sent=True)
-                ops[rel + half][0].stats.add_sparse(final.count, sent=False)
+                ops[rel][0].stats.add_sparse(final.n, sent=True)
+                ops[rel + half][0].stats.add_sparse(final.n, sent=False)
     return final
 
 
@@ -288,7 +288,7 @@ def _local_topk_leader(ops, divide=True):
             raise ProtocolError("sparse dim mismatch in topk_allreduce")
         idx[r, : lst.cap].copy_(lst.idx)
         val[r, : lst.cap].copy_(lst.val)
-        cnt[r:r + 1].copy_(lst.count)
+        cnt[r:r + 1].copy_(lst.n)
     out = torch.empty(m, dtype=torch.float32, device=dev)
     _dev.topk_accumulate(idx, val, cnt, P, cap, m, out, divide=divide)
     _allgather_stats(ops, cnt)

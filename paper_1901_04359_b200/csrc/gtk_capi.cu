@@ -104,19 +104,31 @@ static cudaEvent_t pool_get() {
   return e;
 }
 
+// pairs recorded while a stream was being captured become event-record nodes
+// of the graph: they are re-recorded on every replay and read in place
+static std::vector<PendingPair> g_graph_pairs;
+static std::vector<cudaEvent_t> g_graph_open[kProfN];
+
 void prof_record(int id, cudaStream_t st, bool begin) {
   if (!g_prof_on.load(std::memory_order_relaxed) || id < 0 || id >= kProfN) return;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return;
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
   std::lock_guard<std::mutex> g(g_prof_mu);
   cudaEvent_t e = pool_get();
-  if (!e || cudaEventRecord(e, st) != cudaSuccess) return;
+  if (!e) return;
+  if (capturing) {
+    if (cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) != cudaSuccess) return;
+  } else if (cudaEventRecord(e, st) != cudaSuccess) {
+    return;
+  }
+  auto& open = capturing ? g_graph_open[id] : g_open[id];
   if (begin) {
-    g_open[id].push_back(e);
-  } else if (!g_open[id].empty()) {
-    cudaEvent_t a = g_open[id].back();
-    g_open[id].pop_back();
-    g_pending.push_back(PendingPair{id, a, e});
+    open.push_back(e);
+  } else if (!open.empty()) {
+    cudaEvent_t a = open.back();
+    open.pop_back();
+    (capturing ? g_graph_pairs : g_pending).push_back(PendingPair{id, a, e});
   }
 }
 
@@ -155,10 +167,36 @@ extern "C" int gtk_prof_reset(void) {
     g_pool.push_back(p.b);
   }
   g_pending.clear();
+  for (auto& p : g_graph_pairs) {
+    g_pool.push_back(p.a);
+    g_pool.push_back(p.b);
+  }
+  g_graph_pairs.clear();
   for (int i = 0; i < kProfN; ++i) {
     g_sum_ms[i] = 0;
     g_cnt[i] = 0;
+    g_open[i].clear();
+    g_graph_open[i].clear();
   }
+  return GTK_OK;
+}
+
+extern "C" int gtk_prof_graph_read(int id, double* ms, int64_t* count) {
+  using namespace gtk;
+  if (id < 0 || id >= kProfN || !ms || !count) return GTK_EINVAL;
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  double s = 0;
+  int64_t n = 0;
+  for (auto& p : g_graph_pairs) {
+    if (p.id != id) continue;
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess) {
+      s += t;
+      ++n;
+    }
+  }
+  *ms = s;
+  *count = n;
   return GTK_OK;
 }
 

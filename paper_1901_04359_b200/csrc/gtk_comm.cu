@@ -50,6 +50,9 @@ struct ExchangeArgs {
   const volatile uint32_t* d_abort;
   int64_t timeout_ns;
   int32_t* step_counts;  // [nsteps][2] (sent, received) entry counts, for stats
+  const int32_t* in_idx; // optional input list copied into acc first (keeps the
+  const float* in_val;   // caller's local selection intact for K3)
+  const int32_t* d_in_n;
   MergeArgs merge;       // workspace pointers; list pointers filled per step
 };
 
@@ -66,7 +69,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
 __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   MergeSmem& S = *reinterpret_cast<MergeSmem*>(dsm);
-  __shared__ uint32_t s_n;
+  __shared__ uint32_t s_n, s_hint;
   const unsigned G = gridDim.x, blk = blockIdx.x;
   // every block reads the counter before anyone advances it (block 0 does so
   // after the final grid barrier)
@@ -77,6 +80,22 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   // step so no peer hangs, but sends count = -1; receivers flag PEER_FAILED
   // and forward the poison, so every rank fails the step and K3 is skipped.
   const bool self_poison = (__ldcg(a.d_status) & GTK_DEV_NONFINITE) != 0;
+
+  if (a.in_idx) {  // acc = input list
+    uint32_t n = self_poison ? 0u : (uint32_t)__ldcg(a.d_in_n);
+    if (n > (uint32_t)a.k) n = a.k;
+    const uint32_t per = (n + G - 1) / G;
+    const uint32_t e0 = min(n, blk * per), e1 = min(n, e0 + per);
+    for (uint32_t e = e0 + threadIdx.x; e < e1; e += kMergeThreads) {
+      a.acc_idx[e] = __ldcg(a.in_idx + e);
+      a.acc_val[e] = __ldcg(a.in_val + e);
+    }
+    if (blk == 0 && threadIdx.x == 0) {
+      a.d_acc_n[0] = (int32_t)n;
+      a.d_acc_n[1] = __ldcg(a.d_in_n + 1);  // k-th key hint
+    }
+    grid_sync(&a.merge.ews->bar, G);
+  }
 
   for (int s = 0; s < a.nsteps; ++s) {
     const Step st = a.steps[s];
@@ -95,7 +114,8 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
         r_val[e] = __ldcg(a.acc_val + e);
       }
       if (blk == 0 && threadIdx.x == 0) {
-        *r_n = poisoned ? -1 : (int32_t)n;
+        r_n[0] = poisoned ? -1 : (int32_t)n;
+        r_n[1] = poisoned ? 0 : __ldcg(a.d_acc_n + 1);  // k-th key hint travels with the list
         if (a.step_counts) a.step_counts[2 * s] = (int32_t)n;
       }
       __syncthreads();
@@ -131,13 +151,15 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
         int32_t n = __ldcg((const int32_t*)slot);
         if (n < 0 && blk == 0) atomicOr(a.d_status, GTK_DEV_PEER_FAILED);
         s_n = (uint32_t)(n < 0 ? 0 : (n > a.k ? a.k : n));  // clamp (garbage after a timeout)
+        s_hint = (uint32_t)__ldcg((const int32_t*)slot + 1);
       }
       __syncthreads();
-      const uint32_t n_in = s_n;
+      const uint32_t n_in = s_n, hint_in = s_hint;
       if (blk == 0 && threadIdx.x == 0 && a.step_counts) a.step_counts[2 * s + 1] = (int32_t)n_in;
       if (st.merge) {
         uint32_t n_own = self_poison ? 0u : (uint32_t)__ldcg(a.d_acc_n);
         if (n_own > (uint32_t)a.k) n_own = a.k;
+        const uint32_t hint_own = self_poison ? 0u : (uint32_t)__ldcg(a.d_acc_n + 1);
         grid_sync(&a.merge.ews->bar, G);  // everyone has read the counts
         MergeArgs m = a.merge;
         m.a_idx = in_idx;
@@ -147,7 +169,7 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
         m.o_idx = a.acc_idx;
         m.o_val = a.acc_val;
         m.d_no = a.d_acc_n;
-        merge_device(m, n_in, n_own, G, S);
+        merge_device(m, n_in, n_own, hint_in, hint_own, G, S);
       } else {
         const uint32_t per = (n_in + G - 1) / G;
         const uint32_t e0 = min(n_in, blk * per), e1 = min(n_in, e0 + per);
@@ -155,7 +177,10 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
           a.acc_idx[e] = __ldcg(in_idx + e);
           a.acc_val[e] = __ldcg(in_val + e);
         }
-        if (blk == 0 && threadIdx.x == 0) *a.d_acc_n = (int32_t)n_in;
+        if (blk == 0 && threadIdx.x == 0) {
+          a.d_acc_n[0] = (int32_t)n_in;
+          a.d_acc_n[1] = (int32_t)hint_in;
+        }
       }
     }
     grid_sync(&a.merge.ews->bar, G);
@@ -218,7 +243,8 @@ extern "C" int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedu
                                   void* const* peer_inbox, uint64_t* const* peer_flags, uint64_t* d_epoch,
                                   int32_t* acc_idx, float* acc_val, int32_t* d_acc_n, int32_t k,
                                   uint32_t* d_status, const uint32_t* d_abort, int64_t timeout_ns,
-                                  int32_t* step_counts, void* ws, size_t ws_bytes, void* stream) {
+                                  int32_t* step_counts, const int32_t* in_idx, const float* in_val,
+                                  const int32_t* d_in_n, void* ws, size_t ws_bytes, void* stream) {
   if (P < 1 || P > kMaxRanks || rank < 0 || rank >= P || nsteps < 0 || nsteps > kMaxSteps || k < 1)
     return GTK_EINVAL;
   if (!acc_idx || !acc_val || !d_acc_n || !d_status || !ws || !d_epoch) return GTK_EINVAL;
@@ -248,6 +274,10 @@ extern "C" int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedu
   a.d_abort = (const volatile uint32_t*)d_abort;
   a.timeout_ns = timeout_ns;
   a.step_counts = step_counts;
+  if (in_idx && (!in_val || !d_in_n)) return GTK_EINVAL;
+  a.in_idx = in_idx;
+  a.in_val = in_val;
+  a.d_in_n = d_in_n;
   char* base = (char*)ws;
   a.merge = MergeArgs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, (uint32_t)k, nullptr, nullptr,
                       nullptr, (MergeCtl*)(base + L.ctl), (EngineWS*)(base + L.engine),

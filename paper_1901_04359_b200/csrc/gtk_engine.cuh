@@ -6,14 +6,16 @@
 // stable, so no sort is ever needed).
 //
 // Runs inside a cooperative kernel: G blocks, block b owning the contiguous
-// slot range [s0, s1) (ranges ascending with b).  The slice normally lives in
-// shared memory (SmemSrc), so every pass below is LDS-speed; the dense exact
-// fallback streams its slice from global memory (DenseSrc).  The k-th key tau
-// is found by radix refinement over 2049-bin histograms (2048 window bins +
-// OVER), rounds shrinking the window 2^11-fold, finishing either when a bin is
-// one key wide or when the target bin holds <= kGatherCap entries (gathered
-// and ranked by brute force).  Ties at tau are resolved in index order with a
-// grid-wide prefix of per-block equal-key counts.
+// slot range [s0, s1) (ranges ascending with b), normally staged in shared
+// memory.  The k-th key tau is located with 2049-bin histograms (2048 window
+// bins + OVER): find the bin b holding rank kt; if b is narrow enough
+// (<= kGatherCap entries, or a single key) finish with ONE grid barrier:
+//     every block counts its entries above b and gathers its entries inside b
+//     as (key, idx, block); after the barrier every block derives tau, the
+//     index-order tie ranks and its own output offset from the gathered set
+//     and the per-block counts, and writes its winners;
+// otherwise refine the window inside b (2^11-fold per round).
+// With G == 1 histograms and the gather stay in shared memory (no barriers).
 #pragma once
 
 #include "gtk_common.cuh"
@@ -24,15 +26,18 @@ constexpr int kBins = 2048;                 // window bins
 constexpr int kHistLen = kBins + 1;         // + OVER
 constexpr int kHistStride = 2056;           // padded
 constexpr int kRounds = 4;
-constexpr int kGatherCap = 1024;
+constexpr int kGatherCap = 1024;  // gather buffer size
+constexpr int kGatherMax = 384;   // gather (O(n^2) ranking) only bins this small; else refine
 constexpr int kMaxBlocks = 1024;
 
 struct EngineWS {
   GridBarrier bar;
-  uint32_t gather_n[kRounds];
+  uint32_t gather_n[kRounds];  // zeroed by the producer of the run's first histogram
   uint32_t pad0[10];
   uint32_t hist[kRounds][kHistStride];
   uint32_t gather_key[kGatherCap];
+  int32_t gather_idx[kGatherCap];
+  uint32_t gather_blk[kGatherCap];
   uint32_t cta_a[kMaxBlocks];
   uint32_t cta_b[kMaxBlocks];
 };
@@ -41,8 +46,11 @@ template <int NT>
 struct EngineSmem {
   uint32_t hist[kHistStride];
   uint32_t keys[kGatherCap];
+  int32_t gidx[kGatherCap];
+  uint32_t gblk[kGatherCap];
   uint32_t scan[NT / 32 + 2];
   uint32_t bcast[8];
+  uint32_t ng;
 };
 
 // ---- slot sources -------------------------------------------------------------
@@ -84,8 +92,9 @@ struct DenseSrc {  // dense fallback: slot s is element s
 struct Sink {
   int32_t* o_idx;
   float* o_val;
-  int32_t* d_count;
-  float* zero_at;  // select: res_out[idx] = +0.0 for kept entries (nullable)
+  int32_t* d_count;  // d_count[0] = kept entries; d_count[1] = kt-th key hint (0 = none)
+  float* zero_at;    // select: res_out[idx] = +0.0 for kept entries (nullable)
+  bool write_hint;
 };
 
 __device__ __forceinline__ void slice_of(uint32_t N, unsigned G, unsigned b, uint32_t& s0, uint32_t& s1) {
@@ -108,7 +117,7 @@ __device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t* red) {
   return t;
 }
 
-// Histogram my slice's keys in [lo, hi) into a round's global histogram.
+// Histogram my slice's keys in [lo, hi) into sm.hist; flush to ghist if given.
 template <int NT, class Src>
 __device__ void engine_hist(const Src& src, uint32_t s0, uint32_t s1, uint32_t lo, uint64_t hi,
                             uint32_t shift, uint32_t* ghist, EngineSmem<NT>& sm) {
@@ -124,17 +133,20 @@ __device__ void engine_hist(const Src& src, uint32_t s0, uint32_t s1, uint32_t l
     }
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < kHistLen; b += NT) {
-    const uint32_t c = sm.hist[b];
-    if (c) atomicAdd(ghist + b, c);
+  if (ghist) {
+    for (int b = threadIdx.x; b < kHistLen; b += NT) {
+      const uint32_t c = sm.hist[b];
+      if (c) atomicAdd(ghist + b, c);
+    }
   }
 }
 
-// Find the bin holding rank t (1-based, from the top, OVER first).  All blocks
-// compute the same answer.  Returns false if the histogram holds < t entries.
+// Find the bin holding rank t (1-based, from the top, OVER first) of a
+// histogram in global (ldcg) or shared memory.  All blocks compute the same
+// answer.  Returns false if the histogram holds < t entries.
 template <int NT>
-__device__ bool engine_find_bin(const uint32_t* ghist, uint32_t t, EngineSmem<NT>& sm, uint32_t& bin,
-                                uint32_t& above, uint32_t& in_bin, uint32_t& total) {
+__device__ bool engine_find_bin(const uint32_t* hist, bool in_smem, uint32_t t, EngineSmem<NT>& sm,
+                                uint32_t& bin, uint32_t& above, uint32_t& in_bin) {
   constexpr int PER = (kHistLen + NT - 1) / NT;
   // thread t owns reversed positions [t*PER, t*PER+PER): rb = 0 is OVER (bin 2048)
   uint32_t c[PER];
@@ -142,7 +154,7 @@ __device__ bool engine_find_bin(const uint32_t* ghist, uint32_t t, EngineSmem<NT
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     const int rb = threadIdx.x * PER + j;
-    c[j] = rb < kHistLen ? __ldcg(ghist + (kBins - rb)) : 0u;
+    c[j] = rb < kHistLen ? (in_smem ? hist[kBins - rb] : __ldcg(hist + (kBins - rb))) : 0u;
     sum += c[j];
   }
   uint32_t tot;
@@ -162,7 +174,6 @@ __device__ bool engine_find_bin(const uint32_t* ghist, uint32_t t, EngineSmem<NT
     }
   }
   __syncthreads();
-  total = tot;
   bin = sm.bcast[0];
   above = sm.bcast[1];
   in_bin = sm.bcast[2];
@@ -170,161 +181,18 @@ __device__ bool engine_find_bin(const uint32_t* ghist, uint32_t t, EngineSmem<NT
   return tot >= t && bin != 0xFFFFFFFFu;
 }
 
-// The engine proper.  Every block calls it with its own slice [s0, s1).
-// Returns false (consistently in all blocks) if the round-0 histogram holds
-// fewer than kt entries (select: fallback needed).
-//   round0_ready: ws->hist[0] already holds the slots' histogram over
-//                 [lo0, 2^31) with bin width 2^shift0 (built by the producer
-//                 and made visible by a grid barrier or kernel boundary)
-//   kt / keep_all: keep_all keeps every valid slot (kt is then ignored and the
-//                 output count is the number of valid slots).
-template <int NT, class Src>
-__device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt, bool keep_all, uint32_t lo0,
-                           uint32_t shift0, bool round0_ready, EngineWS* ws, EngineSmem<NT>& sm,
-                           const Sink& out, unsigned G) {
-  const unsigned blk = blockIdx.x;
-  uint32_t tau = 0, n_gt = 0, need = 0;
-  if (!keep_all) {
-    uint32_t lo = lo0, shift = shift0;
-    uint64_t hi = 0x80000000ull;
-    uint32_t t = kt, acc_above = 0;
-    bool done = false;
-    for (int r = 0; r < kRounds && !done; ++r) {
-      if (r > 0 || !round0_ready) {
-        engine_hist<NT>(src, s0, s1, lo, hi, shift, ws->hist[r], sm);
-        grid_sync(&ws->bar, G);
-      }
-      uint32_t bin, above, in_bin, total;
-      if (!engine_find_bin<NT>(ws->hist[r], t, sm, bin, above, in_bin, total)) return false;
-      uint64_t blo, bhi;
-      if (bin < (uint32_t)kBins) {
-        blo = (uint64_t)lo + ((uint64_t)bin << shift);
-        bhi = blo + (1ull << shift);
-        if (bhi > hi) bhi = hi;
-      } else {
-        blo = (uint64_t)lo + ((uint64_t)kBins << shift);
-        bhi = hi;
-      }
-      const uint32_t t_in = t - above;
-      if (bhi - blo == 1) {
-        tau = (uint32_t)blo;
-        n_gt = acc_above + above;
-        done = true;
-        break;
-      }
-      if (in_bin <= (uint32_t)kGatherCap) {
-        // gather the keys of the target bin, rank them by brute force
-        for (uint32_t s = s0 + threadIdx.x; s < s1; s += NT) {
-          uint32_t key;
-          int32_t i;
-          float v;
-          if (src.get(s, key, i, v) && key >= blo && key < bhi) {
-            const uint32_t p = atomicAdd(&ws->gather_n[r], 1u);
-            ws->gather_key[p] = key;
-          }
-        }
-        grid_sync(&ws->bar, G);
-        const uint32_t ng = __ldcg(&ws->gather_n[r]);
-        for (uint32_t j = threadIdx.x; j < ng; j += NT) sm.keys[j] = __ldcg(&ws->gather_key[j]);
-        __syncthreads();
-        for (uint32_t j = threadIdx.x; j < ng; j += NT) {
-          const uint32_t x = sm.keys[j];
-          uint32_t gt = 0, ge = 0;
-          for (uint32_t q = 0; q < ng; ++q) {
-            const uint32_t y = sm.keys[q];
-            gt += (y > x);
-            ge += (y >= x);
-          }
-          if (gt < t_in && ge >= t_in) {
-            sm.bcast[3] = x;
-            sm.bcast[4] = gt;
-          }
-        }
-        __syncthreads();
-        tau = sm.bcast[3];
-        n_gt = acc_above + above + sm.bcast[4];
-        __syncthreads();
-        done = true;
-        break;
-      }
-      // refine inside the target bin
-      acc_above += above;
-      t = t_in;
-      lo = (uint32_t)blo;
-      hi = bhi;
-      const uint64_t width = bhi - blo;
-      shift = width <= (uint64_t)kBins ? 0u : ceil_log2_u64((width + kBins - 1) / kBins);
-    }
-    if (!done) return false;  // unreachable: shift reaches 0 within kRounds
-    need = kt - n_gt;
-  }
-
-  // ---- compaction: per-block counts, grid prefix, stable write -------------
-  uint32_t c_a = 0, c_b = 0;  // keep_all: (valid, -)  else (gt, eq)
-  for (uint32_t s = s0 + threadIdx.x; s < s1; s += NT) {
-    uint32_t key;
-    int32_t i;
-    float v;
-    if (src.get(s, key, i, v)) {
-      if (keep_all) {
-        c_a++;
-      } else {
-        c_a += key > tau;
-        c_b += key == tau;
-      }
-    }
-  }
-  c_a = block_sum<NT>(c_a, sm.scan);
-  c_b = block_sum<NT>(c_b, sm.scan);
-  if (threadIdx.x == 0) {
-    ws->cta_a[blk] = c_a;
-    ws->cta_b[blk] = c_b;
-  }
-  grid_sync(&ws->bar, G);
-
-  // self-clean the histogram/gather state for the next engine use (every block
-  // is past its last histogram read)
-  if (blk == 0) {
-    for (int r = 0; r < kRounds; ++r)
-      for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[r][b] = 0;
-    if (threadIdx.x < kRounds) ws->gather_n[threadIdx.x] = 0;
-  }
-
-  uint32_t a_before = 0, b_before = 0, a_all = 0;
-  for (unsigned j = threadIdx.x; j < G; j += NT) {
-    const uint32_t a = __ldcg(&ws->cta_a[j]);
-    const uint32_t b = __ldcg(&ws->cta_b[j]);
-    if (j < blk) {
-      a_before += a;
-      b_before += b;
-    }
-    a_all += a;
-  }
-  a_before = block_sum<NT>(a_before, sm.scan);
-  b_before = block_sum<NT>(b_before, sm.scan);
-  a_all = block_sum<NT>(a_all, sm.scan);
-
-  uint32_t out_pos = keep_all ? a_before : a_before + min(b_before, need);
-  uint32_t eq_seen = b_before;
+// Stable index-order write of my slice's kept entries at out_pos.. .
+// keep(key, idx) decides; returns nothing (positions via block scans).
+template <int NT, class Src, class Keep>
+__device__ void engine_write(const Src& src, uint32_t s0, uint32_t s1, uint32_t out_pos, const Keep& keep_fn,
+                             EngineSmem<NT>& sm, const Sink& out) {
   for (uint32_t base = s0; base < s1; base += NT) {
     const uint32_t s = base + threadIdx.x;
     uint32_t key = 0;
     int32_t i = 0;
     float v = 0.f;
-    bool valid = false;
-    if (s < s1) valid = src.get(s, key, i, v);
-    bool keep;
-    uint32_t is_eq = 0;
-    if (keep_all) {
-      keep = valid;
-    } else {
-      is_eq = valid && key == tau;
-      keep = valid && key > tau;
-    }
-    uint32_t eq_tot = 0;
-    uint32_t eq_rank = 0;
-    if (!keep_all) eq_rank = block_excl_scan<NT>(is_eq, sm.scan, &eq_tot);
-    if (is_eq && eq_seen + eq_rank < need) keep = true;
+    bool keep = false;
+    if (s < s1 && src.get(s, key, i, v)) keep = keep_fn(key, i);
     uint32_t k_tot;
     const uint32_t k_rank = block_excl_scan<NT>(keep ? 1u : 0u, sm.scan, &k_tot);
     if (keep) {
@@ -334,10 +202,249 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       if (out.zero_at) out.zero_at[i] = 0.0f;
     }
     out_pos += k_tot;
-    eq_seen += eq_tot;
   }
-  if (blk == 0 && threadIdx.x == 0) *out.d_count = (int32_t)(keep_all ? a_all : kt);
-  return true;
+}
+
+// The engine proper.  Every block calls it with its own slice [s0, s1).
+// hist0: the round-0 histogram over [lo0, 2^31) with bin width 2^shift0,
+//        already complete (global: built before a grid barrier / by an earlier
+//        kernel; with G == 1 it may live in sm.hist: hist0_smem), or nullptr to
+//        build it here.
+// Returns false (consistently in all blocks) if round 0 holds fewer than kt
+// entries (select: fallback needed; merge: widen the window).
+// keep_all keeps every valid slot (kt = number of valid slots).
+template <int NT, class Src>
+__device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt, bool keep_all, uint32_t lo0,
+                           uint32_t shift0, const uint32_t* hist0, bool hist0_smem, EngineWS* ws,
+                           EngineSmem<NT>& sm, const Sink& out, unsigned G) {
+  const unsigned blk = blockIdx.x;
+  const bool solo = G == 1;
+
+  if (keep_all) {
+    uint32_t c = 0;
+    for (uint32_t s = s0 + threadIdx.x; s < s1; s += NT) {
+      uint32_t key;
+      int32_t i;
+      float v;
+      c += src.get(s, key, i, v) ? 1u : 0u;
+    }
+    c = block_sum<NT>(c, sm.scan);
+    uint32_t before = 0;
+    if (!solo) {
+      if (threadIdx.x == 0) ws->cta_a[blk] = c;
+      grid_sync(&ws->bar, G);
+      for (unsigned j = threadIdx.x; j < blk; j += NT) before += __ldcg(&ws->cta_a[j]);
+      before = block_sum<NT>(before, sm.scan);
+    }
+    engine_write<NT>(src, s0, s1, before, [](uint32_t, int32_t) { return true; }, sm, out);
+    if (blk == 0) {
+      for (int r = 0; r < kRounds; ++r)
+        for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[r][b] = 0;
+      if (threadIdx.x == 0) {
+        out.d_count[0] = (int32_t)kt;
+        if (out.write_hint) out.d_count[1] = 0;
+      }
+    }
+    return true;
+  }
+
+  uint32_t lo = lo0, shift = shift0;
+  uint64_t hi = 0x80000000ull;
+  uint32_t t = kt;
+  const uint32_t* hist = hist0;
+  bool hsm = hist0_smem;
+  for (int r = 0; r < kRounds; ++r) {
+    if (hist == nullptr) {
+      engine_hist<NT>(src, s0, s1, lo, hi, shift, solo ? nullptr : ws->hist[r], sm);
+      if (!solo) grid_sync(&ws->bar, G);
+      hist = solo ? sm.hist : ws->hist[r];
+      hsm = solo;
+    }
+    uint32_t bin, above, in_bin;
+    if (!engine_find_bin<NT>(hist, hsm, t, sm, bin, above, in_bin)) return false;
+    uint64_t blo, bhi;
+    if (bin < (uint32_t)kBins) {
+      blo = (uint64_t)lo + ((uint64_t)bin << shift);
+      bhi = blo + (1ull << shift);
+      if (bhi > hi) bhi = hi;
+    } else {
+      blo = (uint64_t)lo + ((uint64_t)kBins << shift);
+      bhi = hi;
+    }
+    const uint32_t t_in = t - above;  // rank of the target inside the bin
+    const bool single_key = (bhi - blo == 1);
+    // the last round always gathers if it can (a bin is then at most 8 keys wide)
+    if (in_bin <= (uint32_t)kGatherMax || (in_bin <= (uint32_t)kGatherCap && (r == kRounds - 1 || shift <= 3))) {
+      // ---- finish with one barrier: gather (key, idx, block) of the bin ------
+      uint32_t n_above = 0;
+      if (solo && threadIdx.x == 0) sm.ng = 0;
+      if (solo) __syncthreads();
+      for (uint32_t s = s0 + threadIdx.x; s < s1; s += NT) {
+        uint32_t key;
+        int32_t i;
+        float v;
+        if (!src.get(s, key, i, v)) continue;
+        if ((uint64_t)key >= bhi) {
+          ++n_above;
+        } else if (key >= blo) {
+          if (solo) {
+            const uint32_t p = atomicAdd(&sm.ng, 1u);
+            sm.keys[p] = key;
+            sm.gidx[p] = i;
+            sm.gblk[p] = blk;
+          } else {
+            const uint32_t p = atomicAdd(&ws->gather_n[r], 1u);
+            ws->gather_key[p] = key;
+            ws->gather_idx[p] = i;
+            ws->gather_blk[p] = blk;
+          }
+        }
+      }
+      n_above = block_sum<NT>(n_above, sm.scan);
+      uint32_t above_before = 0;
+      if (!solo) {
+        if (threadIdx.x == 0) ws->cta_a[blk] = n_above;
+        grid_sync(&ws->bar, G);
+        const uint32_t ng = __ldcg(&ws->gather_n[r]);
+        for (uint32_t j = threadIdx.x; j < ng; j += NT) {
+          sm.keys[j] = __ldcg(&ws->gather_key[j]);
+          sm.gidx[j] = __ldcg(&ws->gather_idx[j]);
+          sm.gblk[j] = __ldcg(&ws->gather_blk[j]);
+        }
+        for (unsigned j = threadIdx.x; j < blk; j += NT) above_before += __ldcg(&ws->cta_a[j]);
+        if (threadIdx.x == 0) sm.ng = ng;
+      }
+      above_before = block_sum<NT>(above_before, sm.scan);  // also publishes sm.keys / sm.ng
+      const uint32_t ng = sm.ng;
+      // tau = t_in-th largest gathered key; gt = # gathered keys > tau
+      if (threadIdx.x == 0) sm.bcast[3] = sm.bcast[4] = 0;
+      __syncthreads();
+      for (uint32_t j = threadIdx.x; j < ng; j += NT) {
+        const uint32_t x = sm.keys[j];
+        uint32_t gt = 0, ge = 0;
+        for (uint32_t q = 0; q < ng; ++q) {
+          const uint32_t y = sm.keys[q];
+          gt += (y > x);
+          ge += (y >= x);
+        }
+        if (gt < t_in && ge >= t_in) {
+          sm.bcast[3] = x;
+          sm.bcast[4] = gt;
+        }
+      }
+      __syncthreads();
+      const uint32_t tau = sm.bcast[3];
+      const uint32_t need = t_in - sm.bcast[4];  // entries with key == tau to keep, lowest idx first
+      // kept flags of the gathered entries (reuse gblk's top bit), my offset
+      uint32_t extra = 0;
+      for (uint32_t j = threadIdx.x; j < ng; j += NT) {
+        const uint32_t x = sm.keys[j];
+        bool kept = x > tau;
+        if (x == tau) {
+          uint32_t rank = 0;
+          const int32_t ij = sm.gidx[j];
+          for (uint32_t q = 0; q < ng; ++q) rank += (sm.keys[q] == tau && sm.gidx[q] < ij);
+          kept = rank < need;
+        }
+        if (kept) {
+          sm.gblk[j] |= 0x80000000u;
+          if ((sm.gblk[j] & 0x7FFFFFFFu) < blk) ++extra;
+        }
+      }
+      extra = block_sum<NT>(extra, sm.scan);
+      const uint32_t bl = (uint32_t)blo, bh32 = (uint32_t)min(bhi, (uint64_t)0xFFFFFFFFu);
+      const bool bh_max = bhi > 0xFFFFFFFFull;
+      auto keep_fn = [&](uint32_t key, int32_t i) -> bool {
+        if (!bh_max && key >= bh32) return true;
+        if (key < bl) return false;
+        for (uint32_t q = 0; q < ng; ++q)
+          if (sm.gidx[q] == i) return (sm.gblk[q] & 0x80000000u) != 0;
+        return false;
+      };
+      engine_write<NT>(src, s0, s1, above_before + extra, keep_fn, sm, out);
+      if (blk == 0) {  // every block is past its last histogram read
+        for (int rr = 0; rr < kRounds; ++rr)
+          for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[rr][b] = 0;
+        if (threadIdx.x == 0) {
+          out.d_count[0] = (int32_t)kt;
+          if (out.write_hint) out.d_count[1] = (int32_t)tau;
+        }
+      }
+      return true;
+    }
+    if (single_key) {
+      // ---- massive tie on one key: per-block gt/eq counts, one barrier -------
+      const uint32_t tau = (uint32_t)blo;
+      const uint32_t need = t_in;
+      uint32_t c_gt = 0, c_eq = 0;
+      for (uint32_t s = s0 + threadIdx.x; s < s1; s += NT) {
+        uint32_t key;
+        int32_t i;
+        float v;
+        if (src.get(s, key, i, v)) {
+          c_gt += key > tau;
+          c_eq += key == tau;
+        }
+      }
+      c_gt = block_sum<NT>(c_gt, sm.scan);
+      c_eq = block_sum<NT>(c_eq, sm.scan);
+      uint32_t gt_before = 0, eq_before = 0;
+      if (!solo) {
+        if (threadIdx.x == 0) {
+          ws->cta_a[blk] = c_gt;
+          ws->cta_b[blk] = c_eq;
+        }
+        grid_sync(&ws->bar, G);
+        for (unsigned j = threadIdx.x; j < blk; j += NT) {
+          gt_before += __ldcg(&ws->cta_a[j]);
+          eq_before += __ldcg(&ws->cta_b[j]);
+        }
+        gt_before = block_sum<NT>(gt_before, sm.scan);
+        eq_before = block_sum<NT>(eq_before, sm.scan);
+      }
+      uint32_t out_pos = gt_before + min(eq_before, need);
+      uint32_t eq_seen = eq_before;
+      for (uint32_t base = s0; base < s1; base += NT) {
+        const uint32_t s = base + threadIdx.x;
+        uint32_t key = 0;
+        int32_t i = 0;
+        float v = 0.f;
+        const bool valid = s < s1 && src.get(s, key, i, v);
+        const uint32_t is_eq = valid && key == tau;
+        bool keep = valid && key > tau;
+        uint32_t eq_tot;
+        const uint32_t eq_rank = block_excl_scan<NT>(is_eq, sm.scan, &eq_tot);
+        if (is_eq && eq_seen + eq_rank < need) keep = true;
+        uint32_t k_tot;
+        const uint32_t k_rank = block_excl_scan<NT>(keep ? 1u : 0u, sm.scan, &k_tot);
+        if (keep) {
+          const uint32_t p = out_pos + k_rank;
+          out.o_idx[p] = i;
+          out.o_val[p] = v;
+          if (out.zero_at) out.zero_at[i] = 0.0f;
+        }
+        out_pos += k_tot;
+        eq_seen += eq_tot;
+      }
+      if (blk == 0) {
+        for (int rr = 0; rr < kRounds; ++rr)
+          for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[rr][b] = 0;
+        if (threadIdx.x == 0) {
+          out.d_count[0] = (int32_t)kt;
+          if (out.write_hint) out.d_count[1] = (int32_t)tau;
+        }
+      }
+      return true;
+    }
+    // ---- refine inside the target bin ------------------------------------------
+    t = t_in;
+    lo = (uint32_t)blo;
+    hi = bhi;
+    const uint64_t width = bhi - blo;
+    shift = width <= (uint64_t)kBins ? 0u : ceil_log2_u64((width + kBins - 1) / kBins);
+    hist = nullptr;
+  }
+  return false;  // unreachable: a bin is one key wide after kRounds
 }
 
 }  // namespace gtk

@@ -11,7 +11,8 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   MergeSmem& S = *reinterpret_cast<MergeSmem*>(dsm);
   const uint32_t na = (uint32_t)__ldcg(a.d_na), nb = (uint32_t)__ldcg(a.d_nb);
-  merge_device(a, na, nb, gridDim.x, S);
+  const uint32_t ha = (uint32_t)__ldcg(a.d_na + 1), hb = (uint32_t)__ldcg(a.d_nb + 1);
+  merge_device(a, na, nb, ha, hb, gridDim.x, S);
 }
 
 // blocks for a merge of two lists of <= cap entries: ~2K merged slots per

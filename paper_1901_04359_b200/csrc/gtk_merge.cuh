@@ -135,19 +135,36 @@ static __device__ __forceinline__ uint32_t upper_bound_s(const int32_t* s, uint3
   return lo;
 }
 
-// na/nb are passed by value: the caller read them before any output write.
-static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t na, uint32_t nb, unsigned G,
-                                                    MergeSmem& S) {
+// Window of the round-0 histogram from the inputs' k-th-key hints: a list with
+// k entries has all of them >= its hint, so (cancellations aside) the union
+// has >= k entries >= max(hint); 2048 linear bins over the 2 octaves above it
+// (sums of correlated ranks' entries can double a value: +1 octave) isolate
+// the k-th key in one round.  A miss (cancellation on shared indices) falls
+// back to the full key range.
+constexpr uint32_t kMergeWinShift = 13;  // 2048 << 13 = 2^24 keys = 2 octaves
+
+// na/nb and the hints are passed by value: the caller read them before any
+// output write.
+static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t na, uint32_t nb, uint32_t hint_a,
+                                                    uint32_t hint_b, unsigned G, MergeSmem& S) {
   EngineSmem<kMergeThreads>& esm = S.esm;
   const unsigned blk = blockIdx.x;
   const uint32_t N = na + nb;
   if (N == 0) {
-    if (blk == 0 && threadIdx.x == 0) *a.d_no = 0;
+    if (blk == 0 && threadIdx.x == 0) {
+      a.d_no[0] = 0;
+      a.d_no[1] = 0;
+    }
     grid_sync(&a.ews->bar, G);  // callers may reuse the inputs right after
     return;
   }
+  uint32_t win_lo = 0;
+  if (na >= a.k && hint_a < kInfKey) win_lo = max(win_lo, hint_a);
+  if (nb >= a.k && hint_b < kInfKey) win_lo = max(win_lo, hint_b);
+  const uint32_t win_shift = win_lo ? kMergeWinShift : 20u;
   for (int b = threadIdx.x; b < kHistLen; b += kMergeThreads) esm.hist[b] = 0;
   if (threadIdx.x == 0) S.s_valid = 0;
+  if (blk == 0 && threadIdx.x < kRounds) a.ews->gather_n[threadIdx.x] = 0;  // read only after a barrier
 
   uint32_t d0, d1;
   slice_of(N, G, blk, d0, d1);
@@ -199,7 +216,8 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
       }
       if (valid) {
         ++my_valid;
-        atomicAdd(&esm.hist[merge_key_of(v) >> 20], 1u);
+        const uint32_t key = merge_key_of(v);
+        if (key >= win_lo) atomicAdd(&esm.hist[min((uint32_t)kBins, (key - win_lo) >> win_shift)], 1u);
       }
     }
     for (uint32_t t = threadIdx.x; t < lb; t += kMergeThreads) {
@@ -218,7 +236,8 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
       }
       if (valid) {
         ++my_valid;
-        atomicAdd(&esm.hist[merge_key_of(v) >> 20], 1u);
+        const uint32_t key = merge_key_of(v);
+        if (key >= win_lo) atomicAdd(&esm.hist[min((uint32_t)kBins, (key - win_lo) >> win_shift)], 1u);
       }
     }
     __syncthreads();
@@ -226,20 +245,39 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   my_valid = warp_sum(my_valid);
   if (lane_id() == 0 && my_valid) atomicAdd(&S.s_valid, my_valid);
   __syncthreads();
-  for (int b = threadIdx.x; b < kHistLen; b += kMergeThreads) {
-    const uint32_t c = esm.hist[b];
-    if (c) atomicAdd(&a.ews->hist[0][b], c);
+  const bool solo = G == 1;
+  uint32_t n_valid;
+  if (solo) {
+    n_valid = S.s_valid;  // the histogram stays in shared memory
+  } else {
+    for (int b = threadIdx.x; b < kHistLen; b += kMergeThreads) {
+      const uint32_t c = esm.hist[b];
+      if (c) atomicAdd(&a.ews->hist[0][b], c);
+    }
+    if (threadIdx.x == 0 && S.s_valid) atomicAdd(&a.ctl->n_valid, S.s_valid);
+    grid_sync(&a.ews->bar, G);
+    n_valid = __ldcg(&a.ctl->n_valid);
   }
-  if (threadIdx.x == 0 && S.s_valid) atomicAdd(&a.ctl->n_valid, S.s_valid);
-  grid_sync(&a.ews->bar, G);
-
-  const uint32_t n_valid = __ldcg(&a.ctl->n_valid);
   const bool keep_all = n_valid <= a.k;
   const SliceSrc src{S.slice_idx, S.slice_val, a.u_idx, a.u_val, d0, in_smem, true};
-  const Sink out{a.o_idx, a.o_val, a.d_no, nullptr};
-  engine_run<kMergeThreads>(src, d0, d1, keep_all ? n_valid : a.k, keep_all, 0u, 20u, true, a.ews, esm, out, G);
+  const Sink out{a.o_idx, a.o_val, a.d_no, nullptr, true};
+  const uint32_t* h0 = solo ? esm.hist : a.ews->hist[0];
+  bool ok = engine_run<kMergeThreads>(src, d0, d1, keep_all ? n_valid : a.k, keep_all, win_lo, win_shift, h0, solo,
+                                      a.ews, esm, out, G);
+  if (!ok) {  // the hint window missed (cancellation): full key range
+    if (!solo) {
+      grid_sync(&a.ews->bar, G);
+      if (blk == 0) {
+        for (int r = 0; r < kRounds; ++r)
+          for (int b = threadIdx.x; b < kHistLen; b += kMergeThreads) a.ews->hist[r][b] = 0;
+        if (threadIdx.x < kRounds) a.ews->gather_n[threadIdx.x] = 0;
+      }
+      grid_sync(&a.ews->bar, G);
+    }
+    engine_run<kMergeThreads>(src, d0, d1, a.k, false, 0u, 20u, nullptr, false, a.ews, esm, out, G);
+  }
   // every block read n_valid before the engine's first barrier
-  if (blk == 0 && threadIdx.x == 0) a.ctl->n_valid = 0;
+  if (!solo && blk == 0 && threadIdx.x == 0) a.ctl->n_valid = 0;
 }
 
 }  // namespace gtk

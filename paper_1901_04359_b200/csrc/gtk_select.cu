@@ -179,6 +179,7 @@ struct WindowArgs {
   SelectCtl* ctl;
   uint32_t* hist;
   uint32_t* coarse;
+  EngineWS* ews;
 };
 
 __global__ void __launch_bounds__(kSampleThreads) select_window_kernel(WindowArgs a) {
@@ -240,6 +241,10 @@ __global__ void __launch_bounds__(kSampleThreads) select_window_kernel(WindowArg
     ctl->ovf_cursor = 0;
     ctl->overflow = 0;
     ctl->nonfinite = 0;
+  }
+  if (threadIdx.x < kRounds) {  // the finish engine's gather counters (read only after its barrier)
+    EngineWS* ews = a.ews;
+    ews->gather_n[threadIdx.x] = 0;
   }
 }
 
@@ -442,12 +447,12 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
     }
     return;
   }
-  const Sink out{a.sel_idx, a.sel_val, a.d_count, a.res_out};
+  const Sink out{a.sel_idx, a.sel_val, a.d_count, a.res_out, true};
 
   // my tile range and its place in the global (index-ordered) candidate list
   const uint32_t per = (a.ntiles + G - 1) / G;
   const uint32_t t0 = min(a.ntiles, blk * per), t1 = min(a.ntiles, t0 + per);
-  uint32_t before = 0, all = 0;
+  uint32_t before = 0, all = 0, own = 0;
   // tile_info is padded to a multiple of 4 with zeros: 128-bit loads
   const uint32_t n4 = (a.ntiles + 3) / 4;
 #pragma unroll 4
@@ -456,18 +461,18 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
     const uint32_t c[4] = {q.x & ~kOvfBit, q.y & ~kOvfBit, q.z & ~kOvfBit, q.w & ~kOvfBit};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
+      const uint32_t t = 4 * t4 + j;
       all += c[j];
-      before += (4 * t4 + j) < t0 ? c[j] : 0u;
+      before += t < t0 ? c[j] : 0u;
+      own += (t >= t0 && t < t1) ? c[j] : 0u;
     }
   }
   before = block_sum<kFinishThreads>(before, sm.scan);
+  own = block_sum<kFinishThreads>(own, sm.scan);
   const uint32_t C = block_sum<kFinishThreads>(all, sm.scan);
   const bool overflow = __ldcg(&a.ctl->overflow) != 0;
   if (!overflow && C >= a.k && C <= a.ord_cap) {
-    // own count, then copy my tiles' candidates into my slice (smem if it fits)
-    uint32_t own = 0;
-    for (uint32_t t = t0 + threadIdx.x; t < t1; t += kFinishThreads) own += __ldcg(a.tile_info + t) & ~kOvfBit;
-    own = block_sum<kFinishThreads>(own, sm.scan);
+    // copy my tiles' candidates into my slice (smem if it fits)
     const bool in_smem = own <= (uint32_t)kSliceCap;
     int32_t* di = in_smem ? s_idx : a.ord_idx + before;
     float* dv = in_smem ? s_val : a.ord_val + before;
@@ -516,7 +521,7 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
     }
     SliceSrc src{s_idx, s_val, a.ord_idx, a.ord_val, before, in_smem, false};
     if (engine_run<kFinishThreads>(src, before, before + own, a.k, false, __ldcg(&a.ctl->lo),
-                                   __ldcg(&a.ctl->shift), true, a.ews, sm, out, G))
+                                   __ldcg(&a.ctl->shift), a.ews->hist[0], false, a.ews, sm, out, G))
       return;
   }
   // exact dense fallback over acc (= res_out, untouched so far)
@@ -531,7 +536,7 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
   DenseSrc dsrc{a.res_out};
   uint32_t s0, s1;
   slice_of(a.m, G, blk, s0, s1);
-  engine_run<kFinishThreads>(dsrc, s0, s1, a.k, false, 0u, 20u, false, a.ews, sm, out, G);
+  engine_run<kFinishThreads>(dsrc, s0, s1, a.k, false, 0u, 20u, nullptr, false, a.ews, sm, out, G);
 }
 
 }  // namespace gtk
@@ -585,7 +590,7 @@ extern "C" int gtk_select(const float* res_in, const float* grad, float* res_out
   select_sample_kernel<<<nchunks, kSampleThreads, 0, st>>>(sa);
   GTK_CHECK_LAUNCH();
   WindowArgs wa{r_lo, r_hi, (uint32_t)((flags & GTK_SELECT_FORCE_EXACT) ? 1 : 0), ctl, shist,
-                shist + kSampleBins};
+                shist + kSampleBins, ews};
   select_window_kernel<<<1, kSampleThreads, 0, st>>>(wa);
   GTK_CHECK_LAUNCH();
 

@@ -54,7 +54,9 @@ class DeviceList:
         self.device = device
         self.idx = torch.empty(self.cap, dtype=torch.int32, device=device)
         self.val = torch.empty(self.cap, dtype=torch.float32, device=device)
-        self.count = torch.zeros(1, dtype=torch.int32, device=device)
+        # {count, k-th key hint (0 = unknown)}: the hint lets a later merge
+        # histogram a narrow key window in a single round
+        self.count = torch.zeros(2, dtype=torch.int32, device=device)
 
     @classmethod
     def from_host(cls, dim, indices, values, device, cap=None) -> "DeviceList":
@@ -64,11 +66,17 @@ class DeviceList:
         if n:
             lst.idx[:n].copy_(torch.from_numpy(indices.astype(np.int32)), non_blocking=False)
             lst.val[:n].copy_(torch.from_numpy(np.asarray(values, dtype=F32)), non_blocking=False)
-        lst.count.fill_(n)
+        lst.count[0] = n
+        lst.count[1] = 0
         return lst
 
+    @property
+    def n(self) -> torch.Tensor:
+        """The 1-element device count (view)."""
+        return self.count[0:1]
+
     def nnz(self) -> int:
-        return int(self.count.item())
+        return int(self.count[0].item())
 
     def to_host(self):
         n = self.nnz()

@@ -129,19 +129,14 @@ class DistDeviceGroup:
         if self.aborted:
             raise TransportError("cluster aborted")
         plan = self.plan(k, lst.dim)
-        if lst is not plan.acc:
-            plan.acc.copy_from(lst)
         if self.world == 1:
+            if lst is not plan.acc:
+                plan.acc.copy_from(lst)
             return plan.acc
         st = status if status is not None else plan.status
         if status is None:
             st.zero_()
-        _lib.call(
-            "gtk_gtopk_exchange", self.rank, self.world, plan.schedule, plan.nsteps, plan.peer_inbox,
-            plan.peer_flags, P(plan.epoch), P(plan.acc.idx), P(plan.acc.val), P(plan.acc.count),
-            k, P(st), None, ctypes.c_int64(int(self.timeout * 1e9)), P(plan.step_counts), P(plan.ws),
-            ctypes.c_size_t(plan.ws.numel()), _dev.stream_of(self.device),
-        )
+        self.enqueue_exchange(plan, lst, st)
         counts = plan.step_counts.clone()  # snapshot for lazy byte accounting
         for j, (s, r, _mg) in enumerate(plan.steps):
             if s >= 0:
@@ -153,11 +148,24 @@ class DistDeviceGroup:
             _dev.raise_status(word)
         return plan.acc
 
+    def enqueue_exchange(self, plan: _ExchangePlan, lst: DeviceList, status: torch.Tensor) -> None:
+        """Launch the fused exchange kernel on the current stream: plan.acc
+        becomes the global top-k of every rank's `lst`.  No host sync; the
+        launch is CUDA-graph capturable (device-side epoch)."""
+        src = None if lst is plan.acc else lst
+        _lib.call(
+            "gtk_gtopk_exchange", self.rank, self.world, plan.schedule, plan.nsteps, plan.peer_inbox,
+            plan.peer_flags, P(plan.epoch), P(plan.acc.idx), P(plan.acc.val), P(plan.acc.count),
+            plan.k, P(status), None, ctypes.c_int64(int(self.timeout * 1e9)), P(plan.step_counts),
+            P(src.idx if src else None), P(src.val if src else None), P(src.count if src else None),
+            P(plan.ws), ctypes.c_size_t(plan.ws.numel()), _dev.stream_of(self.device),
+        )
+
     # -- TopKAllReduce baseline: NCCL allgather + rank-order accumulation -----
     def topk(self, ep: Endpoint, lst: DeviceList, divide: bool = True) -> torch.Tensor:
         W = self.world
         cnts = torch.empty(W, dtype=torch.int32, device=self.device)
-        dist.all_gather_into_tensor(cnts, lst.count)
+        dist.all_gather_into_tensor(cnts, lst.n)
         cap = max(int(cnts.max().item()), 1)
         idx = torch.zeros(W * cap, dtype=torch.int32, device=self.device)
         val = torch.zeros(W * cap, dtype=torch.float32, device=self.device)
@@ -210,12 +218,16 @@ class DistEndpoint(Endpoint):
         self._gloo = gloo
 
     def _send_impl(self, dest, tag, payload):
+        # non-blocking like the reference's queue put (transport.py:255-258):
+        # gloo's blocking send would deadlock the dissemination barrier
         if self.group is not None and self.group.aborted:
             raise TransportError("endpoint aborted")
+        self._pending = [(w, keep) for w, keep in getattr(self, "_pending", []) if not w.is_completed()]
         n = torch.tensor([len(payload)], dtype=torch.int64)
-        dist.send(n, dest, group=self._gloo, tag=tag)
+        self._pending.append((dist.isend(n, dest, group=self._gloo, tag=tag), n))
         if len(payload):
-            dist.send(torch.frombuffer(bytearray(payload), dtype=torch.uint8), dest, group=self._gloo, tag=tag)
+            buf = torch.frombuffer(bytearray(payload), dtype=torch.uint8)
+            self._pending.append((dist.isend(buf, dest, group=self._gloo, tag=tag), buf))
 
     def _recv_impl(self, source, tag):
         n = torch.zeros(1, dtype=torch.int64)
@@ -231,6 +243,9 @@ class DistEndpoint(Endpoint):
             self.group.abort()
 
     def close(self):
+        for w, _keep in getattr(self, "_pending", []):
+            w.wait()
+        self._pending = []
         if self.group is not None and hasattr(self.group, "close"):
             self.group.close()
 

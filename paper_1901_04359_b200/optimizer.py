@@ -73,6 +73,7 @@ class OptimizerState:
                 torch.from_numpy(as_dense(residual).copy()).to(self._dev)
             if self._res.numel() != self._w.numel():
                 raise ValueError("residual dim must match weights dim")
+            self._res2 = torch.empty_like(self._res)
             if velocity is not None:
                 self._vel = velocity if _is_cuda(velocity) else torch.from_numpy(as_dense(velocity).copy()).to(self._dev)
         else:
@@ -225,11 +226,14 @@ class StepReport:
 
 
 def _grad_to_device(grad, device) -> torch.Tensor:
-    if _is_cuda(grad):
+    if isinstance(grad, torch.Tensor):
         if grad.dim() != 1:
             raise ValueError(f"dense vector must be 1-D, got shape {tuple(grad.shape)}")
         g = grad.to(torch.float32)
-        return g if g.device == device else g.to(device)
+        if g.device == device:
+            return g
+        # host tensor: async H2D when pinned (stream-ordered before K1)
+        return g.to(device, non_blocking=g.is_pinned())
     g = as_dense(grad)
     return torch.from_numpy(np.ascontiguousarray(g)).to(device, non_blocking=False)
 
@@ -307,7 +311,7 @@ def gtopk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float =
         lost_mass, divergence = _divergence(ep, sel, glist, k, state.m)
     _dev.scatter_update(state._w, state._res2, state._vel, glist, sel, state.m, float(np.float32(state.lr)),
                         float(np.float32(state.momentum)), P, _scaling_code(state), skip=status[0:1])
-    word, gnnz = _finish(status, glist.count)
+    word, gnnz = _finish(status, glist.n)
     _dev.raise_status(word)
     state._commit(swap_residual=True)
     return StepReport(loss=loss, t_compute_ms=t_compute_ms, t_compress_ms=tm.ms(0, 1),
@@ -334,7 +338,7 @@ def topk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float = 
     averaged = _coll.topk_allreduce(ep, DeviceSparseVector(sel), P)
     tm.mark(2)
     _dense_update(state, averaged)
-    word, nnz = _finish(status, sel.count)
+    word, nnz = _finish(status, sel.n)
     _dev.raise_status(word)
     state._commit(swap_residual=True)
     return StepReport(loss=loss, t_compute_ms=t_compute_ms, t_compress_ms=tm.ms(0, 1),
@@ -430,7 +434,7 @@ def gtopk_naive_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: f
     scaling = 1 if state.update_scaling == "average" else 2
     _dev.scatter_update(state._w, state._res2, state._vel, gsel, sel, state.m, float(np.float32(state.lr)),
                         float(np.float32(state.momentum)), P, scaling, skip=status[0:1])
-    word, nnz = _finish(status, gsel.count)
+    word, nnz = _finish(status, gsel.n)
     _dev.raise_status(word)
     state._commit(swap_residual=True)
     return StepReport(loss=loss, t_compute_ms=t_compute_ms, t_compress_ms=tm.ms(0, 1),

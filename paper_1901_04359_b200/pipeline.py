@@ -1,0 +1,158 @@
+"""Device-resident gTop-k S-SGD step for one rank, replayed from CUDA graphs.
+
+`gtopk_step` (optimizer.py) is the reference-compatible API: one call per
+step, one 8-byte status/count read per step.  `GTopKPipeline` is the same
+hot path -- K1 select -> gTopKAllReduce -> K3 update, the identical kernels --
+for a training loop that keeps gradients in HBM: the step is captured once
+per residual parity into a CUDA graph and replayed with no host work; the
+device status word is sticky (an error in any step makes every later K3 a
+no-op) and is raised by `check()`.
+
+The graph-capturability comes from the kernels keeping all per-call state on
+the device (select workspace counters, the exchange's epoch counter).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import device as _dev
+from .device import DeviceList
+
+
+class GTopKPipeline:
+    """gtopk_step for fixed (state, k, P, gradient buffers), graph-replayed.
+
+    grads: list of device gradient tensors; step t reads grads[t % len(grads)].
+    The residual alternates between the state's two buffers (parity t % 2),
+    so len(grads) must be 1 or 2 for a graph per parity."""
+
+    def __init__(self, ep, state, k: int, grads, use_graph: bool = True):
+        from .optimizer import _scaling_code
+
+        self.ep = ep
+        self.group = ep.group
+        self.P = ep.world_size
+        self.dev = self.group.device
+        state.to_device(self.dev)
+        state._ensure_velocity()
+        self.state = state
+        self.m = state.m
+        self.k = int(k)
+        if not 1 <= self.k <= self.m:
+            raise ValueError(f"k must be in [1, {self.m}], got {k}")
+        if len(grads) not in (1, 2):
+            raise ValueError("one or two gradient buffers")
+        for g in grads:
+            if not (g.is_cuda and g.device == self.dev and g.numel() == self.m and g.dtype == torch.float32):
+                raise ValueError("gradients must be float32 tensors of the state's size on its device")
+        self.grads = [g.contiguous() for g in grads]
+        self.res = [state._res, state._res2]
+        self.sel = DeviceList(self.m, self.k, self.dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.lr = float(np.float32(state.lr))
+        self.mom = float(np.float32(state.momentum))
+        self.scaling = _scaling_code(state)
+        self.plan = None
+        if self.P > 1:
+            if not hasattr(self.group, "enqueue_exchange"):
+                raise TypeError("GTopKPipeline with P > 1 needs one process per GPU (init_dist_cluster)")
+            self.plan = self.group.plan(self.k, self.m)
+        self.t = 0
+        self.graphs = None
+        self.kernels_per_step = None
+        self.use_graph = use_graph
+
+    # -- one step's launches (current stream) --------------------------------
+    def _enqueue(self, parity: int) -> None:
+        grad = self.grads[parity % len(self.grads)]
+        res_in, res_out = self.res[parity], self.res[1 - parity]
+        _dev.select(res_in, grad, res_out, self.k, self.sel, self.status)
+        if self.P > 1:
+            self.group.enqueue_exchange(self.plan, self.sel, self.status)
+            glist = self.plan.acc
+        else:
+            glist = self.sel
+        _dev.scatter_update(self.state._w, res_out, self.state._vel, glist, self.sel, self.m, self.lr, self.mom,
+                            self.P, self.scaling, skip=self.status)
+
+    def capture(self) -> None:
+        """Warm the workspaces with two eager steps, then capture one graph per
+        residual parity."""
+        for _ in range(2):
+            self.step_eager()
+        torch.cuda.synchronize(self.dev)
+        stream = torch.cuda.Stream(self.dev)
+        graphs = []
+        n0 = _lib.load().gtk_launch_count()
+        for parity in (0, 1):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                self._enqueue(parity)
+            graphs.append(g)
+        self.kernels_per_step = (_lib.load().gtk_launch_count() - n0) // 2
+        self.graphs = graphs
+        torch.cuda.synchronize(self.dev)
+
+    def profile(self, replays: int = 20) -> dict:
+        """Per-stage device time (ms) of a step, measured with CUDA event
+        nodes captured around each launch (on its stream) in a dedicated
+        graph, replayed back-to-back like the timed loop.  The profiling graph
+        re-runs one parity, so the state is re-synchronised afterwards."""
+        lib = _lib.load()
+        torch.cuda.synchronize(self.dev)
+        lib.gtk_prof_reset()
+        lib.gtk_prof_enable(1)
+        stream = torch.cuda.Stream(self.dev)
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g, stream=stream):
+                self._enqueue(self.t % 2)
+        finally:
+            lib.gtk_prof_enable(0)
+        ids = {"select_main": _lib.PROF_SELECT_MAIN, "select": _lib.PROF_SELECT,
+               "exchange": _lib.PROF_EXCHANGE, "update": _lib.PROF_UPDATE}
+        acc = {k: [] for k in ids}
+        for _ in range(replays):
+            g.replay()
+            torch.cuda.synchronize(self.dev)
+            for name, pid in ids.items():
+                ms, n = _lib.prof_graph_read(pid)
+                if n:
+                    acc[name].append(ms / n)
+        lib.gtk_prof_reset()
+        return {k: (sum(v) / len(v) if v else None) for k, v in acc.items()}
+
+    def step_eager(self) -> None:
+        self._enqueue(self.t % 2)
+        self.t += 1
+
+    def run(self, n: int) -> None:
+        """Enqueue n steps (graph replays when captured)."""
+        for _ in range(n):
+            if self.graphs is not None:
+                self.graphs[self.t % 2].replay()
+                self.t += 1
+            else:
+                self.step_eager()
+
+    def check(self) -> None:
+        """Synchronise, raise the first error of any step, and hand the
+        state's buffers back in their current roles."""
+        word = int(self.status.item())
+        _dev.raise_status(word)
+
+    def sync_state(self) -> None:
+        """Reflect the steps run so far in the OptimizerState (residual role
+        and iteration count)."""
+        st = self.state
+        p = self.t % 2
+        st._res, st._res2 = self.res[p], self.res[1 - p]
+        st.iteration += self.t - getattr(self, "_synced_t", 0)
+        self._synced_t = self.t
+        st._host_cache.clear()
+
+    def global_list(self) -> DeviceList:
+        return self.plan.acc if self.plan is not None else self.sel

@@ -1,0 +1,122 @@
+"""Worker for tests/test_gpu_dist.py: one process per GPU (torchrun, NCCL +
+IPC).  Checks the fused NVLink exchange kernel and the full gtopk_step
+against the CPU oracle (the checker), bit-exactly, for the butterfly and the
+tree + broadcast schedules, the poison path and the CUDA-graph pipeline.
+Prints one JSON line per rank."""
+
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle import gtopk_oracle as orc  # noqa: E402
+from paper_1901_04359_b200 import collectives as coll  # noqa: E402
+from paper_1901_04359_b200 import optimizer as opt  # noqa: E402
+from paper_1901_04359_b200.dist import init_dist_cluster  # noqa: E402
+from paper_1901_04359_b200.pipeline import GTopKPipeline  # noqa: E402
+from paper_1901_04359_b200.sparse import SparseVector  # noqa: E402
+from paper_1901_04359_b200.transport import TransportError  # noqa: E402
+
+F32 = np.float32
+
+
+def bits(a):
+    return np.asarray(a, F32).view(np.uint32)
+
+
+def main():
+    mode = sys.argv[1] if len(sys.argv) > 1 else "auto"
+    ep = init_dist_cluster(timeout=30.0, mode=mode)
+    r, P = ep.rank, ep.world_size
+    out = {"rank": r, "P": P, "mode": mode, "fails": []}
+
+    def check(cond, what):
+        if not cond:
+            out["fails"].append(what)
+
+    # 1. gtopk_allreduce on random / tied / cancelling inputs vs the tree fold
+    rng = np.random.default_rng(77)
+    for trial in range(12):
+        m = int(rng.integers(50, 300_000))
+        k = int(rng.integers(1, min(3000, m // 4) + 2))
+        kind = trial % 3
+        base = rng.standard_normal(m).astype(F32)
+        lists = []
+        for q in range(P):
+            if kind == 0:
+                g = rng.standard_normal(m).astype(F32)
+            elif kind == 1:
+                g = rng.integers(-3, 4, m).astype(F32)
+            else:  # odd ranks cancel even ranks exactly on shared indices
+                g = base if q % 2 == 0 else -base
+            lists.append(orc.top_k_select(g, k)[:2])
+        want_i, want_v = orc.tree_fold(lists, k)
+        before = ep.stats.snapshot()
+        res = coll.gtopk_allreduce(ep, SparseVector(m, *lists[r]), k, P)
+        d = ep.stats.snapshot().delta(before)
+        check(np.array_equal(res.global_topk.indices, want_i), f"idx trial {trial}")
+        check(np.array_equal(bits(res.global_topk.values), bits(want_v)), f"val trial {trial}")
+        check(d.msgs_sent >= 1, f"stats trial {trial}")
+
+    # 2. full gtopk_step trajectories vs the oracle (m=270K ResNet-20 size)
+    m, k, steps = 270_000, 270, 4
+    g_rng = np.random.default_rng(5)
+    grads = [[g_rng.standard_normal(m).astype(F32) for _ in range(P)] for _ in range(steps)]
+    st = opt.make_state(np.zeros(m, F32), lr=0.1)
+    for it in range(steps):
+        rep = opt.gtopk_step(st, ep, grads[it][r], k, P)
+    ref = [orc.State(np.zeros(m, F32), 0.1) for _ in range(P)]
+    for it in range(steps):
+        orc.gtopk_step_all(ref, grads[it], k)
+    check(np.array_equal(bits(st.weights), bits(ref[r].weights)), "step weights")
+    check(np.array_equal(bits(st.residual), bits(ref[r].residual)), "step residual")
+    check(rep.selected_k == k, "selected_k")
+
+    # 3. the CUDA-graph pipeline gives the same trajectory
+    dev = ep.group.device
+    dg = [torch.from_numpy(grads[0][r]).to(dev), torch.from_numpy(grads[1][r]).to(dev)]
+    st2 = opt.make_state(torch.zeros(m, device=dev), lr=0.1)
+    pipe = GTopKPipeline(ep, st2, k, dg)
+    pipe.capture()  # two eager steps
+    pipe.run(2)  # two graph replays
+    pipe.check()
+    pipe.sync_state()
+    ref2 = [orc.State(np.zeros(m, F32), 0.1) for _ in range(P)]
+    for it in range(4):
+        orc.gtopk_step_all(ref2, grads[it % 2], k)
+    check(np.array_equal(bits(st2.weights.cpu().numpy()), bits(ref2[r].weights)), "pipeline weights")
+    check(np.array_equal(bits(st2.residual.cpu().numpy()), bits(ref2[r].residual)), "pipeline residual")
+
+    # 4. poison: a non-finite gradient on rank P-1 fails the step everywhere,
+    #    state untouched
+    st3 = opt.make_state(np.zeros(1000, F32), lr=0.1)
+    g = np.ones(1000, F32)
+    if r == P - 1:
+        g[17] = np.inf
+    w_before = st3.weights.copy()
+    try:
+        opt.gtopk_step(st3, ep, g, 10, P)
+        check(False, "poison: no exception")
+    except FloatingPointError:
+        check(r == P - 1, "poison: FloatingPointError on a healthy rank")
+    except TransportError:
+        check(r != P - 1, "poison: TransportError on the failing rank")
+    check(np.array_equal(st3.weights, w_before) and st3.iteration == 0, "poison: state changed")
+    # the cluster is still usable afterwards
+    res = coll.gtopk_allreduce(ep, SparseVector(100, [r], [1.0 + r]), 1, P)
+    check(res.global_topk.indices.tolist() == [P - 1], "after poison")
+
+    print("RESULT " + json.dumps(out), flush=True)
+    dist.barrier()
+    ep.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

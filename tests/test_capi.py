@@ -70,7 +70,7 @@ def test_argument_validation_without_gpu(lib):
     assert lib.gtk_select(null, null, null, 10, 1, null, null, null, null, null, 0, 0, null) == _lib.GTK_EINVAL
     assert lib.gtk_top_op(null, null, null, null, null, null, 1, 0, null, null, null, null, 0, null) == _lib.GTK_EINVAL
     assert lib.gtk_gtopk_exchange(0, 0, null, 0, null, null, null, null, null, null, 1, null, null, 0, null,
-                                  null, 0, null) == _lib.GTK_EINVAL
+                                  null, null, null, null, 0, null) == _lib.GTK_EINVAL
     with pytest.raises(ValueError):
         _lib.check(_lib.GTK_EINVAL, "x")
     with pytest.raises(FloatingPointError):

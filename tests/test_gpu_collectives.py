@@ -91,10 +91,11 @@ def test_steps_golden(gk, opt):
         P, m, k = int(z[f"c{c}_P"]), int(z[f"c{c}_m"]), int(z[f"c{c}_k"])
         lr, mom, scaling = float(z[f"c{c}_lr"]), float(z[f"c{c}_mom"]), str(z[f"c{c}_scaling"])
         grads = z[f"c{c}_grads"]
+        winit = z[f"c{c}_winit"]  # NpzFile reads are not thread-safe: load before the workers
         fn = opt.STEP_FNS[algo]
 
         def worker(ep):
-            st = opt.make_state(z[f"c{c}_winit"], lr=lr, momentum=mom, update_scaling=scaling)
+            st = opt.make_state(winit, lr=lr, momentum=mom, update_scaling=scaling)
             ks = []
             for it in range(grads.shape[0]):
                 if algo == "dense":

@@ -1,0 +1,57 @@
+"""Multi-GPU parity of the fused NVLink exchange (one process per GPU via
+torchrun).  Needs >= 2 visible GPUs (gpurun --gpus 2 / 4); skipped otherwise.
+Emulating several ranks on one GPU is not done: kernels that wait on each
+other must not share a GPU."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+
+def n_gpus():
+    try:
+        import torch
+
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(n_gpus() < 2, reason="needs >= 2 GPUs")]
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def run(world, mode):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "tests", "gpu_dist_worker.py"), mode]
+    proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-4000:]
+    res = [json.loads(l.split("RESULT ", 1)[1]) for l in proc.stdout.splitlines() if "RESULT " in l]
+    assert len(res) == world, proc.stdout[-2000:]
+    for r in res:
+        assert not r["fails"], r
+
+
+@pytest.mark.parametrize("mode", ["auto", "tree"])
+def test_exchange_all_gpus(mode):
+    run(n_gpus(), mode)
+
+
+def test_exchange_three_ranks_tree():
+    if n_gpus() < 3:
+        pytest.skip("needs >= 3 GPUs")
+    run(3, "auto")
