@@ -85,6 +85,15 @@ __device__ __forceinline__ void st_stream4(float* p, float4 v) {
   __stcs(reinterpret_cast<float4*>(p), v);
 }
 
+// ---- programmatic dependent launch (sm_90+) ---------------------------------
+// launch_dependents: let the next kernel in the stream (launched with the
+// programmatic-serialization attribute) start now; wait: block until the
+// previous kernel has completed and its memory is visible.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---- grid-wide barrier for cooperative launches ---------------------------
 // Generation barrier; count returns to 0 after every use so the workspace
 // needs a single zero-initialisation.

@@ -17,6 +17,25 @@ bool ensure_dyn_smem(const void* func, size_t bytes);
 // blocks for a cooperative ⊤-merge kernel over lists of <= cap entries
 int merge_grid_for(const void* func, int32_t cap);
 
+// Launch with the programmatic-stream-serialization attribute: the kernel may
+// start as soon as the previous kernel in the stream executes
+// griddepcontrol.launch_dependents; it must griddepcontrol.wait before
+// consuming that kernel's results.  Graph-capturable.
+template <typename Arg>
+cudaError_t launch_pdl(void (*kernel)(Arg), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Arg arg) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, arg);
+}
+
 // ---- profiling hooks (bench.py): CUDA events around a launch, recorded on the
 // launching stream, only when enabled and the stream is not being captured ----
 enum ProfId { kProfSelectMain = 0, kProfSelect = 1, kProfExchange = 2, kProfMerge = 3, kProfUpdate = 4, kProfN = 8 };

@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(kSampleThreads) select_sample_kernel(SampleArg
   // (the cost of this kernel) are spread over ~1 block per SM
   __shared__ uint32_t sh[kSampleBins];
   static_assert(kSampleBins == 32 * kSampleThreads, "thread t owns exponent t's 32 fine bins");
+  pdl_launch_dependents();  // the window kernel may launch (it waits for us)
   for (int b = threadIdx.x; b < kSampleBins; b += kSampleThreads) sh[b] = 0;
   const uint64_t e0 = (uint64_t)blockIdx.x * a.stride + threadIdx.x * 4;
   float x[4];
@@ -185,6 +186,8 @@ struct WindowArgs {
 __global__ void __launch_bounds__(kSampleThreads) select_window_kernel(WindowArgs a) {
   __shared__ uint32_t scan[kSampleThreads / 32 + 2];
   __shared__ uint32_t s_exp[2], s_above[2], s_bin[2];
+  pdl_launch_dependents();  // the main pass may launch and start streaming its tiles
+  pdl_wait();               // the sample histograms are complete
   const uint32_t ce = __ldcg(a.coarse + (kSampleThreads - 1 - threadIdx.x));  // descending exponent
   uint32_t tot;
   const uint32_t pre = block_excl_scan<kSampleThreads>(ce, scan, &tot);
@@ -290,6 +293,10 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
       gv[q] = ld_stream4(a.grad + e);
       if (a.res) rv[q] = ld_stream4(a.res + e);
     }
+    // everything below consumes the window kernel's results (and may write
+    // res_out = res in place, which the sample kernel reads): wait for it --
+    // the loads above are already in flight (programmatic dependent launch)
+    pdl_wait();
 #pragma unroll
     for (int q = 0; q < kMainVec; ++q) {
       float4 x = gv[q];
@@ -307,6 +314,7 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
       v[q][3] = x.w;
     }
   } else {
+    pdl_wait();
 #pragma unroll
     for (int q = 0; q < kMainVec; ++q)
 #pragma unroll
@@ -591,7 +599,7 @@ extern "C" int gtk_select(const float* res_in, const float* grad, float* res_out
   GTK_CHECK_LAUNCH();
   WindowArgs wa{r_lo, r_hi, (uint32_t)((flags & GTK_SELECT_FORCE_EXACT) ? 1 : 0), ctl, shist,
                 shist + kSampleBins, ews};
-  select_window_kernel<<<1, kSampleThreads, 0, st>>>(wa);
+  GTK_CUDA(launch_pdl(select_window_kernel, dim3(1), dim3(kSampleThreads), 0, st, wa));
   GTK_CHECK_LAUNCH();
 
   MainArgs ma{res_in,
@@ -610,7 +618,7 @@ extern "C" int gtk_select(const float* res_in, const float* grad, float* res_out
               ews->hist[0]};
   {
     ProfScope prof_main(kProfSelectMain, st);
-    select_main_kernel<<<L.ntiles, kMainThreads, 0, st>>>(ma);
+    GTK_CUDA(launch_pdl(select_main_kernel, dim3(L.ntiles), dim3(kMainThreads), 0, st, ma));
     GTK_CHECK_LAUNCH();
   }
 

@@ -14,6 +14,9 @@ the device (select workspace counters, the exchange's epoch counter).
 
 from __future__ import annotations
 
+import os
+import statistics
+
 import numpy as np
 import torch
 
@@ -123,7 +126,10 @@ class GTopKPipeline:
                 if n:
                     acc[name].append(ms / n)
         lib.gtk_prof_reset()
-        return {k: (sum(v) / len(v) if v else None) for k, v in acc.items()}
+        if os.environ.get("GTK_PROF_DEBUG"):
+            print("profile per replay:", {k: [round(x * 1e3, 1) for x in v] for k, v in acc.items()}, flush=True)
+        # median: robust to a replay delayed by host-side interference
+        return {k: (statistics.median(v) if v else None) for k, v in acc.items()}
 
     def step_eager(self) -> None:
         self._enqueue(self.t % 2)

@@ -30,7 +30,8 @@ def test_dist_host_path(world):
            os.path.join(ROOT, "tests", "dist_worker.py")]
     proc = subprocess.run(cmd, capture_output=True, text=True, timeout=240, env=env, cwd=ROOT)
     assert proc.returncode == 0, proc.stderr[-3000:]
-    results = [json.loads(line.split("RESULT ", 1)[1]) for line in proc.stdout.splitlines() if "RESULT " in line]
+    dec = json.JSONDecoder()  # ranks share stdout: split on the marker, not on lines
+    results = [dec.raw_decode(chunk.strip())[0] for chunk in proc.stdout.split("RESULT ")[1:]]
     assert len(results) == world
     for res in results:
         r = res["rank"]

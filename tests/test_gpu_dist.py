@@ -40,7 +40,9 @@ def run(world, mode):
            os.path.join(ROOT, "tests", "gpu_dist_worker.py"), mode]
     proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-4000:]
-    res = [json.loads(l.split("RESULT ", 1)[1]) for l in proc.stdout.splitlines() if "RESULT " in l]
+    # ranks share stdout: lines may interleave, so split on the marker itself
+    dec = json.JSONDecoder()
+    res = [dec.raw_decode(chunk.strip())[0] for chunk in proc.stdout.split("RESULT ")[1:]]
     assert len(res) == world, proc.stdout[-2000:]
     for r in res:
         assert not r["fails"], r
