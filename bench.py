@@ -28,6 +28,7 @@ cpu_baseline : the numpy oracle port of the reference (oracle/) on host cores.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -252,6 +253,10 @@ def run_b200(args, rank, world):
         return float(t.item())
 
     # ---- device-resident pipeline, CUDA graphs ------------------------------
+    trace = None
+    if os.environ.get("GTK_TRACE") and world > 1:
+        trace = torch.zeros(64, dtype=torch.int64, device=dev)
+        lib.gtk_exchange_set_trace(ctypes.c_void_p(trace.data_ptr()))
     state = opt.make_state(torch.zeros(m, device=dev), lr=0.01)
     pipe = GTopKPipeline(ep, state, k, dgrads)
     pipe.capture()
@@ -269,6 +274,9 @@ def run_b200(args, rank, world):
     ev1.record()
     ev1.synchronize()
     elapsed = ev0.elapsed_time(ev1)
+    dbg = bool(os.environ.get("GTK_PROF_DEBUG"))
+    if dbg:
+        print(f"[rank {rank}] after timed loop: status=0x{int(pipe.status.item()):x}", flush=True)
     # keep the GPU busy until the clock sampler has seen it under load
     soak_end = time.monotonic() + 0.5
     while time.monotonic() < soak_end:
@@ -278,11 +286,25 @@ def run_b200(args, rank, world):
     barrier()
     pipe.check()
     pipe.sync_state()
+    if trace is not None:
+        t = trace.cpu().numpy().astype(np.int64)
+        ns = pipe.plan.nsteps
+        stamps = [("start", t[0])] + [(f"s{j}.{w}", t[2 + 4 * j + i]) for j in range(ns)
+                                      for i, w in enumerate(("push", "flag", "merge", "bar"))] + [("end", t[1])]
+        base = t[0]
+        print(f"[rank {rank}] exchange trace (us from start): " +
+              " ".join(f"{n}={(v - base) / 1e3:.1f}" for n, v in stamps if v), flush=True)
+        lib.gtk_exchange_set_trace(None)
     ms_step = max_over_ranks(elapsed / args.steps)
     gpu_launches = pipe.kernels_per_step * args.steps
 
     # ---- stage breakdown + roofline: CUDA event nodes inside a step graph ----
-    stage = pipe.profile(replays=max(10, min(args.steps, 50)))
+    if dbg:
+        print(f"[rank {rank}] after soak ({pipe.t} steps): status=0x{int(pipe.status.item()):x}", flush=True)
+    stage = pipe.profile(steps=max(10, min(args.steps, 30)))
+    pipe.sync_state()
+    if dbg:
+        print(f"[rank {rank}] after profile: status=0x{int(pipe.status.item()):x}", flush=True)
     pipe.check()
     main_ms = max_over_ranks(stage["select_main"])
     hbm_peak, peak_kind = peaks()

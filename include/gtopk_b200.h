@@ -184,6 +184,10 @@ int gtk_prof_reset(void);
  * synchronised replay this returns the sum of their current durations */
 int gtk_prof_graph_read(int id, double* ms, int64_t* count);
 int64_t gtk_launch_count(void); /* kernels launched by this library so far */
+/* subsequent gtk_gtopk_exchange launches stamp %globaltimer into d_trace[0..]:
+ * [0] start, [1] end, [2+4s+{0,1,2,3}] step s: pushed, flag seen, merged, barrier
+ * (NULL disables) */
+int gtk_exchange_set_trace(int64_t* d_trace);
 
 #ifdef __cplusplus
 }

@@ -61,6 +61,7 @@ EXPORTS = (
     "gtk_prof_reset",
     "gtk_prof_graph_read",
     "gtk_launch_count",
+    "gtk_exchange_set_trace",
 )
 
 _P = ctypes.c_void_p
@@ -104,6 +105,7 @@ _SIGS = {
     "gtk_prof_reset": ([], _I32),
     "gtk_prof_graph_read": ([_I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)], _I32),
     "gtk_launch_count": ([], _I64),
+    "gtk_exchange_set_trace": ([_P], _I32),
 }
 
 PROF_SELECT_MAIN = 0

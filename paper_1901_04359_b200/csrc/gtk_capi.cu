@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -92,6 +93,18 @@ static double g_sum_ms[kProfN];
 static long long g_cnt[kProfN];
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+static int64_t* g_trace = nullptr;
+int64_t* trace_buffer() { return g_trace; }
+void set_trace_buffer(int64_t* p) { g_trace = p; }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("GTK_NO_PDL");
+    return !(v && v[0] && v[0] != '0');
+  }();
+  return on;
+}
 
 static cudaEvent_t pool_get() {
   if (!g_pool.empty()) {

@@ -50,14 +50,37 @@ struct ExchangeArgs {
   const volatile uint32_t* d_abort;
   int64_t timeout_ns;
   int32_t* step_counts;  // [nsteps][2] (sent, received) entry counts, for stats
+  int64_t* trace;        // optional %globaltimer phase stamps (block 0), see gtk_exchange_set_trace
   const int32_t* in_idx; // optional input list copied into acc first (keeps the
   const float* in_val;   // caller's local selection intact for K3)
   const int32_t* d_in_n;
   MergeArgs merge;       // workspace pointers; list pointers filled per step
 };
 
+// inbox slot: 16 B header {count, hint} | idx[k4] | val[k4], k4 = k rounded up
+// to 4 so both arrays are 16-byte aligned for 128-bit peer stores
+__host__ __device__ inline size_t slot_k4(int32_t k) { return ((size_t)k + 3) & ~size_t(3); }
 __host__ __device__ inline size_t slot_bytes(int32_t k) {
-  return (16 + (size_t)k * 8 + 255) & ~size_t(255);
+  return (16 + slot_k4(k) * 8 + 255) & ~size_t(255);
+}
+
+// copy entries [e0, e1) of (src_idx, src_val) to (dst_idx, dst_val) -- 128-bit
+// accesses on the 4-aligned body (all list buffers start 16-byte aligned)
+__device__ __forceinline__ void copy_entries(int32_t* dst_idx, float* dst_val, const int32_t* src_idx,
+                                             const float* src_val, uint32_t e0, uint32_t e1) {
+  const uint32_t a0 = (e0 + 3) & ~3u, a1 = max(a0, e1 & ~3u);
+  for (uint32_t e = e0 + threadIdx.x; e < min(a0, e1); e += blockDim.x) {
+    dst_idx[e] = __ldcg(src_idx + e);
+    dst_val[e] = __ldcg(src_val + e);
+  }
+  for (uint32_t q = a0 / 4 + threadIdx.x; q < a1 / 4; q += blockDim.x) {
+    reinterpret_cast<int4*>(dst_idx)[q] = __ldcg(reinterpret_cast<const int4*>(src_idx) + q);
+    reinterpret_cast<float4*>(dst_val)[q] = __ldcg(reinterpret_cast<const float4*>(src_val) + q);
+  }
+  for (uint32_t e = max(a1, e0) + threadIdx.x; e < e1; e += blockDim.x) {
+    dst_idx[e] = __ldcg(src_idx + e);
+    dst_val[e] = __ldcg(src_val + e);
+  }
 }
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -80,22 +103,13 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   // step so no peer hangs, but sends count = -1; receivers flag PEER_FAILED
   // and forward the poison, so every rank fails the step and K3 is skipped.
   const bool self_poison = (__ldcg(a.d_status) & GTK_DEV_NONFINITE) != 0;
+  const bool tr = a.trace && blk == 0 && threadIdx.x == 0;
+  if (tr) a.trace[0] = (int64_t)globaltimer();
 
-  if (a.in_idx) {  // acc = input list
-    uint32_t n = self_poison ? 0u : (uint32_t)__ldcg(a.d_in_n);
-    if (n > (uint32_t)a.k) n = a.k;
-    const uint32_t per = (n + G - 1) / G;
-    const uint32_t e0 = min(n, blk * per), e1 = min(n, e0 + per);
-    for (uint32_t e = e0 + threadIdx.x; e < e1; e += kMergeThreads) {
-      a.acc_idx[e] = __ldcg(a.in_idx + e);
-      a.acc_val[e] = __ldcg(a.in_val + e);
-    }
-    if (blk == 0 && threadIdx.x == 0) {
-      a.d_acc_n[0] = (int32_t)n;
-      a.d_acc_n[1] = __ldcg(a.d_in_n + 1);  // k-th key hint
-    }
-    grid_sync(&a.merge.ews->bar, G);
-  }
+  // the current list: the caller's input until the first merge/copy writes acc
+  const int32_t* cur_idx = a.in_idx ? a.in_idx : a.acc_idx;
+  const float* cur_val = a.in_idx ? a.in_val : a.acc_val;
+  const int32_t* cur_n = a.in_idx ? a.d_in_n : a.d_acc_n;
 
   for (int s = 0; s < a.nsteps; ++s) {
     const Step st = a.steps[s];
@@ -103,26 +117,26 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
       char* slot = a.inbox[st.send_to] + ((size_t)s * 2 + par) * slot_bytes(a.k);
       int32_t* r_n = (int32_t*)slot;
       int32_t* r_idx = (int32_t*)(slot + 16);
-      float* r_val = (float*)(slot + 16 + (size_t)a.k * 4);
+      float* r_val = (float*)(slot + 16 + slot_k4(a.k) * 4);
       const bool poisoned = self_poison || (__ldcg(a.d_status) & GTK_DEV_PEER_FAILED);
-      uint32_t n = poisoned ? 0u : (uint32_t)__ldcg(a.d_acc_n);
+      uint32_t n = poisoned ? 0u : (uint32_t)__ldcg(cur_n);
       if (n > (uint32_t)a.k) n = a.k;
-      const uint32_t per = (n + G - 1) / G;
+      const uint32_t per = ((n + G - 1) / G + 3) & ~3u;  // 4-aligned shares: 128-bit peer stores
       const uint32_t e0 = min(n, blk * per), e1 = min(n, e0 + per);
-      for (uint32_t e = e0 + threadIdx.x; e < e1; e += kMergeThreads) {
-        r_idx[e] = __ldcg(a.acc_idx + e);
-        r_val[e] = __ldcg(a.acc_val + e);
-      }
+      copy_entries(r_idx, r_val, cur_idx, cur_val, e0, e1);
       if (blk == 0 && threadIdx.x == 0) {
         r_n[0] = poisoned ? -1 : (int32_t)n;
-        r_n[1] = poisoned ? 0 : __ldcg(a.d_acc_n + 1);  // k-th key hint travels with the list
+        r_n[1] = poisoned ? 0 : __ldcg(cur_n + 1);  // k-th key hint travels with the list
         if (a.step_counts) a.step_counts[2 * s] = (int32_t)n;
       }
+      // bar.sync orders every thread's peer stores before thread 0's fence;
+      // the system-scope release then publishes them all (cumulativity)
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence_system();
         red_release_sys_add_u64(a.flags[st.send_to] + s, 1ull);
       }
+      if (tr) a.trace[2 + 4 * s] = (int64_t)globaltimer();
     }
     if (st.recv_from >= 0) {
       if (threadIdx.x == 0) {
@@ -139,14 +153,15 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
               break;
             }
           }
-          __nanosleep(64);
+          if (spins > 64) __nanosleep(32);
         }
         __threadfence();
       }
       __syncthreads();
+      if (tr) a.trace[3 + 4 * s] = (int64_t)globaltimer();
       char* slot = a.inbox[a.rank] + ((size_t)s * 2 + par) * slot_bytes(a.k);
       const int32_t* in_idx = (const int32_t*)(slot + 16);
-      const float* in_val = (const float*)(slot + 16 + (size_t)a.k * 4);
+      const float* in_val = (const float*)(slot + 16 + slot_k4(a.k) * 4);
       if (threadIdx.x == 0) {
         int32_t n = __ldcg((const int32_t*)slot);
         if (n < 0 && blk == 0) atomicOr(a.d_status, GTK_DEV_PEER_FAILED);
@@ -157,18 +172,20 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
       const uint32_t n_in = s_n, hint_in = s_hint;
       if (blk == 0 && threadIdx.x == 0 && a.step_counts) a.step_counts[2 * s + 1] = (int32_t)n_in;
       if (st.merge) {
-        uint32_t n_own = self_poison ? 0u : (uint32_t)__ldcg(a.d_acc_n);
+        // every block reads the own count before the merge's first barrier;
+        // the merge writes acc (and its count) only after that barrier
+        uint32_t n_own = self_poison ? 0u : (uint32_t)__ldcg(cur_n);
         if (n_own > (uint32_t)a.k) n_own = a.k;
-        const uint32_t hint_own = self_poison ? 0u : (uint32_t)__ldcg(a.d_acc_n + 1);
-        grid_sync(&a.merge.ews->bar, G);  // everyone has read the counts
+        const uint32_t hint_own = self_poison ? 0u : (uint32_t)__ldcg(cur_n + 1);
         MergeArgs m = a.merge;
         m.a_idx = in_idx;
         m.a_val = in_val;
-        m.b_idx = a.acc_idx;
-        m.b_val = a.acc_val;
+        m.b_idx = cur_idx;
+        m.b_val = cur_val;
         m.o_idx = a.acc_idx;
         m.o_val = a.acc_val;
         m.d_no = a.d_acc_n;
+        m.trace = a.trace ? a.trace + 32 + 16 * s : nullptr;
         merge_device(m, n_in, n_own, hint_in, hint_own, G, S);
       } else {
         const uint32_t per = (n_in + G - 1) / G;
@@ -182,15 +199,44 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
           a.d_acc_n[1] = (int32_t)hint_in;
         }
       }
+      cur_idx = a.acc_idx;
+      cur_val = a.acc_val;
+      cur_n = a.d_acc_n;
+      if (tr) a.trace[4 + 4 * s] = (int64_t)globaltimer();
     }
-    grid_sync(&a.merge.ews->bar, G);
+    // the next push reads acc written by every block; no barrier after the
+    // last step (the next call starts on a kernel boundary)
+    if (s + 1 < a.nsteps) grid_sync(&a.merge.ews->bar, G);
+    if (tr) a.trace[5 + 4 * s] = (int64_t)globaltimer();
   }
-  if (blk == 0 && threadIdx.x == 0) *a.d_epoch = epoch;
+  if (a.in_idx && cur_idx != a.acc_idx) {  // no step wrote acc: it is the input
+    uint32_t n = (uint32_t)__ldcg(a.d_in_n);
+    if (n > (uint32_t)a.k) n = a.k;
+    const uint32_t per = (n + G - 1) / G;
+    const uint32_t e0 = min(n, blk * per), e1 = min(n, e0 + per);
+    for (uint32_t e = e0 + threadIdx.x; e < e1; e += kMergeThreads) {
+      a.acc_idx[e] = __ldcg(a.in_idx + e);
+      a.acc_val[e] = __ldcg(a.in_val + e);
+    }
+    if (blk == 0 && threadIdx.x == 0) {
+      a.d_acc_n[0] = (int32_t)n;
+      a.d_acc_n[1] = __ldcg(a.d_in_n + 1);
+    }
+  }
+  if (blk == 0 && threadIdx.x == 0) {
+    *a.d_epoch = epoch;
+    if (tr) a.trace[1] = (int64_t)globaltimer();
+  }
 }
 
 }  // namespace gtk
 
 using namespace gtk;
+
+extern "C" int gtk_exchange_set_trace(int64_t* d_trace) {
+  set_trace_buffer(d_trace);
+  return GTK_OK;
+}
 
 extern "C" int gtk_exchange_inbox_bytes(int32_t k, int32_t nsteps, size_t* bytes) {
   if (!bytes || k < 1 || nsteps < 0 || nsteps > kMaxSteps) return GTK_EINVAL;
@@ -274,6 +320,7 @@ extern "C" int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedu
   a.d_abort = (const volatile uint32_t*)d_abort;
   a.timeout_ns = timeout_ns;
   a.step_counts = step_counts;
+  a.trace = trace_buffer();
   if (in_idx && (!in_val || !d_in_n)) return GTK_EINVAL;
   a.in_idx = in_idx;
   a.in_val = in_val;

@@ -102,20 +102,29 @@ struct GridBarrier {
   uint32_t gen;
 };
 
+__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Thread 0 arrives with an acq_rel atomic (cumulative over the block's writes
+// through the preceding bar.sync), the last arriver resets the count and
+// releases the generation, the others acquire it; bar.sync then extends the
+// ordering to the whole block.  Cross-block data is read with ld.global.cg.
 __device__ __forceinline__ void grid_sync(GridBarrier* b, unsigned nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t g = ld_acquire_gpu(&b->gen);
-    __threadfence();
-    const uint32_t prev = atomicAdd(&b->count, 1u);
+    const uint32_t prev = atom_add_acq_rel_gpu(&b->count, 1u);
     if (prev == nblocks - 1) {
-      b->count = 0;
-      __threadfence();
+      b->count = 0;  // ordered before the release below
       st_release_gpu(&b->gen, g + 1);
     } else {
-      while (ld_acquire_gpu(&b->gen) == g) __nanosleep(32);
+      uint32_t spins = 0;
+      while (ld_acquire_gpu(&b->gen) == g)
+        if (++spins > 32) __nanosleep(20);
     }
-    __threadfence();
   }
   __syncthreads();
 }

@@ -42,12 +42,16 @@ struct EngineWS {
   uint32_t cta_b[kMaxBlocks];
 };
 
+constexpr uint32_t kKeptBits = 8192;  // slice slots covered by the kept bitmap
+constexpr uint32_t kSlotBits = 22;    // gather record: (block << 22) | slot within the block's slice
+
 template <int NT>
 struct EngineSmem {
   uint32_t hist[kHistStride];
   uint32_t keys[kGatherCap];
   int32_t gidx[kGatherCap];
   uint32_t gblk[kGatherCap];
+  uint32_t kept_bits[kKeptBits / 32];  // my slice's in-bin winners
   uint32_t scan[NT / 32 + 2];
   uint32_t bcast[8];
   uint32_t ng;
@@ -95,7 +99,16 @@ struct Sink {
   int32_t* d_count;  // d_count[0] = kept entries; d_count[1] = kt-th key hint (0 = none)
   float* zero_at;    // select: res_out[idx] = +0.0 for kept entries (nullable)
   bool write_hint;
+  int64_t* trace;    // optional %globaltimer stamps of block 0: [0] bin found, [1] after gather barrier, [2] ranked, [3] written
 };
+
+__device__ __forceinline__ void sink_stamp(const Sink& out, int i) {
+  if (out.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    out.trace[i] = (int64_t)t;
+  }
+}
 
 __device__ __forceinline__ void slice_of(uint32_t N, unsigned G, unsigned b, uint32_t& s0, uint32_t& s1) {
   const uint32_t S = (N + G - 1) / G;
@@ -110,9 +123,7 @@ __device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t* red) {
   __syncthreads();
   if (lane_id() == 0) red[warp_id()] = v;
   __syncthreads();
-  uint32_t t = 0;
-#pragma unroll
-  for (int w = 0; w < NT / 32; ++w) t += red[w];
+  const uint32_t t = warp_sum(lane_id() < (unsigned)(NT / 32) ? red[lane_id()] : 0u);
   __syncthreads();
   return t;
 }
@@ -192,7 +203,7 @@ __device__ void engine_write(const Src& src, uint32_t s0, uint32_t s1, uint32_t 
     int32_t i = 0;
     float v = 0.f;
     bool keep = false;
-    if (s < s1 && src.get(s, key, i, v)) keep = keep_fn(key, i);
+    if (s < s1 && src.get(s, key, i, v)) keep = keep_fn(key, i, s - s0);
     uint32_t k_tot;
     const uint32_t k_rank = block_excl_scan<NT>(keep ? 1u : 0u, sm.scan, &k_tot);
     if (keep) {
@@ -236,7 +247,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       for (unsigned j = threadIdx.x; j < blk; j += NT) before += __ldcg(&ws->cta_a[j]);
       before = block_sum<NT>(before, sm.scan);
     }
-    engine_write<NT>(src, s0, s1, before, [](uint32_t, int32_t) { return true; }, sm, out);
+    engine_write<NT>(src, s0, s1, before, [](uint32_t, int32_t, uint32_t) { return true; }, sm, out);
     if (blk == 0) {
       for (int r = 0; r < kRounds; ++r)
         for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[r][b] = 0;
@@ -262,6 +273,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
     }
     uint32_t bin, above, in_bin;
     if (!engine_find_bin<NT>(hist, hsm, t, sm, bin, above, in_bin)) return false;
+    sink_stamp(out, 0);
     uint64_t blo, bhi;
     if (bin < (uint32_t)kBins) {
       blo = (uint64_t)lo + ((uint64_t)bin << shift);
@@ -291,12 +303,12 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
             const uint32_t p = atomicAdd(&sm.ng, 1u);
             sm.keys[p] = key;
             sm.gidx[p] = i;
-            sm.gblk[p] = blk;
+            sm.gblk[p] = (blk << kSlotBits) | (s - s0);
           } else {
             const uint32_t p = atomicAdd(&ws->gather_n[r], 1u);
             ws->gather_key[p] = key;
             ws->gather_idx[p] = i;
-            ws->gather_blk[p] = blk;
+            ws->gather_blk[p] = (blk << kSlotBits) | (s - s0);
           }
         }
       }
@@ -305,8 +317,15 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       if (!solo) {
         if (threadIdx.x == 0) ws->cta_a[blk] = n_above;
         grid_sync(&ws->bar, G);
+        // one round trip: the count, the (at most kGatherMax) gathered entries
+        // and the per-block counts are independent loads
         const uint32_t ng = __ldcg(&ws->gather_n[r]);
-        for (uint32_t j = threadIdx.x; j < ng; j += NT) {
+        for (uint32_t j = threadIdx.x; j < (uint32_t)kGatherMax; j += NT) {
+          sm.keys[j] = __ldcg(&ws->gather_key[j]);
+          sm.gidx[j] = __ldcg(&ws->gather_idx[j]);
+          sm.gblk[j] = __ldcg(&ws->gather_blk[j]);
+        }
+        for (uint32_t j = kGatherMax + threadIdx.x; j < ng; j += NT) {  // last-round bins up to kGatherCap
           sm.keys[j] = __ldcg(&ws->gather_key[j]);
           sm.gidx[j] = __ldcg(&ws->gather_idx[j]);
           sm.gblk[j] = __ldcg(&ws->gather_blk[j]);
@@ -315,6 +334,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
         if (threadIdx.x == 0) sm.ng = ng;
       }
       above_before = block_sum<NT>(above_before, sm.scan);  // also publishes sm.keys / sm.ng
+      sink_stamp(out, 1);
       const uint32_t ng = sm.ng;
       // tau = t_in-th largest gathered key; gt = # gathered keys > tau
       if (threadIdx.x == 0) sm.bcast[3] = sm.bcast[4] = 0;
@@ -335,7 +355,12 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       __syncthreads();
       const uint32_t tau = sm.bcast[3];
       const uint32_t need = t_in - sm.bcast[4];  // entries with key == tau to keep, lowest idx first
-      // kept flags of the gathered entries (reuse gblk's top bit), my offset
+      sink_stamp(out, 2);
+      // kept flags of the gathered entries: winners of my slice go to a
+      // bitmap indexed by slot (O(1) lookup in the write), the ones of
+      // earlier blocks shift my output offset
+      for (uint32_t w = threadIdx.x; w < kKeptBits / 32; w += NT) sm.kept_bits[w] = 0;
+      __syncthreads();
       uint32_t extra = 0;
       for (uint32_t j = threadIdx.x; j < ng; j += NT) {
         const uint32_t x = sm.keys[j];
@@ -346,22 +371,29 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
           for (uint32_t q = 0; q < ng; ++q) rank += (sm.keys[q] == tau && sm.gidx[q] < ij);
           kept = rank < need;
         }
+        const uint32_t gb = sm.gblk[j] >> kSlotBits, slot = sm.gblk[j] & ((1u << kSlotBits) - 1);
         if (kept) {
-          sm.gblk[j] |= 0x80000000u;
-          if ((sm.gblk[j] & 0x7FFFFFFFu) < blk) ++extra;
+          if (gb < blk) ++extra;
+          // (a slot beyond the bitmap -- large global-mode slice -- is found
+          // by the scan in keep_fn instead)
+          if (gb == blk && slot < kKeptBits) atomicOr(&sm.kept_bits[slot >> 5], 1u << (slot & 31));
+        } else {
+          sm.gblk[j] = 0xFFFFFFFFu;  // mark "not kept" for the large-slice scan
         }
       }
       extra = block_sum<NT>(extra, sm.scan);
       const uint32_t bl = (uint32_t)blo, bh32 = (uint32_t)min(bhi, (uint64_t)0xFFFFFFFFu);
       const bool bh_max = bhi > 0xFFFFFFFFull;
-      auto keep_fn = [&](uint32_t key, int32_t i) -> bool {
+      auto keep_fn = [&](uint32_t key, int32_t i, uint32_t slot) -> bool {
         if (!bh_max && key >= bh32) return true;
         if (key < bl) return false;
+        if (slot < kKeptBits) return (sm.kept_bits[slot >> 5] >> (slot & 31)) & 1u;
         for (uint32_t q = 0; q < ng; ++q)
-          if (sm.gidx[q] == i) return (sm.gblk[q] & 0x80000000u) != 0;
+          if (sm.gidx[q] == i) return sm.gblk[q] != 0xFFFFFFFFu;
         return false;
       };
       engine_write<NT>(src, s0, s1, above_before + extra, keep_fn, sm, out);
+      sink_stamp(out, 3);
       if (blk == 0) {  // every block is past its last histogram read
         for (int rr = 0; rr < kRounds; ++rr)
           for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[rr][b] = 0;

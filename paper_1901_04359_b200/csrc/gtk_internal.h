@@ -21,8 +21,18 @@ int merge_grid_for(const void* func, int32_t cap);
 // start as soon as the previous kernel in the stream executes
 // griddepcontrol.launch_dependents; it must griddepcontrol.wait before
 // consuming that kernel's results.  Graph-capturable.
+bool pdl_enabled();  // GTK_NO_PDL=1 disables (A/B measurements)
+// debug trace buffer (gtk_exchange_set_trace): exchange stamps at [0..31],
+// merge phase stamps at [32 + 16*step ..] (standalone merges use [32..])
+int64_t* trace_buffer();
+void set_trace_buffer(int64_t* p);
+
 template <typename Arg>
 cudaError_t launch_pdl(void (*kernel)(Arg), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Arg arg) {
+  if (!pdl_enabled()) {
+    kernel<<<grid, block, smem, st>>>(arg);
+    return cudaGetLastError();
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

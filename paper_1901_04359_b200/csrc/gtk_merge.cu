@@ -57,6 +57,6 @@ extern "C" int gtk_top_op(const int32_t* a_idx, const float* a_val, const int32_
   char* base = (char*)ws;
   MergeArgs args{a_idx, a_val, d_na, b_idx, b_val, d_nb, (uint32_t)k, o_idx, o_val, d_no,
                  (MergeCtl*)(base + L.ctl), (EngineWS*)(base + L.engine), (int32_t*)(base + L.u_idx),
-                 (float*)(base + L.u_val)};
+                 (float*)(base + L.u_val), trace_buffer() ? trace_buffer() + 32 : nullptr};
   return launch_merge(args, cap < 1 ? 1 : cap, (cudaStream_t)stream);
 }

@@ -70,7 +70,16 @@ struct MergeArgs {
   EngineWS* ews;
   int32_t* u_idx;  // global slot scratch for slices larger than kMergeSliceCap
   float* u_val;
+  int64_t* trace;  // optional %globaltimer stamps of block 0 (phase boundaries)
 };
+
+__device__ __forceinline__ void merge_stamp(const MergeArgs& a, int i) {
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[i] = (int64_t)t;
+  }
+}
 
 struct MergeSmem {
   EngineSmem<kMergeThreads> esm;
@@ -172,25 +181,46 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   const bool in_smem = L <= (uint32_t)kMergeSliceCap;
   const uint32_t nsub = (L + kMergeSub - 1) / kMergeSub;
   // all sub-chunk boundaries of the slice, one warp each, in parallel
+  merge_stamp(a, 0);
   for (uint32_t j = warp_id(); j <= nsub; j += kMergeThreads / 32) {
     const uint32_t d = min(d1, d0 + j * kMergeSub);
     const uint32_t i = merge_path_warp(a.a_idx, na, a.b_idx, nb, d);
     if (lane_id() == 0) S.split[j] = i;
   }
   __syncthreads();
+  merge_stamp(a, 1);  // merge-path splits known
   uint32_t my_valid = 0;
   for (uint32_t j = 0; j < nsub; ++j) {
     const uint32_t sub = d0 + j * kMergeSub, sub_end = min(d1, sub + kMergeSub);
     const uint32_t ia = S.split[j], ib = S.split[j + 1];
     const uint32_t ja = sub - ia, jb = sub_end - ib;
     const uint32_t la = ib - ia, lb = jb - ja;
-    for (uint32_t t = threadIdx.x; t < la; t += kMergeThreads) {
-      S.sAi[t] = __ldcg(a.a_idx + ia + t);
-      S.sAv[t] = __ldcg(a.a_val + ia + t);
-    }
-    for (uint32_t t = threadIdx.x; t < lb; t += kMergeThreads) {
-      S.sBi[t] = __ldcg(a.b_idx + ja + t);
-      S.sBv[t] = __ldcg(a.b_val + ja + t);
+    // stage A[ia, ib) and B[ja, jb): every load of the sub-chunk in flight at once
+    for (uint32_t base = 0; base < la + lb; base += 4 * kMergeThreads) {
+      int32_t ri[4];
+      float rv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t t = base + u * kMergeThreads + threadIdx.x;
+        if (t < la) {
+          ri[u] = __ldcg(a.a_idx + ia + t);
+          rv[u] = __ldcg(a.a_val + ia + t);
+        } else if (t < la + lb) {
+          ri[u] = __ldcg(a.b_idx + ja + (t - la));
+          rv[u] = __ldcg(a.b_val + ja + (t - la));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t t = base + u * kMergeThreads + threadIdx.x;
+        if (t < la) {
+          S.sAi[t] = ri[u];
+          S.sAv[t] = rv[u];
+        } else if (t < la + lb) {
+          S.sBi[t - la] = ri[u];
+          S.sBv[t - la] = rv[u];
+        }
+      }
     }
     const int32_t prevA = ia > 0 ? __ldcg(a.a_idx + ia - 1) : -1;
     const int32_t nextB = jb < nb ? __ldcg(a.b_idx + jb) : -1;
@@ -245,6 +275,7 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   my_valid = warp_sum(my_valid);
   if (lane_id() == 0 && my_valid) atomicAdd(&S.s_valid, my_valid);
   __syncthreads();
+  merge_stamp(a, 2);  // union slots + histogram built
   const bool solo = G == 1;
   uint32_t n_valid;
   if (solo) {
@@ -258,12 +289,14 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
     grid_sync(&a.ews->bar, G);
     n_valid = __ldcg(&a.ctl->n_valid);
   }
+  merge_stamp(a, 3);  // after the histogram barrier
   const bool keep_all = n_valid <= a.k;
   const SliceSrc src{S.slice_idx, S.slice_val, a.u_idx, a.u_val, d0, in_smem, true};
-  const Sink out{a.o_idx, a.o_val, a.d_no, nullptr, true};
+  const Sink out{a.o_idx, a.o_val, a.d_no, nullptr, true, a.trace ? a.trace + 5 : nullptr};
   const uint32_t* h0 = solo ? esm.hist : a.ews->hist[0];
   bool ok = engine_run<kMergeThreads>(src, d0, d1, keep_all ? n_valid : a.k, keep_all, win_lo, win_shift, h0, solo,
                                       a.ews, esm, out, G);
+  merge_stamp(a, 4);  // engine done
   if (!ok) {  // the hint window missed (cancellation): full key range
     if (!solo) {
       grid_sync(&a.ews->bar, G);

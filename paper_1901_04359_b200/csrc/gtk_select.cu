@@ -3,11 +3,10 @@
 //
 // Four launches per call, no host synchronisation:
 //   1. select_sample  : ~128/rho sampled elements of acc = res + g (evenly
-//                       strided 4 KB chunks, one per block) into an 8192-bin
-//                       histogram of the top key bits + a 256-bin exponent
-//                       histogram.
-//   2. select_window  : one block turns the sample histograms into a
-//                       conservative key window [lo, hi) around the k-th key.
+//                       strided 4 KB chunks, one per block); each block keeps
+//                       its exact top-32 keys (bitwise binary search on counts).
+//   2. select_window  : one block finds the exact sample order statistics
+//                       around rank k*s/m (+-4 sigma) -> key window [lo, hi).
 //   3. select_main    : THE HBM pass.  One 4096-element tile per block, no
 //                       inter-block dependency: 128-bit streaming loads of res
 //                       and g, acc = __fadd_rn(res, g) streamed to res_out, key
@@ -39,8 +38,8 @@ constexpr int kMainVec = 4;                                  // float4 per threa
 constexpr int kTile = kMainThreads * kMainVec * 4;          // 4096 elements
 constexpr int kSampleThreads = 256;
 constexpr int kSampleChunk = kSampleThreads * 4;            // 1024 elements per chunk
-constexpr int kSampleBins = 8192;                            // key >> 18
-constexpr int kSampleShift = 18;
+constexpr int kSampleTop = 32;                               // top keys kept per sample block
+constexpr int kSampleMaxChunks = 1024;                       // sample blocks (window holds 32K keys)
 constexpr int kFinishThreads = 512;
 constexpr int kSliceCap = 3072;                              // candidates staged per finish block
 constexpr uint32_t kOvfBit = 0x80000000u;
@@ -55,7 +54,7 @@ struct SelectCtl {
 };
 
 struct SelectLayout {
-  size_t ctl, sample_hist, engine, tile_info, tile_ovf, slot_idx, slot_val, ovf_idx, ovf_val, ord_idx, ord_val,
+  size_t ctl, sample_top, engine, tile_info, tile_ovf, slot_idx, slot_val, ovf_idx, ovf_val, ord_idx, ord_val,
       total;
   uint32_t ntiles, slots, ovf_cap, ord_cap;
 };
@@ -79,8 +78,8 @@ static SelectLayout select_layout(int64_t m, int32_t k) {
   size_t off = 0;
   L.ctl = off;
   off = al(off + sizeof(SelectCtl));
-  L.sample_hist = off;
-  off = al(off + sizeof(uint32_t) * (kSampleBins + 256));
+  L.sample_top = off;
+  off = al(off + sizeof(uint32_t) * kSampleMaxChunks * kSampleTop);
   L.engine = off;
   off = al(off + sizeof(EngineWS));
   L.tile_info = off;
@@ -104,24 +103,87 @@ static SelectLayout select_layout(int64_t m, int32_t k) {
 }
 
 // ---------------------------------------------------------------------------
-// 1. sampling pass
+// 1. sampling pass: per-block top-kSampleTop keys (exact, no atomics)
 // ---------------------------------------------------------------------------
+// The threshold window must come from exact sample ORDER STATISTICS, not from
+// histogram bin edges: an accumulated residual develops a flat-topped
+// magnitude distribution (every entry grows until it is selected), where the
+// top k all lie within ~0.1% of tau -- a bin edge would admit a large fraction
+// of m as candidates.
 struct SampleArgs {
   const float* res;
   const float* grad;
   uint32_t m;
-  uint32_t stride;   // elements between chunk starts
-  uint32_t* hist;    // [kSampleBins] fine, zero on entry (re-zeroed by the window kernel)
-  uint32_t* coarse;  // [256] per-exponent sums, same protocol
+  uint32_t stride;  // elements between chunk starts
+  uint32_t* top;    // [nchunks][kSampleTop] block-local top keys (0-padded)
 };
 
+// The r1-th and r2-th largest of the keys held by the block (NT threads x PER
+// keys each) in one bitwise binary search on counts (both counts packed in
+// one word: fewer than 2^16 keys); r >= 1.  A rank beyond the number of
+// nonzero keys yields 0.
+template <int NT, int PER>
+__device__ __forceinline__ uint2 block_rank_keys(const uint32_t (&keys)[PER], uint32_t r1, uint32_t r2,
+                                                 uint32_t (&red)[2][NT / 32]) {
+  static_assert(NT * PER < 65536, "packed 16-bit counts");
+  uint32_t p1 = 0, p2 = 0;
+#pragma unroll 1
+  for (int bit = 30; bit >= 0; --bit) {
+    const uint32_t c1 = p1 | (1u << bit), c2 = p2 | (1u << bit);
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) c += (keys[j] >= c1 ? 1u : 0u) + (keys[j] >= c2 ? 0x10000u : 0u);
+    c = warp_sum(c);
+    uint32_t* rb = red[bit & 1];  // double-buffered: one barrier per iteration
+    if (lane_id() == 0) rb[warp_id()] = c;
+    __syncthreads();
+    uint32_t tot = lane_id() < (unsigned)(NT / 32) ? rb[lane_id()] : 0u;
+    tot = warp_sum(tot);
+    if ((tot & 0xFFFFu) >= r1) p1 = c1;
+    if ((tot >> 16) >= r2) p2 = c2;
+  }
+  return make_uint2(p1, p2);
+}
+
+// r-th largest of the keys held by one warp (32 lanes x PER keys), bitwise
+// binary search on warp-reduced counts; 0 if fewer than r nonzero keys.
+template <int PER>
+__device__ __forceinline__ uint32_t warp_rank_key(const uint32_t (&keys)[PER], uint32_t r) {
+  uint32_t p = 0;
+#pragma unroll 1
+  for (int bit = 30; bit >= 0; --bit) {
+    const uint32_t cand = p | (1u << bit);
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) c += keys[j] >= cand;
+    if (warp_sum(c) >= r) p = cand;
+  }
+  return p;
+}
+
+// Write the warp's kSampleTop largest keys (all keys > th, then keys == th,
+// order irrelevant, zero-padded) to out[0..kSampleTop).
+template <int PER>
+__device__ __forceinline__ void warp_emit_top(const uint32_t (&keys)[PER], uint32_t th, uint32_t* out) {
+  const unsigned lane = lane_id();
+  uint32_t n = 0;
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const bool f = pass == 0 ? keys[j] > th : (keys[j] == th && th > 0);
+      const unsigned bal = __ballot_sync(kFull, f);
+      const uint32_t pos = n + __popc(bal & lanemask_lt());
+      if (f && pos < (uint32_t)kSampleTop) out[pos] = keys[j];
+      n += __popc(bal);
+    }
+  }
+  for (uint32_t p = n + lane; p < (uint32_t)kSampleTop; p += 32) out[p] = 0;
+}
+
 __global__ void __launch_bounds__(kSampleThreads) select_sample_kernel(SampleArgs a) {
-  // one 1024-element chunk per block: the per-element shared-memory atomics
-  // (the cost of this kernel) are spread over ~1 block per SM
-  __shared__ uint32_t sh[kSampleBins];
-  static_assert(kSampleBins == 32 * kSampleThreads, "thread t owns exponent t's 32 fine bins");
+  __shared__ uint32_t s_wtop[kSampleThreads / 32][kSampleTop];
   pdl_launch_dependents();  // the window kernel may launch (it waits for us)
-  for (int b = threadIdx.x; b < kSampleBins; b += kSampleThreads) sh[b] = 0;
   const uint64_t e0 = (uint64_t)blockIdx.x * a.stride + threadIdx.x * 4;
   float x[4];
   if (e0 + 4 <= a.m) {
@@ -141,7 +203,7 @@ __global__ void __launch_bounds__(kSampleThreads) select_sample_kernel(SampleArg
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint64_t e = e0 + j;
-      float v = __int_as_float(0x7F800000);  // +inf: ignored below
+      float v = 0.0f;
       if (e < a.m) {
         v = a.grad[e];
         if (a.res) v = __fadd_rn(a.res[e], v);
@@ -149,89 +211,59 @@ __global__ void __launch_bounds__(kSampleThreads) select_sample_kernel(SampleArg
       x[j] = v;
     }
   }
-  __syncthreads();
+  uint32_t key[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const uint32_t key = key_of(x[j]);
-    if (key < kInfKey) atomicAdd(&sh[key >> kSampleShift], 1u);
+    const uint32_t kk = key_of(x[j]);
+    key[j] = kk < kInfKey ? kk : 0u;  // non-finite: ignored (K1 reports it)
   }
+  // level 1: each warp's top-32 of its 128 keys (warp-only search, no barrier)
+  const uint32_t wth = warp_rank_key<4>(key, kSampleTop);
+  uint32_t* wtop = s_wtop[warp_id()];
+  warp_emit_top<4>(key, wth, wtop);
   __syncthreads();
-  // flush (fire-and-forget reductions): thread t owns exponent t's 32 fine bins
-  uint32_t csum = 0;
-#pragma unroll 8
-  for (int j = 0; j < 32; ++j) {
-    const int b = threadIdx.x * 32 + ((j + threadIdx.x) & 31);  // rotated: no bank conflicts
-    const uint32_t v = sh[b];
-    if (v) {
-      atomicAdd(a.hist + b, v);
-      csum += v;
-    }
+  // level 2: warp 0 takes the block's top-32 of the 8 x 32 warp winners
+  if (warp_id() == 0) {
+    uint32_t k2[kSampleThreads / 32];
+#pragma unroll
+    for (int w = 0; w < kSampleThreads / 32; ++w) k2[w] = s_wtop[w][lane_id()];
+    const uint32_t bth = warp_rank_key<kSampleThreads / 32>(k2, kSampleTop);
+    warp_emit_top<kSampleThreads / 32>(k2, bth, a.top + (size_t)blockIdx.x * kSampleTop);
   }
-  if (csum) atomicAdd(a.coarse + threadIdx.x, csum);
 }
 
 // ---------------------------------------------------------------------------
-// 2. threshold window (one block)
+// 2. threshold window (one block): exact sample ranks r_lo / r_hi
 // ---------------------------------------------------------------------------
+constexpr int kWindowThreads = 512;  // x PER keys each, PER in {8, 16, 32, 64} by sample size
+
 struct WindowArgs {
-  uint32_t r_lo;         // rank (from top) whose bin's LOWER edge becomes lo
-  uint32_t r_hi;         // rank whose bin's UPPER edge bounds the window
+  uint32_t r_lo;         // sample rank (from top) whose key becomes lo
+  uint32_t r_hi;         // sample rank whose key (+1) becomes hi
+  uint32_t nkeys;        // nchunks * kSampleTop
   uint32_t force_exact;  // 1 -> lo = 0x7FFFFFFF (forces the dense fallback)
   SelectCtl* ctl;
-  uint32_t* hist;
-  uint32_t* coarse;
+  const uint32_t* top;
   EngineWS* ews;
 };
 
-__global__ void __launch_bounds__(kSampleThreads) select_window_kernel(WindowArgs a) {
-  __shared__ uint32_t scan[kSampleThreads / 32 + 2];
-  __shared__ uint32_t s_exp[2], s_above[2], s_bin[2];
+template <int PER>
+__global__ void __launch_bounds__(kWindowThreads) select_window_kernel(WindowArgs a) {
+  __shared__ uint32_t red[2][kWindowThreads / 32];
   pdl_launch_dependents();  // the main pass may launch and start streaming its tiles
-  pdl_wait();               // the sample histograms are complete
-  const uint32_t ce = __ldcg(a.coarse + (kSampleThreads - 1 - threadIdx.x));  // descending exponent
-  uint32_t tot;
-  const uint32_t pre = block_excl_scan<kSampleThreads>(ce, scan, &tot);
-  if (threadIdx.x == 0) {
-    s_exp[0] = s_exp[1] = 0xFFFFFFFFu;
-    s_bin[0] = s_bin[1] = 0xFFFFFFFFu;
-  }
-  __syncthreads();
-  const uint32_t rk[2] = {a.r_lo, a.r_hi};
+  pdl_wait();               // the sample tops are complete
+  uint32_t key[PER];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
-    if (ce && pre < rk[i] && pre + ce >= rk[i]) {
-      s_exp[i] = kSampleThreads - 1 - threadIdx.x;
-      s_above[i] = pre;
-    }
-  __syncthreads();
-  if (warp_id() < 2) {
-    const int i = warp_id();
-    const unsigned lane = lane_id();
-    if (s_exp[i] != 0xFFFFFFFFu) {
-      const uint32_t bin = s_exp[i] * 32 + 31 - lane;  // descending inside the exponent
-      const uint32_t v = __ldcg(a.hist + bin);
-      uint32_t incl = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, incl, o);
-        if (lane >= (unsigned)o) incl += y;
-      }
-      const uint32_t ex = s_above[i] + incl - v;
-      if (v && ex < rk[i] && ex + v >= rk[i]) s_bin[i] = bin;
-    }
+  for (int j = 0; j < PER; ++j) {
+    const uint32_t i = j * kWindowThreads + threadIdx.x;
+    key[j] = i < a.nkeys ? __ldcg(a.top + i) : 0u;
   }
-  __syncthreads();
-  for (int b = threadIdx.x; b < kSampleBins; b += kSampleThreads) a.hist[b] = 0;
-  a.coarse[threadIdx.x] = 0;
+  const uint2 kk = block_rank_keys<kWindowThreads, PER>(key, a.r_lo, a.r_hi, red);
+  const uint32_t klo = kk.x, khi = kk.y;
+  if (threadIdx.x < kRounds) a.ews->gather_n[threadIdx.x] = 0;  // the finish engine's counters
   if (threadIdx.x == 0) {
-    uint32_t lo = s_bin[0] == 0xFFFFFFFFu ? 0u : (s_bin[0] << kSampleShift);  // too few samples: all
-    uint32_t hi;
-    if (s_bin[1] == 0xFFFFFFFFu) {
-      hi = 0x80000000u;
-    } else {
-      hi = (s_bin[1] + 1) << kSampleShift;
-      if (hi <= lo) hi = lo + (1u << kSampleShift);
-    }
+    uint32_t lo = klo;  // 0 when the sample holds fewer than r_lo nonzero keys: take all
+    uint32_t hi = khi >= lo ? khi + 1 : lo + 1;
     if (a.force_exact) {
       lo = 0x7FFFFFFFu;
       hi = 0x80000000u;
@@ -244,10 +276,6 @@ __global__ void __launch_bounds__(kSampleThreads) select_window_kernel(WindowArg
     ctl->ovf_cursor = 0;
     ctl->overflow = 0;
     ctl->nonfinite = 0;
-  }
-  if (threadIdx.x < kRounds) {  // the finish engine's gather counters (read only after its barrier)
-    EngineWS* ews = a.ews;
-    ews->gather_n[threadIdx.x] = 0;
   }
 }
 
@@ -441,7 +469,16 @@ struct FinishArgs {
   float* sel_val;
   int32_t* d_count;
   uint32_t* d_status;
+  int64_t* trace;  // optional phase stamps (block 0): [0] start [1] scanned [2] copied [3..6] engine
 };
+
+__device__ __forceinline__ void finish_stamp(const FinishArgs& a, int i) {
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[i] = (int64_t)t;
+  }
+}
 
 __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArgs a) {
   __shared__ EngineSmem<kFinishThreads> sm;
@@ -455,7 +492,8 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
     }
     return;
   }
-  const Sink out{a.sel_idx, a.sel_val, a.d_count, a.res_out, true};
+  const Sink out{a.sel_idx, a.sel_val, a.d_count, a.res_out, true, a.trace ? a.trace + 3 : nullptr};
+  finish_stamp(a, 0);
 
   // my tile range and its place in the global (index-ordered) candidate list
   const uint32_t per = (a.ntiles + G - 1) / G;
@@ -479,6 +517,7 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
   own = block_sum<kFinishThreads>(own, sm.scan);
   const uint32_t C = block_sum<kFinishThreads>(all, sm.scan);
   const bool overflow = __ldcg(&a.ctl->overflow) != 0;
+  finish_stamp(a, 1);
   if (!overflow && C >= a.k && C <= a.ord_cap) {
     // copy my tiles' candidates into my slice (smem if it fits)
     const bool in_smem = own <= (uint32_t)kSliceCap;
@@ -527,6 +566,7 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
       run += tot;
       __syncthreads();
     }
+    finish_stamp(a, 2);
     SliceSrc src{s_idx, s_val, a.ord_idx, a.ord_val, before, in_smem, false};
     if (engine_run<kFinishThreads>(src, before, before + own, a.k, false, __ldcg(&a.ctl->lo),
                                    __ldcg(&a.ctl->shift), a.ews->hist[0], false, a.ews, sm, out, G))
@@ -571,19 +611,21 @@ extern "C" int gtk_select(const float* res_in, const float* grad, float* res_out
   char* base = (char*)ws;
   SelectCtl* ctl = (SelectCtl*)(base + L.ctl);
   EngineWS* ews = (EngineWS*)(base + L.engine);
-  uint32_t* shist = (uint32_t*)(base + L.sample_hist);
+  uint32_t* stop = (uint32_t*)(base + L.sample_top);
 
-  // sample plan: expect ~128 sampled elements above the k-th key
+  // sample plan: ~128 sampled elements expected above the k-th key, at most
+  // kSampleMaxChunks chunks of 1024 (each keeps its top kSampleTop keys)
   const double mu_full = 128.0;
-  const uint64_t s_target = (uint64_t)std::ceil(mu_full * (double)m / (double)k);
+  const uint64_t chunks_all = (uint64_t)((m + kSampleChunk - 1) / kSampleChunk);
+  uint64_t swant = (uint64_t)std::ceil(mu_full * (double)m / (double)k / kSampleChunk);
+  if (swant < 1) swant = 1;
   uint32_t nchunks, stride, r_lo, r_hi;
-  if (s_target * 2 >= (uint64_t)m) {  // small problem: scan everything, exact window
-    nchunks = (uint32_t)((m + kSampleChunk - 1) / kSampleChunk);
+  if (swant * 2 >= chunks_all && chunks_all <= (uint64_t)kSampleMaxChunks) {
+    nchunks = (uint32_t)chunks_all;  // small problem: every element, exact rank k
     stride = kSampleChunk;
-    r_lo = (uint32_t)k;
-    r_hi = (uint32_t)k;
+    r_lo = r_hi = (uint32_t)k;
   } else {
-    nchunks = (uint32_t)((s_target + kSampleChunk - 1) / kSampleChunk);
+    nchunks = (uint32_t)(swant < (uint64_t)kSampleMaxChunks ? swant : (uint64_t)kSampleMaxChunks);
     stride = (uint32_t)((uint64_t)m / nchunks) & ~3u;
     if (stride < (uint32_t)kSampleChunk) stride = kSampleChunk;
     const double s = (double)nchunks * kSampleChunk;
@@ -594,12 +636,19 @@ extern "C" int gtk_select(const float* res_in, const float* grad, float* res_out
     r_hi = rh < 1.0 ? 1u : (uint32_t)rh;
   }
   ProfScope prof_all(kProfSelect, st);
-  SampleArgs sa{res_in, grad, (uint32_t)m, stride, shist, shist + kSampleBins};
+  SampleArgs sa{res_in, grad, (uint32_t)m, stride, stop};
   select_sample_kernel<<<nchunks, kSampleThreads, 0, st>>>(sa);
   GTK_CHECK_LAUNCH();
-  WindowArgs wa{r_lo, r_hi, (uint32_t)((flags & GTK_SELECT_FORCE_EXACT) ? 1 : 0), ctl, shist,
-                shist + kSampleBins, ews};
-  GTK_CUDA(launch_pdl(select_window_kernel, dim3(1), dim3(kSampleThreads), 0, st, wa));
+  WindowArgs wa{r_lo, r_hi, nchunks * (uint32_t)kSampleTop, (uint32_t)((flags & GTK_SELECT_FORCE_EXACT) ? 1 : 0),
+                ctl, stop, ews};
+  {
+    const uint32_t nk = wa.nkeys;
+    auto* wk = nk <= 8 * kWindowThreads    ? select_window_kernel<8>
+               : nk <= 16 * kWindowThreads ? select_window_kernel<16>
+               : nk <= 32 * kWindowThreads ? select_window_kernel<32>
+                                           : select_window_kernel<64>;
+    GTK_CUDA(launch_pdl(wk, dim3(1), dim3(kWindowThreads), 0, st, wa));
+  }
   GTK_CHECK_LAUNCH();
 
   MainArgs ma{res_in,
@@ -641,7 +690,8 @@ extern "C" int gtk_select(const float* res_in, const float* grad, float* res_out
                 sel_idx,
                 sel_val,
                 d_count,
-                d_status};
+                d_status,
+                trace_buffer() ? trace_buffer() + 48 : nullptr};
 
 
   int G = coop_grid((const void*)select_finish_kernel, kFinishThreads, 0);

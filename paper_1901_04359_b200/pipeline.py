@@ -99,37 +99,32 @@ class GTopKPipeline:
         self.graphs = graphs
         torch.cuda.synchronize(self.dev)
 
-    def profile(self, replays: int = 20) -> dict:
-        """Per-stage device time (ms) of a step, measured with CUDA event
-        nodes captured around each launch (on its stream) in a dedicated
-        graph, replayed back-to-back like the timed loop.  The profiling graph
-        re-runs one parity, so the state is re-synchronised afterwards."""
+    def profile(self, steps: int = 20) -> dict:
+        """Per-stage device time (ms) of a step: CUDA events recorded by the
+        library around each launch on its stream, for `steps` eager steps
+        queued behind a long spin kernel -- so they execute back-to-back with
+        no host gaps, exactly like graph replays."""
         lib = _lib.load()
         torch.cuda.synchronize(self.dev)
         lib.gtk_prof_reset()
         lib.gtk_prof_enable(1)
-        stream = torch.cuda.Stream(self.dev)
-        g = torch.cuda.CUDAGraph()
         try:
-            with torch.cuda.graph(g, stream=stream):
-                self._enqueue(self.t % 2)
+            torch.cuda._sleep(int(4e7))  # ~20 ms: covers the host enqueue of every step
+            for _ in range(steps):
+                self.step_eager()
         finally:
             lib.gtk_prof_enable(0)
+        torch.cuda.synchronize(self.dev)
         ids = {"select_main": _lib.PROF_SELECT_MAIN, "select": _lib.PROF_SELECT,
                "exchange": _lib.PROF_EXCHANGE, "update": _lib.PROF_UPDATE}
-        acc = {k: [] for k in ids}
-        for _ in range(replays):
-            g.replay()
-            torch.cuda.synchronize(self.dev)
-            for name, pid in ids.items():
-                ms, n = _lib.prof_graph_read(pid)
-                if n:
-                    acc[name].append(ms / n)
+        out = {}
+        for name, pid in ids.items():
+            ms, n = _lib.prof_read(pid)
+            out[name] = ms / n if n else None
         lib.gtk_prof_reset()
         if os.environ.get("GTK_PROF_DEBUG"):
-            print("profile per replay:", {k: [round(x * 1e3, 1) for x in v] for k, v in acc.items()}, flush=True)
-        # median: robust to a replay delayed by host-side interference
-        return {k: (statistics.median(v) if v else None) for k, v in acc.items()}
+            print("profile (ms per launch):", out, flush=True)
+        return out
 
     def step_eager(self) -> None:
         self._enqueue(self.t % 2)

@@ -169,6 +169,43 @@ def test_select_full_size_properties(dev):
         assert int(eq_out.min()) > int(eq_in.max())
 
 
+def test_select_flat_top_no_fallback(dev):
+    """A flat-topped magnitude distribution (what an accumulated residual
+    looks like: the top k within ~0.1% of tau) must stay on the sampled fast
+    path (no GTK_DEV_FALLBACK) and be exact."""
+    from oracle import gtopk_oracle as orc
+
+    rng = np.random.default_rng(11)
+    m, k = 4_000_000, 4000
+    g = (500.0 + rng.random(m)).astype(F32) * np.where(rng.random(m) < 0.5, -1, 1).astype(F32)
+    wi, wv, wres = orc.top_k_select(g, k)
+    i, v, res, word = _device_select(dev, g, k)
+    assert word & 0x2 == 0, "flat-topped input fell back to the dense exact path"
+    assert np.array_equal(i, wi) and np.array_equal(v.view(np.uint32), wv.view(np.uint32))
+    assert np.array_equal(res.view(np.uint32), wres.view(np.uint32))
+
+
+def test_pipeline_steady_state_no_fallback(gk):
+    """Thousands of residual-accumulation steps (the bench's steady state)
+    keep every select on the fast path."""
+    import torch
+
+    from paper_1901_04359_b200 import optimizer as opt
+    from paper_1901_04359_b200.pipeline import GTopKPipeline
+
+    d = torch.device("cuda", 0)
+    m, k = 2_000_000, 2000
+    gen = torch.Generator(device=d).manual_seed(5)
+    grads = [torch.randn(m, device=d, generator=gen) for _ in range(2)]
+    ep = gk.create_local_cluster(1)[0]
+    st = opt.make_state(torch.zeros(m, device=d), lr=0.01)
+    pipe = GTopKPipeline(ep, st, k, grads)
+    pipe.capture()
+    pipe.run(3000)
+    pipe.check()
+    assert int(pipe.status.item()) & 0x2 == 0, "steady-state select used the dense fallback"
+
+
 def test_top_op_golden(gk):
     z = load_golden("top_op.npz")
     for c in range(int(z["n"])):
