@@ -260,6 +260,12 @@ def run_b200(args, rank, world):
     state = opt.make_state(torch.zeros(m, device=dev), lr=0.01)
     pipe = GTopKPipeline(ep, state, k, dgrads)
     pipe.capture()
+    # mid-training residual: gTop-k's residual builds up over ~1/rho steps
+    # before its magnitudes settle; precondition it (untimed) so the timed
+    # steps see the steady state a long training run spends its time in
+    pipe.run(args.precondition)
+    torch.cuda.synchronize(dev)
+    pipe.status.zero_()  # (misses while the residual built up are informational)
     sampler = ClockSampler(dev.index) if rank == 0 else None
     if sampler:
         sampler.start()
@@ -274,6 +280,7 @@ def run_b200(args, rank, world):
     ev1.record()
     ev1.synchronize()
     elapsed = ev0.elapsed_time(ev1)
+    timed_fallback = bool(int(pipe.status.item()) & 0x2)  # any dense-fallback select in the timed steps
     dbg = bool(os.environ.get("GTK_PROF_DEBUG"))
     if dbg:
         print(f"[rank {rank}] after timed loop: status=0x{int(pipe.status.item()):x}", flush=True)
@@ -314,7 +321,7 @@ def run_b200(args, rank, world):
 
     # ---- e2e: public API with pinned host gradients --------------------------
     pinned = [torch.from_numpy(g).pin_memory() for g in host_grads]
-    st2 = opt.make_state(torch.zeros(m, device=dev), lr=0.01)
+    st2 = state  # the same (steady-state) training state, continued through the public API
     for i in range(max(2, args.warmup)):
         opt.gtopk_step(st2, ep, pinned[i % 2], k, P)
     barrier()
@@ -356,6 +363,8 @@ def run_b200(args, rank, world):
                 "m": m, "k": k, "rho": rho, "P": P, "exchange": exch,
                 "step": "K1 select + gTopKAllReduce + K3 update, CUDA-graph replay",
                 "l2": "inputs larger than L2: 307 MB streamed by K1 per step vs 126 MB L2",
+                "residual": f"steady state: {args.precondition} untimed preconditioning steps before warmup",
+                "dense_fallback_in_timed_steps": timed_fallback,
             },
             "roofline": {"bound": "hbm", "kernel": "select_main_kernel (K1 HBM pass)",
                          "achieved": round(achieved, 1), "peak": hbm_peak, "peak_kind": peak_kind,
@@ -387,6 +396,8 @@ def main():
     ap.add_argument("--rho", type=float, default=RHO_DEFAULT)
     ap.add_argument("--mode", choices=["auto", "butterfly", "tree"], default="auto")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    ap.add_argument("--precondition", type=int, default=1500,
+                    help="untimed steps that build the residual up to its steady state")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", "0"))

@@ -81,6 +81,22 @@ int gtk_select(const float* res_in, const float* grad, float* res_out, int64_t m
                int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
                size_t ws_bytes, int32_t flags, void* stream);
 
+/* gtk_select with a per-parameter key window carried from call to call.
+ *   d_window : device uint32[8] owned by the caller, one per parameter (the
+ *              residual whose selections follow each other), zeroed once.
+ *              Each call leaves {valid | margin level << 8, lo, shift, k,
+ *              approx. k-th key, previous one, 0, 0} measured from its own candidate
+ *              histogram; the next call with the same k skips the sampling
+ *              pass and streams against that window (shifted by the last
+ *              growth of the k-th key).  A stale window can only cost the
+ *              exact dense fallback (GTK_DEV_FALLBACK), after which the window
+ *              is invalid (the next call samples again) and, if it admitted
+ *              too few keys, its margin level rises.
+ *              Results are bit-identical to gtk_select in every case. */
+int gtk_select_windowed(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
+                        int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
+                        size_t ws_bytes, int32_t flags, uint32_t* d_window, void* stream);
+
 /* ------------------------------------------------------------------------
  * K2: the sparse top-k merge operator ⊤.
  * Replaces sparse.py:157-195 (top_op(a, b, k)); a = received, b = own

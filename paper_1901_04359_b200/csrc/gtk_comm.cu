@@ -94,6 +94,8 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   MergeSmem& S = *reinterpret_cast<MergeSmem*>(dsm);
   __shared__ uint32_t s_n, s_hint;
   const unsigned G = gridDim.x, blk = blockIdx.x;
+  pdl_wait();               // launched programmatically behind the select
+  pdl_launch_dependents();  // K3 may become resident; it waits for our completion
   // every block reads the counter before anyone advances it (block 0 does so
   // after the final grid barrier)
   const uint64_t epoch = __ldcg((const unsigned long long*)a.d_epoch) + 1;
@@ -333,5 +335,6 @@ extern "C" int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedu
   if (G <= 0) return GTK_ECUDA;
   void* args[] = {&a};
   ProfScope prof(kProfExchange, (cudaStream_t)stream);
-  return coop_launch((const void*)exchange_kernel, G, kMergeThreads, args, sizeof(MergeSmem), (cudaStream_t)stream);
+  return coop_launch((const void*)exchange_kernel, G, kMergeThreads, args, sizeof(MergeSmem), (cudaStream_t)stream,
+                     true);
 }

@@ -108,6 +108,13 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v
   return old;
 }
 
+// wrapping ticket: old value; the counter returns to 0 after lim
+__device__ __forceinline__ uint32_t atom_inc_acq_rel_gpu(uint32_t* p, uint32_t lim) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.inc.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(lim) : "memory");
+  return old;
+}
+
 // Thread 0 arrives with an acq_rel atomic (cumulative over the block's writes
 // through the preceding bar.sync), the last arriver resets the count and
 // releases the generation, the others acquire it; bar.sync then extends the

@@ -100,6 +100,10 @@ struct Sink {
   float* zero_at;    // select: res_out[idx] = +0.0 for kept entries (nullable)
   bool write_hint;
   int64_t* trace;    // optional %globaltimer stamps of block 0: [0] bin found, [1] after gather barrier, [2] ranked, [3] written
+  uint32_t* next_window;  // select only (nullable): the next call's key window, see engine_run
+  uint32_t window_level;  // margin level L >= 1: the next window admits ~k (1 + 2^L / 2) keys
+  uint32_t prev_tau;      // the previous call's approximate k-th key (0: none)
+  uint32_t prev_tau2;     // ... and the one before
 };
 
 __device__ __forceinline__ void sink_stamp(const Sink& out, int i) {
@@ -157,7 +161,8 @@ __device__ void engine_hist(const Src& src, uint32_t s0, uint32_t s1, uint32_t l
 // answer.  Returns false if the histogram holds < t entries.
 template <int NT>
 __device__ bool engine_find_bin(const uint32_t* hist, bool in_smem, uint32_t t, EngineSmem<NT>& sm,
-                                uint32_t& bin, uint32_t& above, uint32_t& in_bin) {
+                                uint32_t& bin, uint32_t& above, uint32_t& in_bin, uint32_t t2 = 0,
+                                uint32_t t3 = 0, uint32_t* bin2 = nullptr, uint32_t* bin3 = nullptr) {
   constexpr int PER = (kHistLen + NT - 1) / NT;
   // thread t owns reversed positions [t*PER, t*PER+PER): rb = 0 is OVER (bin 2048)
   uint32_t c[PER];
@@ -170,7 +175,7 @@ __device__ bool engine_find_bin(const uint32_t* hist, bool in_smem, uint32_t t, 
   }
   uint32_t tot;
   uint32_t pre = block_excl_scan<NT>(sum, sm.scan, &tot);
-  if (threadIdx.x == 0) sm.bcast[0] = 0xFFFFFFFFu;
+  if (threadIdx.x == 0) sm.bcast[0] = sm.bcast[5] = sm.bcast[6] = 0xFFFFFFFFu;
   __syncthreads();
   if (pre < t && pre + sum >= t) {
     uint32_t acc = pre;
@@ -184,10 +189,21 @@ __device__ bool engine_find_bin(const uint32_t* hist, bool in_smem, uint32_t t, 
       acc += c[j];
     }
   }
+  if (t2 != 0) {  // extra ranks (bins only), same scan
+    uint32_t acc = pre;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      if (acc < t2 && acc + c[j] >= t2) sm.bcast[5] = kBins - (threadIdx.x * PER + j);
+      if (acc < t3 && acc + c[j] >= t3) sm.bcast[6] = kBins - (threadIdx.x * PER + j);
+      acc += c[j];
+    }
+  }
   __syncthreads();
   bin = sm.bcast[0];
   above = sm.bcast[1];
   in_bin = sm.bcast[2];
+  if (bin2) *bin2 = sm.bcast[5];
+  if (bin3) *bin3 = sm.bcast[6];
   __syncthreads();
   return tot >= t && bin != 0xFFFFFFFFu;
 }
@@ -272,7 +288,53 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       hsm = solo;
     }
     uint32_t bin, above, in_bin;
-    if (!engine_find_bin<NT>(hist, hsm, t, sm, bin, above, in_bin)) return false;
+    if (r == 0 && out.next_window) {
+      // select: besides rank kt, the ranks kt (1 + 2^L / 2) and kt/2 of this
+      // window give the next call's window [lo', hi') -- the same parameter's
+      // accumulated residual moves slowly from step to step, so next time
+      // about that many candidates pass lo' (a miss costs one exact dense
+      // fallback and raises L)
+      uint32_t b2, b3;
+      const uint64_t t2w = (uint64_t)kt + (((uint64_t)kt << out.window_level) >> 1);
+      const uint32_t t2 = (uint32_t)min(t2w, (uint64_t)0xFFFFFFFFu), t3 = max(1u, kt / 2);
+      if (!engine_find_bin<NT>(hist, hsm, t, sm, bin, above, in_bin, t2, t3, &b2, &b3)) return false;
+      if (blk == 0 && threadIdx.x == 0) {
+        uint64_t lo_n = lo, hi_n = hi;
+        if (b2 != 0xFFFFFFFFu) lo_n = (uint64_t)lo + ((uint64_t)b2 << shift);
+        if (b3 != 0xFFFFFFFFu && b3 < (uint32_t)kBins) hi_n = (uint64_t)lo + ((uint64_t)(b3 + 1) << shift);
+        if (hi_n > hi) hi_n = hi;
+        // the k-th key's recent path (keys are log-scaled: a common relative
+        // growth of the magnitudes is a common key offset):
+        //  - jitter J = |second difference|: keep lo' at least 2^(L-1) J below
+        //    the k-th key (flat-topped residuals pack many k below tau);
+        //  - steady growth (the residual building up): shift by half the
+        //    smaller of the last two increments.
+        const uint32_t tau_n = (uint32_t)min((uint64_t)lo + ((uint64_t)bin << shift), (uint64_t)0x7FFFFFFFu);
+        const uint32_t p1 = out.prev_tau, p2 = out.prev_tau2;
+        if (p1 != 0 && p2 != 0) {
+          const int64_t i1 = (int64_t)tau_n - (int64_t)p1, i2 = (int64_t)p1 - (int64_t)p2;
+          const uint64_t jit = (uint64_t)(i1 > i2 ? i1 - i2 : i2 - i1);
+          const uint64_t back = jit << (out.window_level - 1);
+          const uint64_t lo_j = tau_n > back ? tau_n - back : 0u;
+          if (lo_j < lo_n) lo_n = lo_j;
+          if (i1 > 0 && i2 > 0) {
+            const uint64_t d = (uint64_t)min(i1, i2) / 2;
+            lo_n = min(lo_n + d, (uint64_t)0x7FFFFFFFu);
+            hi_n = min(hi_n + d, (uint64_t)0x80000000u);
+          }
+        }
+        if (hi_n <= lo_n) hi_n = lo_n + 1;
+        const uint64_t width = hi_n - lo_n;
+        out.next_window[1] = (uint32_t)lo_n;
+        out.next_window[2] = width <= (uint64_t)kBins ? 0u : ceil_log2_u64((width + kBins - 1) / kBins);
+        out.next_window[3] = kt;
+        out.next_window[4] = tau_n;
+        out.next_window[5] = p1;
+        out.next_window[0] = 1u | (out.window_level << 8);
+      }
+    } else if (!engine_find_bin<NT>(hist, hsm, t, sm, bin, above, in_bin)) {
+      return false;
+    }
     sink_stamp(out, 0);
     uint64_t blo, bhi;
     if (bin < (uint32_t)kBins) {

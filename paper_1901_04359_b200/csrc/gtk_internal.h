@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #include "../../include/gtopk_b200.h"
 
 namespace gtk {
@@ -11,7 +13,10 @@ void set_last_cuda_error(cudaError_t e);
 int num_sms();
 // max co-resident blocks of `func` (cooperative launch limit) on the current device
 int coop_grid(const void* func, int threads, size_t smem);
-int coop_launch(const void* func, int grid, int threads, void** args, size_t smem, cudaStream_t st);
+// pdl: programmatic dependent launch on the previous kernel of the stream
+// (the kernel must griddepcontrol.wait before consuming its outputs)
+int coop_launch(const void* func, int grid, int threads, void** args, size_t smem, cudaStream_t st,
+                bool pdl = false);
 // opt a kernel into > 48 KB of dynamic shared memory (once per device); false on error
 bool ensure_dyn_smem(const void* func, size_t bytes);
 // blocks for a cooperative ⊤-merge kernel over lists of <= cap entries
@@ -27,10 +32,11 @@ bool pdl_enabled();  // GTK_NO_PDL=1 disables (A/B measurements)
 int64_t* trace_buffer();
 void set_trace_buffer(int64_t* p);
 
-template <typename Arg>
-cudaError_t launch_pdl(void (*kernel)(Arg), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Arg arg) {
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
   if (!pdl_enabled()) {
-    kernel<<<grid, block, smem, st>>>(arg);
+    kernel<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -43,7 +49,7 @@ cudaError_t launch_pdl(void (*kernel)(Arg), dim3 grid, dim3 block, size_t smem, 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, arg);
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ---- profiling hooks (bench.py): CUDA events around a launch, recorded on the

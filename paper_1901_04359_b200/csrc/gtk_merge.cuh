@@ -292,7 +292,7 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   merge_stamp(a, 3);  // after the histogram barrier
   const bool keep_all = n_valid <= a.k;
   const SliceSrc src{S.slice_idx, S.slice_val, a.u_idx, a.u_val, d0, in_smem, true};
-  const Sink out{a.o_idx, a.o_val, a.d_no, nullptr, true, a.trace ? a.trace + 5 : nullptr};
+  const Sink out{a.o_idx, a.o_val, a.d_no, nullptr, true, a.trace ? a.trace + 5 : nullptr, nullptr, 0u, 0u, 0u};
   const uint32_t* h0 = solo ? esm.hist : a.ews->hist[0];
   bool ok = engine_run<kMergeThreads>(src, d0, d1, keep_all ? n_valid : a.k, keep_all, win_lo, win_shift, h0, solo,
                                       a.ews, esm, out, G);

@@ -1,13 +1,14 @@
 // K1: fused residual-add + exact top-k select (reference optimizer.py:219-220,
 // sparse.py:135-154).
 //
-// Four launches per call, no host synchronisation:
+// Three launches per call (PDL-chained), no host synchronisation:
 //   1. select_sample  : ~128/rho sampled elements of acc = res + g (evenly
 //                       strided 4 KB chunks, one per block); each block keeps
-//                       its exact top-32 keys (bitwise binary search on counts).
-//   2. select_window  : one block finds the exact sample order statistics
-//                       around rank k*s/m (+-4 sigma) -> key window [lo, hi).
-//   3. select_main    : THE HBM pass.  One 4096-element tile per block, no
+//                       its exact top-32 keys (histogram levels in shared
+//                       memory); the last block to finish finds the exact
+//                       sample order statistics around rank k*s/m (+-4 sigma)
+//                       -> key window [lo, hi).
+//   2. select_main    : THE HBM pass.  One 4096-element tile per block, no
 //                       inter-block dependency: 128-bit streaming loads of res
 //                       and g, acc = __fadd_rn(res, g) streamed to res_out, key
 //                       test against lo, warp-ballot compaction of the tile's
@@ -15,7 +16,7 @@
 //                       tile's own slot row -- or, for a dense tile, into an
 //                       atomically reserved overflow region -- and a 2049-bin
 //                       histogram of candidate keys over the window.
-//   4. select_finish  : cooperative.  Block b owns a contiguous range of tiles;
+//   3. select_finish  : cooperative.  Block b owns a contiguous range of tiles;
 //                       it copies their candidates (already index-ordered) into
 //                       shared memory -- its slice of the global candidate
 //                       list -- and the exact engine (gtk_engine.cuh) keeps the
@@ -25,6 +26,7 @@
 //                       acc instead: the exact fallback.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -36,13 +38,17 @@ namespace gtk {
 constexpr int kMainThreads = 256;
 constexpr int kMainVec = 4;                                  // float4 per thread per array
 constexpr int kTile = kMainThreads * kMainVec * 4;          // 4096 elements
-constexpr int kSampleThreads = 256;
-constexpr int kSampleChunk = kSampleThreads * 4;            // 1024 elements per chunk
+constexpr int kMainTilesPerBlock = 2;                      // tiles loaded up front by one main-pass block
+constexpr int kMainDenseHist = 48;                          // candidates per tile above which the histogram goes via smem
+constexpr int kSampleThreads = 1024;
+constexpr int kSampleChunk = kSampleThreads;                // 1024 elements per chunk (one per thread)
 constexpr int kSampleTop = 32;                               // top keys kept per sample block
 constexpr int kSampleMaxChunks = 1024;                       // sample blocks (window holds 32K keys)
 constexpr int kFinishThreads = 512;
 constexpr int kSliceCap = 3072;                              // candidates staged per finish block
 constexpr uint32_t kOvfBit = 0x80000000u;
+constexpr uint32_t kMinWindowLevel = 2;  // carried-window margin: from k (1 + 2^2 / 2) = 3k candidates
+constexpr uint32_t kMaxWindowLevel = 4;  // ... up to k (1 + 2^4 / 2) = 9k
 
 struct SelectCtl {
   uint32_t lo;
@@ -50,7 +56,8 @@ struct SelectCtl {
   uint32_t ovf_cursor;
   uint32_t overflow;
   uint32_t nonfinite;
-  uint32_t pad[11];
+  uint32_t sample_done;  // sample-block ticket (atomicInc, wraps to 0 per launch)
+  uint32_t pad[10];
 };
 
 struct SelectLayout {
@@ -69,8 +76,10 @@ static SelectLayout select_layout(int64_t m, int32_t k) {
   uint32_t s = 16;
   while (s < want && s < 1024) s <<= 1;
   L.slots = s;
-  uint64_t ovf = (uint64_t)k * 4 + 65536;
-  uint64_t ord = (uint64_t)k * 8 + 131072;
+  // generous: a carried window (gtk_select_windowed) admits ~3k-9k keys, tens
+  // of k while a residual builds up; memory is cheap next to a dense fallback
+  uint64_t ovf = (uint64_t)k * 64 + 262144;
+  uint64_t ord = (uint64_t)k * 64 + 262144;
   if (ord > (uint64_t)m) ord = (uint64_t)m;
   if (ovf > (uint64_t)m) ovf = (uint64_t)m;
   L.ovf_cap = (uint32_t)ovf;
@@ -103,167 +112,272 @@ static SelectLayout select_layout(int64_t m, int32_t k) {
 }
 
 // ---------------------------------------------------------------------------
-// 1. sampling pass: per-block top-kSampleTop keys (exact, no atomics)
+// 1. sampling pass + threshold window (one launch)
 // ---------------------------------------------------------------------------
 // The threshold window must come from exact sample ORDER STATISTICS, not from
 // histogram bin edges: an accumulated residual develops a flat-topped
 // magnitude distribution (every entry grows until it is selected), where the
 // top k all lie within ~0.1% of tau -- a bin edge would admit a large fraction
 // of m as candidates.
+//
+// Each block keeps the exact top-kSampleTop keys of its 1024-element chunk;
+// the last block to finish (ticket counter) takes the exact order statistics
+// r_lo / r_hi of the union and publishes the window [lo, hi).
+
+// ---- exact order statistics by histogram levels ---------------------------
+// Three levels over the 31-bit key: bits 30..19 (4096 bins), 18..7 (4096
+// bins), 6..0 (128 bins).  Each level histograms the keys that share the
+// prefix resolved so far (plain shared atomics: a 12-bit digit spreads the
+// keys), one block scan over the bins (both statistics' counts packed in one
+// word) picks the digit.  Key 0 is "absent" (padding, zeros).
+constexpr int kLvlBins = 4096;
+struct LevelSmem {
+  uint32_t hist[2][kLvlBins];  // per statistic; [0] alone while the prefixes agree
+  uint32_t scan[kSampleThreads / 32 + 1];
+  uint32_t pre[2];  // resolved key prefix per statistic
+  uint32_t rem[2];  // rank still to find inside the prefix (0: fewer keys than the rank)
+};
+
+__device__ __forceinline__ void level_geom(int lvl, int& shift, uint32_t& mask, int& pshift) {
+  shift = lvl == 0 ? 19 : (lvl == 1 ? 7 : 0);
+  mask = lvl == 2 ? 0x7Fu : 0xFFFu;
+  pshift = lvl == 0 ? 31 : (lvl == 1 ? 19 : 7);
+}
+
+// out[s] = rank[s]-th largest nonzero key (rank >= 1) of the multiset the
+// block holds, 0 if there are fewer; for_each(f) calls f(key) for every key
+// of this thread.  ghist0 (nullable): level 0 already histogrammed in global
+// memory (read and re-zeroed here).  Precondition: sm.hist zero; kept zero.
+template <int NS, class ForEach>
+__device__ __forceinline__ void block_hist_select(const ForEach& for_each, const uint32_t (&rank)[NS],
+                                                  uint32_t (&out)[NS], LevelSmem& sm, uint32_t* ghist0,
+                                                  int64_t* tr = nullptr) {
+  auto stamp = [&](int i) {
+    if (tr && threadIdx.x == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      tr[i] = (int64_t)t;
+    }
+  };
+  static_assert(NS == 1 || NS == 2, "one or two statistics");
+  constexpr int NT = kSampleThreads;
+  constexpr int PER = kLvlBins / NT;  // bins per thread in the scan
+  static_assert(PER == 4, "scan layout");
+  if (threadIdx.x < NS) {
+    sm.pre[threadIdx.x] = 0;
+    sm.rem[threadIdx.x] = rank[threadIdx.x];
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int lvl = 0; lvl < 3; ++lvl) {
+    int shift, pshift;
+    uint32_t mask;
+    level_geom(lvl, shift, mask, pshift);
+    uint32_t pre[NS], rem[NS];
+    bool live[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      pre[s] = sm.pre[s];
+      rem[s] = sm.rem[s];
+      live[s] = rem[s] != 0;
+    }
+    const bool shared = NS == 1 || (live[0] && live[NS - 1] && pre[0] == pre[NS - 1]) || !live[NS - 1];
+    const bool from_global = lvl == 0 && ghist0 != nullptr;
+    if (!from_global) {
+      for_each([&](uint32_t key) {
+        if (key == 0) return;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          if (s > 0 && shared) break;
+          const int ss = shared ? 0 : s;
+          const bool lv = shared ? live[0] || live[NS - 1] : live[s];
+          const uint32_t p = shared ? (live[0] ? pre[0] : pre[NS - 1]) : pre[s];
+          if (lv && (lvl == 0 || (key >> pshift) == (p >> pshift))) atomicAdd(&sm.hist[ss][(key >> shift) & mask], 1u);
+        }
+      });
+      __syncthreads();
+    }
+    stamp(2 * lvl);
+    // thread t owns bins nb-4(t+1) .. nb-4t-1, read top-down
+    const int nb = (int)mask + 1;
+    const int b0 = nb - PER * ((int)threadIdx.x + 1);
+    uint32_t c[PER];  // packed: low 16 bits hist[0], high 16 bits hist[1]
+    uint32_t sum = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int b = b0 + (PER - 1 - j);
+      uint32_t v = 0;
+      if (b >= 0) {
+        if (from_global) {
+          v = __ldcg(ghist0 + b);
+          ghist0[b] = 0u;
+        } else {
+          v = sm.hist[0][b];
+          sm.hist[0][b] = 0u;
+          if (!shared) {
+            v |= sm.hist[NS - 1][b] << 16;
+            sm.hist[NS - 1][b] = 0u;
+          }
+        }
+      }
+      c[j] = v;
+      sum += v;
+    }
+    uint32_t tot;
+    const uint32_t above = block_excl_scan<NT>(sum, sm.scan, &tot);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (!live[s]) continue;
+      const int sh = (shared || s == 0) ? 0 : 16;
+      const uint32_t m16 = shared ? 0xFFFFFFFFu : 0xFFFFu;
+      const uint32_t r = rem[s];
+      const uint32_t my_above = (above >> sh) & m16, my_sum = (sum >> sh) & m16, total = (tot >> sh) & m16;
+      if (total < r) {
+        if (threadIdx.x == 0) sm.rem[s] = 0;
+      } else if (my_above < r && my_above + my_sum >= r) {
+        uint32_t acc = my_above;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+          const uint32_t cj = (c[j] >> sh) & m16;
+          if (acc + cj >= r) {
+            const uint32_t digit = (uint32_t)(b0 + (PER - 1 - j));
+            sm.pre[s] = pre[s] | (digit << shift);
+            sm.rem[s] = r - acc;
+            break;
+          }
+          acc += cj;
+        }
+      }
+    }
+    __syncthreads();
+    stamp(2 * lvl + 1);
+  }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) out[s] = sm.rem[s] ? sm.pre[s] : 0u;
+}
+
 struct SampleArgs {
   const float* res;
   const float* grad;
   uint32_t m;
-  uint32_t stride;  // elements between chunk starts
-  uint32_t* top;    // [nchunks][kSampleTop] block-local top keys (0-padded)
+  uint32_t stride;       // elements between chunk starts
+  uint32_t nchunks;      // blocks
+  uint32_t r_lo;         // sample rank (from top) whose key becomes lo
+  uint32_t r_hi;         // sample rank whose key (+1) becomes hi
+  uint32_t force_exact;  // 1 -> lo = 0x7FFFFFFF (forces the dense fallback)
+  uint32_t* top;         // [nchunks][kSampleTop] block-local top keys (0-padded)
+  const uint32_t* window; // nullable: {valid | level << 8, lo, shift, k, tau} left by the previous call
+  uint32_t k;
+  SelectCtl* ctl;
+  EngineWS* ews;
+  int64_t* trace;  // optional stamps: [0..3] block 0 phases, [4..6] last block phases
 };
 
-// The r1-th and r2-th largest of the keys held by the block (NT threads x PER
-// keys each) in one bitwise binary search on counts (both counts packed in
-// one word: fewer than 2^16 keys); r >= 1.  A rank beyond the number of
-// nonzero keys yields 0.
-template <int NT, int PER>
-__device__ __forceinline__ uint2 block_rank_keys(const uint32_t (&keys)[PER], uint32_t r1, uint32_t r2,
-                                                 uint32_t (&red)[2][NT / 32]) {
-  static_assert(NT * PER < 65536, "packed 16-bit counts");
-  uint32_t p1 = 0, p2 = 0;
-#pragma unroll 1
-  for (int bit = 30; bit >= 0; --bit) {
-    const uint32_t c1 = p1 | (1u << bit), c2 = p2 | (1u << bit);
-    uint32_t c = 0;
-#pragma unroll
-    for (int j = 0; j < PER; ++j) c += (keys[j] >= c1 ? 1u : 0u) + (keys[j] >= c2 ? 0x10000u : 0u);
-    c = warp_sum(c);
-    uint32_t* rb = red[bit & 1];  // double-buffered: one barrier per iteration
-    if (lane_id() == 0) rb[warp_id()] = c;
-    __syncthreads();
-    uint32_t tot = lane_id() < (unsigned)(NT / 32) ? rb[lane_id()] : 0u;
-    tot = warp_sum(tot);
-    if ((tot & 0xFFFFu) >= r1) p1 = c1;
-    if ((tot >> 16) >= r2) p2 = c2;
+__device__ __forceinline__ void sample_stamp(const SampleArgs& a, int i, bool who) {
+  if (a.trace && who && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[i] = (int64_t)t;
   }
-  return make_uint2(p1, p2);
-}
-
-// r-th largest of the keys held by one warp (32 lanes x PER keys), bitwise
-// binary search on warp-reduced counts; 0 if fewer than r nonzero keys.
-template <int PER>
-__device__ __forceinline__ uint32_t warp_rank_key(const uint32_t (&keys)[PER], uint32_t r) {
-  uint32_t p = 0;
-#pragma unroll 1
-  for (int bit = 30; bit >= 0; --bit) {
-    const uint32_t cand = p | (1u << bit);
-    uint32_t c = 0;
-#pragma unroll
-    for (int j = 0; j < PER; ++j) c += keys[j] >= cand;
-    if (warp_sum(c) >= r) p = cand;
-  }
-  return p;
-}
-
-// Write the warp's kSampleTop largest keys (all keys > th, then keys == th,
-// order irrelevant, zero-padded) to out[0..kSampleTop).
-template <int PER>
-__device__ __forceinline__ void warp_emit_top(const uint32_t (&keys)[PER], uint32_t th, uint32_t* out) {
-  const unsigned lane = lane_id();
-  uint32_t n = 0;
-#pragma unroll
-  for (int pass = 0; pass < 2; ++pass) {
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const bool f = pass == 0 ? keys[j] > th : (keys[j] == th && th > 0);
-      const unsigned bal = __ballot_sync(kFull, f);
-      const uint32_t pos = n + __popc(bal & lanemask_lt());
-      if (f && pos < (uint32_t)kSampleTop) out[pos] = keys[j];
-      n += __popc(bal);
-    }
-  }
-  for (uint32_t p = n + lane; p < (uint32_t)kSampleTop; p += 32) out[p] = 0;
 }
 
 __global__ void __launch_bounds__(kSampleThreads) select_sample_kernel(SampleArgs a) {
-  __shared__ uint32_t s_wtop[kSampleThreads / 32][kSampleTop];
-  pdl_launch_dependents();  // the window kernel may launch (it waits for us)
-  const uint64_t e0 = (uint64_t)blockIdx.x * a.stride + threadIdx.x * 4;
-  float x[4];
-  if (e0 + 4 <= a.m) {
-    float4 g4 = ld_stream4(a.grad + e0);
-    if (a.res) {
-      const float4 r4 = ld_stream4(a.res + e0);
-      g4.x = __fadd_rn(r4.x, g4.x);
-      g4.y = __fadd_rn(r4.y, g4.y);
-      g4.z = __fadd_rn(r4.z, g4.z);
-      g4.w = __fadd_rn(r4.w, g4.w);
-    }
-    x[0] = g4.x;
-    x[1] = g4.y;
-    x[2] = g4.z;
-    x[3] = g4.w;
-  } else {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint64_t e = e0 + j;
-      float v = 0.0f;
-      if (e < a.m) {
-        v = a.grad[e];
-        if (a.res) v = __fadd_rn(a.res[e], v);
+  __shared__ LevelSmem sm;
+  __shared__ uint32_t s_n, s_last;
+  // the previous kernel (K3 of the last step) writes res: wait for it before
+  // reading, and only then let the main pass launch (its early loads read res)
+  pdl_wait();
+  pdl_launch_dependents();
+  if (a.window && !a.force_exact && (__ldcg(a.window) & 1u) && __ldcg(a.window + 3) == a.k) {
+    // the previous call of this parameter measured the window: no sampling
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+      if (threadIdx.x < kRounds) a.ews->gather_n[threadIdx.x] = 0;
+      if (threadIdx.x == 0) {
+        SelectCtl* ctl = a.ctl;
+        ctl->lo = __ldcg(a.window + 1);
+        ctl->shift = __ldcg(a.window + 2);
+        ctl->ovf_cursor = 0;
+        ctl->overflow = 0;
+        ctl->nonfinite = 0;
       }
-      x[j] = v;
     }
+    return;
   }
-  uint32_t key[4];
+  sample_stamp(a, 0, blockIdx.x == 0);
+  {
+    uint4* h = reinterpret_cast<uint4*>(&sm.hist[0][0]);
+    for (int i = threadIdx.x; i < 2 * kLvlBins / 4; i += kSampleThreads) h[i] = make_uint4(0, 0, 0, 0);
+  }
+  if (threadIdx.x == 0) s_n = 0;
+  const uint64_t e = (uint64_t)blockIdx.x * a.stride + threadIdx.x;
+  uint32_t key = 0;
+  if (e < a.m) {
+    float x = __ldcs(a.grad + e);
+    if (a.res) x = __fadd_rn(__ldcs(a.res + e), x);
+    const uint32_t kk = key_of(x);
+    key = kk < kInfKey ? kk : 0u;  // non-finite: ignored (K1 reports it)
+  }
+  sample_stamp(a, 1, blockIdx.x == 0);
+  // the chunk's kSampleTop-th key, then its top keys: > th first, == th to the cap
+  const uint32_t rk[1] = {(uint32_t)kSampleTop};
+  uint32_t th[1];
+  block_hist_select<1>([&](auto&& f) { f(key); }, rk, th, sm, nullptr,
+                       (a.trace && blockIdx.x == 0) ? a.trace + 8 : nullptr);
+  sample_stamp(a, 2, blockIdx.x == 0);
+  uint32_t* out = a.top + (size_t)blockIdx.x * kSampleTop;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t kk = key_of(x[j]);
-    key[j] = kk < kInfKey ? kk : 0u;  // non-finite: ignored (K1 reports it)
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool f = key != 0 && (pass == 0 ? key > th[0] : key == th[0]);
+    const unsigned bal = __ballot_sync(kFull, f);
+    uint32_t base = 0;
+    if (lane_id() == 0 && bal) base = atomicAdd(&s_n, (uint32_t)__popc(bal));
+    base = __shfl_sync(kFull, base, 0);
+    const uint32_t pos = base + __popc(bal & lanemask_lt());
+    if (f && pos < (uint32_t)kSampleTop) out[pos] = key;
+    __syncthreads();
   }
-  // level 1: each warp's top-32 of its 128 keys (warp-only search, no barrier)
-  const uint32_t wth = warp_rank_key<4>(key, kSampleTop);
-  uint32_t* wtop = s_wtop[warp_id()];
-  warp_emit_top<4>(key, wth, wtop);
+  if (threadIdx.x < (unsigned)kSampleTop && threadIdx.x >= s_n) out[threadIdx.x] = 0u;
+
+  // ticket: the last block to arrive computes the window (the barrier orders
+  // the block's writes before thread 0's acq_rel ticket; atom.inc wraps the
+  // counter back to 0, so every complete launch leaves it clean)
   __syncthreads();
-  // level 2: warp 0 takes the block's top-32 of the 8 x 32 warp winners
-  if (warp_id() == 0) {
-    uint32_t k2[kSampleThreads / 32];
+  if (threadIdx.x == 0) s_last = atom_inc_acq_rel_gpu(&a.ctl->sample_done, a.nchunks - 1) == a.nchunks - 1;
+  __syncthreads();
+  sample_stamp(a, 3, blockIdx.x == 0);
+  if (!s_last) return;
+  sample_stamp(a, 4, true);
+  const uint32_t nkeys = a.nchunks * kSampleTop;
+  const uint32_t rk2[2] = {a.r_lo, a.r_hi};
+  uint32_t kk[2];
+  constexpr int kRegKeys = 4;
+  if (nkeys <= (uint32_t)(kSampleThreads * kRegKeys)) {
+    uint32_t k2[kRegKeys];
 #pragma unroll
-    for (int w = 0; w < kSampleThreads / 32; ++w) k2[w] = s_wtop[w][lane_id()];
-    const uint32_t bth = warp_rank_key<kSampleThreads / 32>(k2, kSampleTop);
-    warp_emit_top<kSampleThreads / 32>(k2, bth, a.top + (size_t)blockIdx.x * kSampleTop);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// 2. threshold window (one block): exact sample ranks r_lo / r_hi
-// ---------------------------------------------------------------------------
-constexpr int kWindowThreads = 512;  // x PER keys each, PER in {8, 16, 32, 64} by sample size
-
-struct WindowArgs {
-  uint32_t r_lo;         // sample rank (from top) whose key becomes lo
-  uint32_t r_hi;         // sample rank whose key (+1) becomes hi
-  uint32_t nkeys;        // nchunks * kSampleTop
-  uint32_t force_exact;  // 1 -> lo = 0x7FFFFFFF (forces the dense fallback)
-  SelectCtl* ctl;
-  const uint32_t* top;
-  EngineWS* ews;
-};
-
-template <int PER>
-__global__ void __launch_bounds__(kWindowThreads) select_window_kernel(WindowArgs a) {
-  __shared__ uint32_t red[2][kWindowThreads / 32];
-  pdl_launch_dependents();  // the main pass may launch and start streaming its tiles
-  pdl_wait();               // the sample tops are complete
-  uint32_t key[PER];
+    for (int j = 0; j < kRegKeys; ++j) {
+      const uint32_t i = j * kSampleThreads + threadIdx.x;
+      k2[j] = i < nkeys ? __ldcg(a.top + i) : 0u;
+    }
+    sample_stamp(a, 5, true);
+    block_hist_select<2>(
+        [&](auto&& f) {
 #pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    const uint32_t i = j * kWindowThreads + threadIdx.x;
-    key[j] = i < a.nkeys ? __ldcg(a.top + i) : 0u;
+          for (int j = 0; j < kRegKeys; ++j) f(k2[j]);
+        },
+        rk2, kk, sm, nullptr, a.trace ? a.trace + 16 : nullptr);
+  } else {  // large samples: re-read the keys from L2 per level
+    block_hist_select<2>(
+        [&](auto&& f) {
+#pragma unroll 4
+          for (uint32_t i = threadIdx.x; i < nkeys; i += kSampleThreads) f(__ldcg(a.top + i));
+        },
+        rk2, kk, sm, nullptr);
   }
-  const uint2 kk = block_rank_keys<kWindowThreads, PER>(key, a.r_lo, a.r_hi, red);
-  const uint32_t klo = kk.x, khi = kk.y;
+  sample_stamp(a, 6, true);
   if (threadIdx.x < kRounds) a.ews->gather_n[threadIdx.x] = 0;  // the finish engine's counters
   if (threadIdx.x == 0) {
-    uint32_t lo = klo;  // 0 when the sample holds fewer than r_lo nonzero keys: take all
-    uint32_t hi = khi >= lo ? khi + 1 : lo + 1;
+    uint32_t lo = kk[0];  // 0 when the sample holds fewer than r_lo nonzero keys: take all
+    uint32_t hi = kk[1] >= lo ? kk[1] + 1 : lo + 1;
     if (a.force_exact) {
       lo = 0x7FFFFFFFu;
       hi = 0x80000000u;
@@ -280,7 +394,7 @@ __global__ void __launch_bounds__(kWindowThreads) select_window_kernel(WindowArg
 }
 
 // ---------------------------------------------------------------------------
-// 3. main HBM pass
+// 2. main HBM pass
 // ---------------------------------------------------------------------------
 struct MainArgs {
   const float* res;  // nullable
@@ -299,70 +413,26 @@ struct MainArgs {
   uint32_t* whist;  // engine round-0 histogram [kHistLen]
 };
 
-__global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
-  __shared__ uint32_t s_wt[kMainVec * 8];  // per (vec, warp) candidate totals -> offsets
-  __shared__ uint32_t s_total;
-  __shared__ int32_t* s_didx;
-  __shared__ float* s_dval;
-  __shared__ uint32_t s_nonfinite;
+// v[b >> 2][b & 3] without a dynamically indexed (local-memory) array
+__device__ __forceinline__ float pick(const float (&v)[kMainVec][4], int b) {
+  float x = v[0][0];
+#pragma unroll
+  for (int i = 1; i < kMainVec * 4; ++i) x = b == i ? v[i >> 2][i & 3] : x;
+  return x;
+}
 
-  const uint32_t tile = blockIdx.x;
+// Everything after the loads for one tile whose acc values this thread holds
+// (v[q][j] is element (q * 256 + tid) * 4 + j): candidate flags, index-ordered
+// compaction into the tile's slot row (or the overflow region for a dense
+// tile) and the window histogram.  One block barrier (three for a dense tile);
+// the shared scratch alternates with `par` between a block's tiles.
+__device__ __forceinline__ void main_tile(const MainArgs& a, uint32_t tile, const float (&v)[kMainVec][4], bool full,
+                                          uint32_t lo, uint32_t shift, int par, uint32_t (&s_wt)[2][16],
+                                          int32_t* (&s_didx)[2], float* (&s_dval)[2], uint32_t* s_hist) {
   const uint64_t tbase = (uint64_t)tile * kTile;
   const unsigned lane = lane_id(), w = warp_id();
-  if (threadIdx.x == 0) s_nonfinite = 0;
-
-  float v[kMainVec][4];
-  const bool full = tbase + kTile <= a.m;
-  if (full) {
-    float4 gv[kMainVec], rv[kMainVec];
-#pragma unroll
-    for (int q = 0; q < kMainVec; ++q) {
-      const uint64_t e = tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4;
-      gv[q] = ld_stream4(a.grad + e);
-      if (a.res) rv[q] = ld_stream4(a.res + e);
-    }
-    // everything below consumes the window kernel's results (and may write
-    // res_out = res in place, which the sample kernel reads): wait for it --
-    // the loads above are already in flight (programmatic dependent launch)
-    pdl_wait();
-#pragma unroll
-    for (int q = 0; q < kMainVec; ++q) {
-      float4 x = gv[q];
-      if (a.res) {
-        x.x = __fadd_rn(rv[q].x, x.x);
-        x.y = __fadd_rn(rv[q].y, x.y);
-        x.z = __fadd_rn(rv[q].z, x.z);
-        x.w = __fadd_rn(rv[q].w, x.w);
-      }
-      const uint64_t e = tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4;
-      st_stream4(a.res_out + e, x);
-      v[q][0] = x.x;
-      v[q][1] = x.y;
-      v[q][2] = x.z;
-      v[q][3] = x.w;
-    }
-  } else {
-    pdl_wait();
-#pragma unroll
-    for (int q = 0; q < kMainVec; ++q)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint64_t e = tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4 + j;
-        float x = 0.0f;
-        if (e < a.m) {
-          x = a.grad[e];
-          if (a.res) x = __fadd_rn(a.res[e], x);
-          a.res_out[e] = x;
-        }
-        v[q][j] = x;
-      }
-  }
-  const uint32_t lo = __ldcg(&a.ctl->lo);  // issued after the tile loads: off the critical path
-  const uint32_t shift = __ldcg(&a.ctl->shift);
-  __syncthreads();  // s_nonfinite init visible
-
-  // candidate flags, non-finite check, window histogram
-  uint32_t flags = 0;  // bit q*4+j
+  // candidate flags (bit q*4+j) and the non-finite check
+  uint32_t flags = 0;
   bool nonfinite = false;
 #pragma unroll
   for (int q = 0; q < kMainVec; ++q)
@@ -372,81 +442,179 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
       const uint32_t key = key_of(v[q][j]);
       const bool in = full || e < a.m;
       nonfinite |= in && key >= kInfKey;
-      if (in && key >= lo) {
-        flags |= 1u << (q * 4 + j);
-        atomicAdd(a.whist + min((uint32_t)kBins, (key - lo) >> shift), 1u);
-      }
+      if (in && key >= lo) flags |= 1u << (q * 4 + j);
     }
-  if (__any_sync(kFull, nonfinite) && lane == 0) s_nonfinite = 1;
+  if (__any_sync(kFull, nonfinite) && lane == 0) a.ctl->nonfinite = 1u;
 
-  // in-tile, index-ordered offsets: order is (q, warp, lane, j)
-  uint32_t lane_pre[kMainVec];
+  // index-ordered in-tile offsets, order (q, warp, lane, j): per-lane counts of
+  // the four q segments packed two per word (16-bit fields: a warp's segment
+  // holds <= 128, a tile's <= 1024), one warp scan per word
+  const uint32_t c01 = __popc(flags & 0xFu) | (__popc(flags & 0xF0u) << 16);
+  const uint32_t c23 = __popc(flags & 0xF00u) | (__popc(flags & 0xF000u) << 16);
+  uint32_t i01 = c01, i23 = c23;
 #pragma unroll
-  for (int q = 0; q < kMainVec; ++q) {
-    uint32_t pre = 0, tot = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const unsigned bal = __ballot_sync(kFull, (flags >> (q * 4 + j)) & 1u);
-      pre += __popc(bal & lanemask_lt());
-      tot += __popc(bal);
-    }
-    lane_pre[q] = pre;
-    if (lane == 0) s_wt[q * 8 + w] = tot;
-  }
-  __syncthreads();
-  if (w == 0) {
-    const uint32_t x = s_wt[lane];
-    uint32_t incl = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, incl, o);
-      if (lane >= (unsigned)o) incl += y;
-    }
-    s_wt[lane] = incl - x;
-    const uint32_t total = __shfl_sync(kFull, incl, 31);
-    if (lane == 0) {
-      s_total = total;
-      uint32_t info = total;
-      int32_t* didx = a.slot_idx + (size_t)tile * a.slots;
-      float* dval = a.slot_val + (size_t)tile * a.slots;
-      if (total > a.slots) {  // dense tile: reserve overflow space
-        const uint32_t base = atomicAdd(&a.ctl->ovf_cursor, total);
-        if (base + total > a.ovf_cap) {
-          a.ctl->overflow = 1;
-          didx = nullptr;
-        } else {
-          didx = a.ovf_idx + base;
-          dval = a.ovf_val + base;
-        }
-        a.tile_ovf[tile] = base;
-        info |= kOvfBit;
-      }
-      a.tile_info[tile] = info;
-      s_didx = didx;
-      s_dval = dval;
-      if (s_nonfinite) a.ctl->nonfinite = 1;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y01 = __shfl_up_sync(kFull, i01, o), y23 = __shfl_up_sync(kFull, i23, o);
+    if (lane >= (unsigned)o) {
+      i01 += y01;
+      i23 += y23;
     }
   }
+  if (lane == 31) {
+    s_wt[par][2 * w] = i01;  // warp totals per q
+    s_wt[par][2 * w + 1] = i23;
+  }
   __syncthreads();
-  int32_t* didx = s_didx;
-  float* dval = s_dval;
-  if (s_total == 0 || didx == nullptr) return;
+  // every warp derives its segment bases from the 8 warps' totals: no second barrier
+  uint32_t before01 = 0, before23 = 0, all01 = 0, all23 = 0;
 #pragma unroll
-  for (int q = 0; q < kMainVec; ++q) {
-    uint32_t pos = s_wt[q * 8 + w] + lane_pre[q];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if ((flags >> (q * 4 + j)) & 1u) {
-        didx[pos] = (int32_t)(tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4 + j);
-        dval[pos] = v[q][j];
-        ++pos;
+  for (int ww = 0; ww < 8; ++ww) {
+    const uint32_t t01 = s_wt[par][2 * ww], t23 = s_wt[par][2 * ww + 1];
+    if (ww < (int)w) {
+      before01 += t01;
+      before23 += t23;
+    }
+    all01 += t01;
+    all23 += t23;
+  }
+  const uint32_t T0 = all01 & 0xFFFFu, T1 = all01 >> 16, T2 = all23 & 0xFFFFu, T3 = all23 >> 16;
+  const uint32_t total = T0 + T1 + T2 + T3;
+  // base of (q, this lane): segment start + earlier warps + earlier lanes
+  const uint32_t e01 = i01 - c01, e23 = i23 - c23;
+  const uint32_t base[kMainVec] = {(before01 & 0xFFFFu) + (e01 & 0xFFFFu),
+                                   T0 + (before01 >> 16) + (e01 >> 16),
+                                   T0 + T1 + (before23 & 0xFFFFu) + (e23 & 0xFFFFu),
+                                   T0 + T1 + T2 + (before23 >> 16) + (e23 >> 16)};
+  if (total == 0) {
+    if (threadIdx.x == 0) a.tile_info[tile] = 0u;
+    return;
+  }
+  int32_t* didx = a.slot_idx + (size_t)tile * a.slots;
+  float* dval = a.slot_val + (size_t)tile * a.slots;
+  const bool dense = total > a.slots;
+  if (dense) {  // reserve overflow space (uniform branch)
+    if (threadIdx.x == 0) {
+      const uint32_t b = atomicAdd(&a.ctl->ovf_cursor, total);
+      if (b + total > a.ovf_cap) {
+        a.ctl->overflow = 1u;
+        s_didx[par] = nullptr;
+      } else {
+        s_didx[par] = a.ovf_idx + b;
+        s_dval[par] = a.ovf_val + b;
       }
+      a.tile_ovf[tile] = b;
+    }
+    __syncthreads();
+    didx = s_didx[par];
+    dval = s_dval[par];
+  }
+  if (threadIdx.x == 0) a.tile_info[tile] = total | (dense ? kOvfBit : 0u);
+  // my candidates (set bits only), and -- for a sparse tile -- their histogram
+  // bins straight to the global window histogram
+  const bool hist_direct = total <= (uint32_t)kMainDenseHist;
+  for (uint32_t f = flags; f; f &= f - 1) {
+    const int b = __ffs(f) - 1;
+    const int q = b >> 2, j = b & 3;
+    const float x = pick(v, b);
+    if (didx) {
+      const uint32_t bq = q == 0 ? base[0] : q == 1 ? base[1] : q == 2 ? base[2] : base[3];
+      const uint32_t pos = bq + __popc(flags & ((1u << b) - 1u) & (0xFu << (4 * q)));
+      didx[pos] = (int32_t)(tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4 + j);
+      dval[pos] = x;
+    }
+    if (hist_direct) atomicAdd(a.whist + min((uint32_t)kBins, (key_of(x) - lo) >> shift), 1u);
+  }
+  if (!hist_direct) {
+    // dense tile (a wide window, e.g. while a residual builds up): a shared
+    // histogram first, so a hot bin costs one global atomic per tile
+    for (int b = threadIdx.x; b < kHistLen; b += kMainThreads) s_hist[b] = 0u;
+    __syncthreads();
+    for (uint32_t f = flags; f; f &= f - 1) {
+      const int b = __ffs(f) - 1;
+      atomicAdd(&s_hist[min((uint32_t)kBins, (key_of(pick(v, b)) - lo) >> shift)], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kHistLen; b += kMainThreads) {
+      const uint32_t c = s_hist[b];
+      if (c) atomicAdd(a.whist + b, c);
     }
   }
 }
 
+
+__global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
+  __shared__ uint32_t s_wt[2][16];  // per warp: packed candidate totals of the q segments
+  __shared__ int32_t* s_didx[2];
+  __shared__ float* s_dval[2];
+  __shared__ uint32_t s_hist[kHistLen];  // dense tiles only
+  pdl_launch_dependents();  // the finish grid may become resident as our last wave drains
+
+  // all of this block's tiles are loaded before any is processed: more bytes
+  // in flight per resident block
+  const uint32_t t0 = blockIdx.x * kMainTilesPerBlock;
+  float4 gv[kMainTilesPerBlock][kMainVec], rv[kMainTilesPerBlock][kMainVec];
+#pragma unroll
+  for (int u = 0; u < kMainTilesPerBlock; ++u) {
+    const uint64_t tbase = (uint64_t)(t0 + u) * kTile;
+    if (tbase + kTile <= a.m) {
+#pragma unroll
+      for (int q = 0; q < kMainVec; ++q) {
+        const uint64_t e = tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4;
+        gv[u][q] = ld_stream4(a.grad + e);
+        if (a.res) rv[u][q] = ld_stream4(a.res + e);
+      }
+    }
+  }
+  // everything below consumes the sample kernel's window (and may write
+  // res_out = res in place, which the sample kernel reads): wait for it --
+  // the loads above are already in flight (programmatic dependent launch)
+  pdl_wait();
+  const uint32_t lo = __ldcg(&a.ctl->lo);
+  const uint32_t shift = __ldcg(&a.ctl->shift);
+#pragma unroll
+  for (int u = 0; u < kMainTilesPerBlock; ++u) {
+    const uint32_t tile = t0 + u;
+    const uint64_t tbase = (uint64_t)tile * kTile;
+    if (tbase >= a.m) break;
+    float v[kMainVec][4];
+    const bool full = tbase + kTile <= a.m;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < kMainVec; ++q) {
+        float4 x = gv[u][q];
+        if (a.res) {
+          x.x = __fadd_rn(rv[u][q].x, x.x);
+          x.y = __fadd_rn(rv[u][q].y, x.y);
+          x.z = __fadd_rn(rv[u][q].z, x.z);
+          x.w = __fadd_rn(rv[u][q].w, x.w);
+        }
+        st_stream4(a.res_out + tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4, x);
+        v[q][0] = x.x;
+        v[q][1] = x.y;
+        v[q][2] = x.z;
+        v[q][3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < kMainVec; ++q)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t e = tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4 + j;
+          float x = 0.0f;
+          if (e < a.m) {
+            x = a.grad[e];
+            if (a.res) x = __fadd_rn(a.res[e], x);
+            a.res_out[e] = x;
+          }
+          v[q][j] = x;
+        }
+    }
+    main_tile(a, tile, v, full, lo, shift, u & 1, s_wt, s_didx, s_dval, s_hist);
+  }
+}
+
 // ---------------------------------------------------------------------------
-// 4. finish: per-block candidate slices in smem, exact engine / dense fallback
+// 3. finish: per-block candidate slices in smem, exact engine / dense fallback
 // ---------------------------------------------------------------------------
 struct FinishArgs {
   float* res_out;
@@ -470,6 +638,7 @@ struct FinishArgs {
   int32_t* d_count;
   uint32_t* d_status;
   int64_t* trace;  // optional phase stamps (block 0): [0] start [1] scanned [2] copied [3..6] engine
+  uint32_t* window;  // nullable: {valid | level << 8, lo, shift, k, tau} for the next call (written here)
 };
 
 __device__ __forceinline__ void finish_stamp(const FinishArgs& a, int i) {
@@ -485,14 +654,27 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
   __shared__ int32_t s_idx[kSliceCap];
   __shared__ float s_val[kSliceCap];
   const unsigned G = gridDim.x, blk = blockIdx.x;
+  pdl_wait();  // launched programmatically behind the main pass
+  pdl_launch_dependents();
+  // margin level of the carried window (only block 0 writes the record)
+  const uint32_t wlevel = (a.window && blk == 0) ? min(kMaxWindowLevel, max(kMinWindowLevel, __ldcg(a.window) >> 8)) : kMinWindowLevel;
+  const bool wsame = a.window && blk == 0 && __ldcg(a.window + 3) == a.k;
+  const uint32_t wtau = wsame ? __ldcg(a.window + 4) : 0u, wtau2 = wsame ? __ldcg(a.window + 5) : 0u;
   if (__ldcg(&a.ctl->nonfinite)) {
     if (blk == 0) {
       for (int b = threadIdx.x; b < kHistLen; b += kFinishThreads) a.ews->hist[0][b] = 0;
-      if (threadIdx.x == 0) atomicOr(a.d_status, GTK_DEV_NONFINITE);
+      if (threadIdx.x == 0) {
+        atomicOr(a.d_status, GTK_DEV_NONFINITE);
+        if (a.window) {
+          a.window[0] = wlevel << 8;
+          a.window[4] = a.window[5] = 0u;
+        }
+      }
     }
     return;
   }
-  const Sink out{a.sel_idx, a.sel_val, a.d_count, a.res_out, true, a.trace ? a.trace + 3 : nullptr};
+  const Sink out{a.sel_idx, a.sel_val, a.d_count, a.res_out, true, a.trace ? a.trace + 3 : nullptr,
+                 a.window, wlevel, wtau, wtau2};
   finish_stamp(a, 0);
 
   // my tile range and its place in the global (index-ordered) candidate list
@@ -578,13 +760,24 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
     for (int r = 0; r < kRounds; ++r)
       for (int b = threadIdx.x; b < kHistLen; b += kFinishThreads) a.ews->hist[r][b] = 0;
     if (threadIdx.x < kRounds) a.ews->gather_n[threadIdx.x] = 0;
-    if (threadIdx.x == 0) atomicOr(a.d_status, GTK_DEV_FALLBACK);
+    if (threadIdx.x == 0) {
+      atomicOr(a.d_status, GTK_DEV_FALLBACK);
+      // the next call samples again; a window that admitted too few keys
+      // widens its margin from then on
+      const bool low_miss = !overflow && C < a.k;
+      if (a.window) {
+        a.window[0] = (low_miss ? min(kMaxWindowLevel, wlevel + 1) : wlevel) << 8;
+        a.window[4] = a.window[5] = 0u;  // no growth estimate across a gap
+      }
+    }
   }
   grid_sync(&a.ews->bar, G);
   DenseSrc dsrc{a.res_out};
   uint32_t s0, s1;
   slice_of(a.m, G, blk, s0, s1);
-  engine_run<kFinishThreads>(dsrc, s0, s1, a.k, false, 0u, 20u, nullptr, false, a.ews, sm, out, G);
+  Sink dout = out;
+  dout.next_window = nullptr;
+  engine_run<kFinishThreads>(dsrc, s0, s1, a.k, false, 0u, 20u, nullptr, false, a.ews, sm, dout, G);
 }
 
 }  // namespace gtk
@@ -600,6 +793,13 @@ extern "C" int gtk_select_workspace_bytes(int64_t m, int32_t k, size_t* bytes) {
 extern "C" int gtk_select(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
                           int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
                           size_t ws_bytes, int32_t flags, void* stream) {
+  return gtk_select_windowed(res_in, grad, res_out, m, k, sel_idx, sel_val, d_count, d_status, ws, ws_bytes, flags,
+                             nullptr, stream);
+}
+
+extern "C" int gtk_select_windowed(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
+                                   int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status,
+                                   void* ws, size_t ws_bytes, int32_t flags, uint32_t* d_window, void* stream) {
   if (!grad || !res_out || !sel_idx || !sel_val || !d_count || !d_status || !ws) return GTK_EINVAL;
   if (m < 1 || m >= (int64_t(1) << 31) || k < 1 || k > m) return GTK_EINVAL;
   const SelectLayout L = select_layout(m, k);
@@ -636,19 +836,10 @@ extern "C" int gtk_select(const float* res_in, const float* grad, float* res_out
     r_hi = rh < 1.0 ? 1u : (uint32_t)rh;
   }
   ProfScope prof_all(kProfSelect, st);
-  SampleArgs sa{res_in, grad, (uint32_t)m, stride, stop};
-  select_sample_kernel<<<nchunks, kSampleThreads, 0, st>>>(sa);
-  GTK_CHECK_LAUNCH();
-  WindowArgs wa{r_lo, r_hi, nchunks * (uint32_t)kSampleTop, (uint32_t)((flags & GTK_SELECT_FORCE_EXACT) ? 1 : 0),
-                ctl, stop, ews};
-  {
-    const uint32_t nk = wa.nkeys;
-    auto* wk = nk <= 8 * kWindowThreads    ? select_window_kernel<8>
-               : nk <= 16 * kWindowThreads ? select_window_kernel<16>
-               : nk <= 32 * kWindowThreads ? select_window_kernel<32>
-                                           : select_window_kernel<64>;
-    GTK_CUDA(launch_pdl(wk, dim3(1), dim3(kWindowThreads), 0, st, wa));
-  }
+  SampleArgs sa{res_in, grad, (uint32_t)m, stride, nchunks, r_lo, r_hi,
+                (uint32_t)((flags & GTK_SELECT_FORCE_EXACT) ? 1 : 0), stop, d_window, (uint32_t)k, ctl, ews,
+                trace_buffer() ? trace_buffer() + 64 : nullptr};
+  GTK_CUDA(launch_pdl(select_sample_kernel, dim3(nchunks), dim3(kSampleThreads), 0, st, sa));
   GTK_CHECK_LAUNCH();
 
   MainArgs ma{res_in,
@@ -667,7 +858,8 @@ extern "C" int gtk_select(const float* res_in, const float* grad, float* res_out
               ews->hist[0]};
   {
     ProfScope prof_main(kProfSelectMain, st);
-    GTK_CUDA(launch_pdl(select_main_kernel, dim3(L.ntiles), dim3(kMainThreads), 0, st, ma));
+    const uint32_t gmain = (L.ntiles + kMainTilesPerBlock - 1) / kMainTilesPerBlock;
+    GTK_CUDA(launch_pdl(select_main_kernel, dim3(gmain), dim3(kMainThreads), 0, st, ma));
     GTK_CHECK_LAUNCH();
   }
 
@@ -691,7 +883,8 @@ extern "C" int gtk_select(const float* res_in, const float* grad, float* res_out
                 sel_val,
                 d_count,
                 d_status,
-                trace_buffer() ? trace_buffer() + 48 : nullptr};
+                trace_buffer() ? trace_buffer() + 48 : nullptr,
+                d_window};
 
 
   int G = coop_grid((const void*)select_finish_kernel, kFinishThreads, 0);
@@ -704,5 +897,5 @@ extern "C" int gtk_select(const float* res_in, const float* grad, float* res_out
   if (G > num_sms()) G = num_sms();
   if (G > kMaxBlocks) G = kMaxBlocks;
   void* args[] = {&fa};
-  return coop_launch((const void*)select_finish_kernel, G, kFinishThreads, args, 0, st);
+  return coop_launch((const void*)select_finish_kernel, G, kFinishThreads, args, 0, st, true);
 }

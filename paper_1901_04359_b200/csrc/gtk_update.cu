@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(kUpdThreads)
     scatter_update_kernel(float* w, float* res, const int32_t* g_idx, const float* g_val, const int32_t* d_gn,
                           const int32_t* l_idx, const float* l_val, const int32_t* d_ln, float lr, float Pf,
                           int scaling, int do_weights, const uint32_t* d_skip) {
+  pdl_wait();  // launched programmatically behind the exchange / select
+  pdl_launch_dependents();
   if (skipped(d_skip)) return;
   const uint32_t gn = (uint32_t)__ldg(d_gn);
   const uint32_t ln = l_idx ? (uint32_t)__ldg(d_ln) : 0u;
@@ -72,6 +74,8 @@ __global__ void __launch_bounds__(kUpdThreads)
                         uint32_t m, float lr, float mom, float Pf, int scaling, const uint32_t* d_skip) {
   __shared__ float su[kDenseTile];
   __shared__ uint32_t s_rng[2];
+  pdl_wait();
+  pdl_launch_dependents();
   if (skipped(d_skip)) return;
   const uint32_t gn = (uint32_t)__ldg(d_gn);
   const uint32_t t0 = blockIdx.x * kDenseTile;
@@ -173,12 +177,15 @@ extern "C" int gtk_scatter_update(float* w, float* res, float* vel, const int32_
   if (momentum > 0.0f && !vel) return GTK_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   const float Pf = (float)P;
+  // the local list IS the global list (P = 1): no entry can miss the global set
+  if (l_idx == g_idx && l_val == g_val && d_ln == d_gn) l_idx = nullptr;
   const bool sparse_exact = momentum == 0.0f && std::isfinite(lr) && !std::signbit(lr);
   ProfScope prof(kProfUpdate, st);
   if (!sparse_exact) {
     const int tiles = (int)((m + kDenseTile - 1) / kDenseTile);
-    dense_update_kernel<<<tiles, kUpdThreads, 0, st>>>(w, momentum > 0.0f ? vel : nullptr, g_idx, g_val, d_gn,
-                                                        (uint32_t)m, lr, momentum, Pf, scaling, d_skip);
+    GTK_CUDA(launch_pdl(dense_update_kernel, dim3(tiles), dim3(kUpdThreads), 0, st, w,
+                        momentum > 0.0f ? vel : nullptr, g_idx, g_val, d_gn, (uint32_t)m, lr, momentum, Pf, scaling,
+                        d_skip));
     GTK_CHECK_LAUNCH();
     if (l_idx) {
       scatter_update_kernel<<<num_sms() * 2, kUpdThreads, 0, st>>>(w, res, g_idx, g_val, d_gn, l_idx, l_val, d_ln,
@@ -189,8 +196,8 @@ extern "C" int gtk_scatter_update(float* w, float* res, float* vel, const int32_
   }
   // k-length work: one launch updates w at the global entries and returns the
   // local entries that missed the global set to the residual
-  scatter_update_kernel<<<num_sms() * 2, kUpdThreads, 0, st>>>(w, res, g_idx, g_val, d_gn, l_idx, l_val, d_ln, lr,
-                                                                Pf, scaling, 1, d_skip);
+  GTK_CUDA(launch_pdl(scatter_update_kernel, dim3(num_sms() * 2), dim3(kUpdThreads), 0, st, w, res, g_idx, g_val,
+                      d_gn, l_idx, l_val, d_ln, lr, Pf, scaling, 1, d_skip));
   GTK_CHECK_LAUNCH();
   return GTK_OK;
 }

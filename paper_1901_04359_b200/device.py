@@ -144,17 +144,25 @@ def merge_workspace(cap: int, k: int, device) -> torch.Tensor:
 # ---------------------------------------------------------------------------
 
 
+def new_window(device) -> torch.Tensor:
+    """Per-parameter key-window record for select(window=...): uint32[8], zero
+    = none yet (gtk_select_windowed)."""
+    return torch.zeros(8, dtype=torch.int32, device=device)
+
+
 def select(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, out: DeviceList,
-           status: torch.Tensor, force_exact: bool = False) -> None:
+           status: torch.Tensor, force_exact: bool = False, window: torch.Tensor | None = None) -> None:
     """K1: res_out = res_in + grad (or grad), out = exact top-k of it, res_out
-    zeroed at the winners.  Stream-ordered, no host sync."""
+    zeroed at the winners.  Stream-ordered, no host sync.  `window` (from
+    new_window, one per parameter) carries the key window between the
+    successive selections of one residual; results are identical either way."""
     m = grad.numel()
     dev = grad.device
     ws = select_workspace(m, k, dev)
     _lib.call(
-        "gtk_select", P(res_in), P(grad), P(res_out), m, k, P(out.idx), P(out.val), P(out.count),
+        "gtk_select_windowed", P(res_in), P(grad), P(res_out), m, k, P(out.idx), P(out.val), P(out.count),
         P(status), P(ws), ctypes.c_size_t(ws.numel()),
-        _lib.SELECT_FORCE_EXACT if force_exact else 0, stream_of(dev),
+        _lib.SELECT_FORCE_EXACT if force_exact else 0, P(window), stream_of(dev),
     )
 
 

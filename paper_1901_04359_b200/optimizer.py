@@ -268,7 +268,10 @@ def _select_checked(state, g, k, sel: DeviceList, status) -> None:
     m = state.m
     if not 1 <= k <= m:
         raise ValueError(f"k must be in [1, {m}], got {k}")
-    _dev.select(state._res, g, state._res2, k, sel, status[0:1])
+    win = getattr(state, "_window", None)
+    if win is None or win.device != g.device:
+        win = state._window = _dev.new_window(g.device)  # this residual's key window (K1 hint)
+    _dev.select(state._res, g, state._res2, k, sel, status[0:1], window=win)
 
 
 def _finish(status, count_src) -> tuple[int, int]:

@@ -55,6 +55,7 @@ class GTopKPipeline:
         self.res = [state._res, state._res2]
         self.sel = DeviceList(self.m, self.k, self.dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.window = _dev.new_window(self.dev)  # K1 key window carried between steps
         self.lr = float(np.float32(state.lr))
         self.mom = float(np.float32(state.momentum))
         self.scaling = _scaling_code(state)
@@ -72,7 +73,7 @@ class GTopKPipeline:
     def _enqueue(self, parity: int) -> None:
         grad = self.grads[parity % len(self.grads)]
         res_in, res_out = self.res[parity], self.res[1 - parity]
-        _dev.select(res_in, grad, res_out, self.k, self.sel, self.status)
+        _dev.select(res_in, grad, res_out, self.k, self.sel, self.status, window=self.window)
         if self.P > 1:
             self.group.enqueue_exchange(self.plan, self.sel, self.status)
             glist = self.plan.acc
@@ -125,6 +126,38 @@ class GTopKPipeline:
         if os.environ.get("GTK_PROF_DEBUG"):
             print("profile (ms per launch):", out, flush=True)
         return out
+
+    def profile_graph(self, steps: int = 20) -> dict:
+        """Per-stage device time (ms) from CUDA event nodes captured around
+        each launch inside a step graph, replayed `steps` times and read back
+        after each replay.  Event nodes serialise the launches they bracket,
+        so each stage is timed alone (no overlap with its neighbours).  Every
+        replay repeats the same step from the same residual (res[p] ->
+        res[1-p]); the weights take `steps` updates (a measurement tool)."""
+        lib = _lib.load()
+        torch.cuda.synchronize(self.dev)
+        lib.gtk_prof_reset()
+        lib.gtk_prof_enable(1)
+        stream = torch.cuda.Stream(self.dev)
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                self._enqueue(self.t % 2)
+        finally:
+            lib.gtk_prof_enable(0)
+        ids = {"select_main": _lib.PROF_SELECT_MAIN, "select": _lib.PROF_SELECT,
+               "exchange": _lib.PROF_EXCHANGE, "update": _lib.PROF_UPDATE}
+        acc = {k_: [] for k_ in ids}
+        for _ in range(steps):
+            g.replay()
+            torch.cuda.synchronize(self.dev)
+            for name, pid in ids.items():
+                ms, n = _lib.prof_graph_read(pid)
+                if n:
+                    acc[name].append(ms / n)
+        self.t += 1  # the replays took this parity's step (res[p] -> res[1-p])
+        lib.gtk_prof_reset()
+        return {k_: (sum(v) / len(v) if v else None) for k_, v in acc.items()}
 
     def step_eager(self) -> None:
         self._enqueue(self.t % 2)

@@ -187,7 +187,8 @@ def test_select_flat_top_no_fallback(dev):
 
 def test_pipeline_steady_state_no_fallback(gk):
     """Thousands of residual-accumulation steps (the bench's steady state)
-    keep every select on the fast path."""
+    stay on the fast path: after the residual's build-up (where the carried
+    key window may miss and adapt its margin) no select falls back."""
     import torch
 
     from paper_1901_04359_b200 import optimizer as opt
@@ -201,7 +202,10 @@ def test_pipeline_steady_state_no_fallback(gk):
     st = opt.make_state(torch.zeros(m, device=d), lr=0.01)
     pipe = GTopKPipeline(ep, st, k, grads)
     pipe.capture()
-    pipe.run(3000)
+    pipe.run(2000)
+    pipe.check()
+    pipe.status.zero_()
+    pipe.run(2000)
     pipe.check()
     assert int(pipe.status.item()) & 0x2 == 0, "steady-state select used the dense fallback"
 
@@ -245,3 +249,65 @@ def test_top_op_large_vs_oracle(gk, k):
     o = gk.top_op(gk.SparseVector(m, ai, av), gk.SparseVector(m, bi, bv), k)
     assert np.array_equal(o.indices, wi)
     assert np.array_equal(o.values.view(np.uint32), wv.view(np.uint32))
+
+
+def test_windowed_select_exact_and_adaptive(dev):
+    """gtk_select_windowed: the key window carried from call to call is only a
+    hint -- every call is bit-exact; a stale window (distribution shifted down)
+    costs one dense fallback, invalidates itself, and the next call samples."""
+    import torch
+
+    from oracle import gtopk_oracle as orc
+
+    d = torch.device("cuda", 0)
+    rng = np.random.default_rng(21)
+    m, k = 1_000_003, 1000
+    win = dev.new_window(d)
+    lst = dev.DeviceList(m, k, d)
+    st = torch.zeros(1, dtype=torch.int32, device=d)
+    res = np.zeros(m, F32)
+    words = []
+    for step in range(6):
+        scale = 1.0
+        if step == 4:  # every magnitude collapses (fresh residual, tiny gradient)
+            scale, res = 1e-3, np.zeros(m, F32)
+        g = (scale * rng.standard_normal(m)).astype(F32)
+        wi, wv, wres = orc.top_k_select(res + g, k)
+        gd = torch.from_numpy(g).to(d)
+        rd = torch.from_numpy(res).to(d)
+        out = torch.empty_like(gd)
+        st.zero_()
+        dev.select(rd, gd, out, k, lst, st, window=win)
+        i, v = lst.to_host()
+        assert np.array_equal(i, wi) and np.array_equal(v.view(np.uint32), wv.view(np.uint32)), step
+        got = out.cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), wres.view(np.uint32)), step
+        words.append(int(st.item()))
+        res = wres
+    assert words[0] & 0x2 == 0 and all(w & 0x2 == 0 for w in words[1:4]), words
+    assert words[4] & 0x2, "collapsed magnitudes must miss the carried window"
+    assert words[5] & 0x2 == 0, "after a miss the next call samples again"
+
+
+def test_windowed_select_k_change(dev):
+    """A window recorded for another k is ignored (sampled path, exact)."""
+    import torch
+
+    from oracle import gtopk_oracle as orc
+
+    d = torch.device("cuda", 0)
+    rng = np.random.default_rng(5)
+    m = 500_000
+    win = dev.new_window(d)
+    st = torch.zeros(1, dtype=torch.int32, device=d)
+    g = rng.standard_normal(m).astype(F32)
+    gd = torch.from_numpy(g).to(d)
+    for k in (500, 2000, 2000):
+        lst = dev.DeviceList(m, k, d)
+        out = torch.empty_like(gd)
+        st.zero_()
+        dev.select(None, gd, out, k, lst, st, window=win)
+        wi, wv, _ = orc.top_k_select(g, k)
+        i, v = lst.to_host()
+        assert np.array_equal(i, wi) and np.array_equal(v.view(np.uint32), wv.view(np.uint32)), k
+        assert int(st.item()) & 0x2 == 0, k
