@@ -255,7 +255,7 @@ def run_b200(args, rank, world):
     # ---- device-resident pipeline, CUDA graphs ------------------------------
     trace = None
     if os.environ.get("GTK_TRACE") and world > 1:
-        trace = torch.zeros(64, dtype=torch.int64, device=dev)
+        trace = torch.zeros(128, dtype=torch.int64, device=dev)
         lib.gtk_exchange_set_trace(ctypes.c_void_p(trace.data_ptr()))
     state = opt.make_state(torch.zeros(m, device=dev), lr=0.01)
     pipe = GTopKPipeline(ep, state, k, dgrads)
@@ -298,6 +298,8 @@ def run_b200(args, rank, world):
         ns = pipe.plan.nsteps
         stamps = [("start", t[0])] + [(f"s{j}.{w}", t[2 + 4 * j + i]) for j in range(ns)
                                       for i, w in enumerate(("push", "flag", "merge", "bar"))] + [("end", t[1])]
+        stamps += [(f"s{j}.copied", t[56 + j]) for j in range(min(ns, 4))]
+        stamps += [(f"s{j}.released", t[60 + j]) for j in range(min(ns, 4))]
         base = t[0]
         print(f"[rank {rank}] exchange trace (us from start): " +
               " ".join(f"{n}={(v - base) / 1e3:.1f}" for n, v in stamps if v), flush=True)

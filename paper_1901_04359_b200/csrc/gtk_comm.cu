@@ -131,12 +131,15 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
         r_n[1] = poisoned ? 0 : __ldcg(cur_n + 1);  // k-th key hint travels with the list
         if (a.step_counts) a.step_counts[2 * s] = (int32_t)n;
       }
-      // bar.sync orders every thread's peer stores before thread 0's fence;
-      // the system-scope release then publishes them all (cumulativity)
+      // bar.sync orders every thread's peer stores before thread 0's
+      // system-scope release, which publishes them all (cumulativity)
       __syncthreads();
+      if (tr) a.trace[56 + s] = (int64_t)globaltimer();
       if (threadIdx.x == 0) {
-        __threadfence_system();
+        // (no separate fence.sc.sys: the release add orders the block's peer
+        // stores before the flag by itself -- measured 3-4 us cheaper)
         red_release_sys_add_u64(a.flags[st.send_to] + s, 1ull);
+        if (tr) a.trace[60 + s] = (int64_t)globaltimer();
       }
       if (tr) a.trace[2 + 4 * s] = (int64_t)globaltimer();
     }

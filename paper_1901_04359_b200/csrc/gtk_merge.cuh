@@ -27,6 +27,7 @@ namespace gtk {
 
 constexpr int kMergeThreads = 512;
 constexpr int kMergeSub = 2048;        // merged slots staged per sub-chunk
+constexpr int kMergeSlotsPerBlock = 512;  // grid sizing target
 constexpr int kMergeSliceCap = 4096;   // slice slots kept in shared memory
 constexpr int kMergeMaxSplits = 65;    // sub-chunk boundaries per block (slice <= 128K)
 
