@@ -72,6 +72,7 @@ def main():
     out["butterfly_ok"] = bool(ok_fly)
     ep.barrier()
     print("RESULT " + json.dumps(out), flush=True)
+    ep.close()  # wait for this rank's in-flight sends before tearing gloo down
     dist.destroy_process_group()
 
 
