@@ -97,6 +97,18 @@ int gtk_select_windowed(const float* res_in, const float* grad, float* res_out, 
                         int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
                         size_t ws_bytes, int32_t flags, uint32_t* d_window, void* stream);
 
+/* gtk_select_windowed + K3 in the same launches, for P = 1 where the global
+ * top-k IS the local selection (gtopk_allreduce over one rank is the
+ * identity, collectives.py:188-219): every selected entry also applies
+ * w[idx] -= FLOAT(lr) * u(val) with u as in gtk_scatter_update (scaling 0:
+ * val / FLOAT(P), 1: val, 2: val * FLOAT(P)).  Sparse-exact form only: lr
+ * finite with the sign bit clear (else GTK_EINVAL: run gtk_scatter_update's
+ * dense kernel instead), no momentum.  On a non-finite input w is untouched. */
+int gtk_select_update(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
+                      int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
+                      size_t ws_bytes, int32_t flags, uint32_t* d_window, float* w, float lr, int32_t P,
+                      int32_t scaling, void* stream);
+
 /* ------------------------------------------------------------------------
  * K2: the sparse top-k merge operator ⊤.
  * Replaces sparse.py:157-195 (top_op(a, b, k)); a = received, b = own

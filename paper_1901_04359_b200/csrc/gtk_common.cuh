@@ -168,6 +168,12 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* scratc
   return res;
 }
 
+// K3's per-entry update factor u(v) (optimizer.py:243, _scaled): scaling 0 =
+// "average" v / FLOAT(P), 1 = "sum" v, 2 = v * FLOAT(P) (naive gTop-k "sum")
+__device__ __forceinline__ float scale_u(float v, float Pf, int scaling) {
+  return scaling == 0 ? __fdiv_rn(v, Pf) : (scaling == 2 ? __fmul_rn(v, Pf) : v);
+}
+
 __host__ __device__ __forceinline__ uint32_t ceil_log2_u64(uint64_t x) {
   uint32_t s = 0;
   while ((1ull << s) < x) ++s;

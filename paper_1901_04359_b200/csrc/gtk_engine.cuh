@@ -104,7 +104,21 @@ struct Sink {
   uint32_t window_level;  // margin level L >= 1: the next window admits ~k (1 + 2^L / 2) keys
   uint32_t prev_tau;      // the previous call's approximate k-th key (0: none)
   uint32_t prev_tau2;     // ... and the one before
+  // select + K3 at P = 1 (gtk_select_update): w[idx] -= FLOAT(lr) * u(val) for
+  // every kept entry, the sparse update of gtk_scatter_update (nullable)
+  float* upd_w;
+  float upd_lr;
+  float upd_Pf;
+  int upd_scaling;
 };
+
+// one kept entry to the output list (+ the select's side effects)
+__device__ __forceinline__ void sink_put(const Sink& out, uint32_t p, int32_t i, float v) {
+  out.o_idx[p] = i;
+  out.o_val[p] = v;
+  if (out.zero_at) out.zero_at[i] = 0.0f;
+  if (out.upd_w) out.upd_w[i] = __fsub_rn(out.upd_w[i], __fmul_rn(out.upd_lr, scale_u(v, out.upd_Pf, out.upd_scaling)));
+}
 
 __device__ __forceinline__ void sink_stamp(const Sink& out, int i) {
   if (out.trace && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -222,12 +236,7 @@ __device__ void engine_write(const Src& src, uint32_t s0, uint32_t s1, uint32_t 
     if (s < s1 && src.get(s, key, i, v)) keep = keep_fn(key, i, s - s0);
     uint32_t k_tot;
     const uint32_t k_rank = block_excl_scan<NT>(keep ? 1u : 0u, sm.scan, &k_tot);
-    if (keep) {
-      const uint32_t p = out_pos + k_rank;
-      out.o_idx[p] = i;
-      out.o_val[p] = v;
-      if (out.zero_at) out.zero_at[i] = 0.0f;
-    }
+    if (keep) sink_put(out, out_pos + k_rank, i, v);
     out_pos += k_tot;
   }
 }
@@ -511,12 +520,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
         if (is_eq && eq_seen + eq_rank < need) keep = true;
         uint32_t k_tot;
         const uint32_t k_rank = block_excl_scan<NT>(keep ? 1u : 0u, sm.scan, &k_tot);
-        if (keep) {
-          const uint32_t p = out_pos + k_rank;
-          out.o_idx[p] = i;
-          out.o_val[p] = v;
-          if (out.zero_at) out.zero_at[i] = 0.0f;
-        }
+        if (keep) sink_put(out, out_pos + k_rank, i, v);
         out_pos += k_tot;
         eq_seen += eq_tot;
       }

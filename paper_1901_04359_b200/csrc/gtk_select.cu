@@ -639,6 +639,10 @@ struct FinishArgs {
   uint32_t* d_status;
   int64_t* trace;  // optional phase stamps (block 0): [0] start [1] scanned [2] copied [3..6] engine
   uint32_t* window;  // nullable: {valid | level << 8, lo, shift, k, tau} for the next call (written here)
+  float* upd_w;      // nullable: fused K3 at P = 1 (gtk_select_update)
+  float upd_lr;
+  float upd_Pf;
+  int upd_scaling;
 };
 
 __device__ __forceinline__ void finish_stamp(const FinishArgs& a, int i) {
@@ -674,7 +678,7 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
     return;
   }
   const Sink out{a.sel_idx, a.sel_val, a.d_count, a.res_out, true, a.trace ? a.trace + 3 : nullptr,
-                 a.window, wlevel, wtau, wtau2};
+                 a.window, wlevel, wtau, wtau2, a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling};
   finish_stamp(a, 0);
 
   // my tile range and its place in the global (index-ordered) candidate list
@@ -797,9 +801,40 @@ extern "C" int gtk_select(const float* res_in, const float* grad, float* res_out
                              nullptr, stream);
 }
 
+namespace {
+struct FusedUpdate {
+  float* w;
+  float lr;
+  float Pf;
+  int scaling;
+};
+}  // namespace
+
+static int select_impl(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
+                       int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
+                       size_t ws_bytes, int32_t flags, uint32_t* d_window, FusedUpdate upd, void* stream);
+
 extern "C" int gtk_select_windowed(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
                                    int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status,
                                    void* ws, size_t ws_bytes, int32_t flags, uint32_t* d_window, void* stream) {
+  return select_impl(res_in, grad, res_out, m, k, sel_idx, sel_val, d_count, d_status, ws, ws_bytes, flags,
+                     d_window, FusedUpdate{nullptr, 0.0f, 1.0f, 0}, stream);
+}
+
+extern "C" int gtk_select_update(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
+                                 int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
+                                 size_t ws_bytes, int32_t flags, uint32_t* d_window, float* w, float lr, int32_t P,
+                                 int32_t scaling, void* stream) {
+  // only the sparse-exact form (see gtk_update.cu) fuses; the caller runs the
+  // dense K3 for any other lr
+  if (!w || P < 1 || scaling < 0 || scaling > 2 || !std::isfinite(lr) || std::signbit(lr)) return GTK_EINVAL;
+  return select_impl(res_in, grad, res_out, m, k, sel_idx, sel_val, d_count, d_status, ws, ws_bytes, flags,
+                     d_window, FusedUpdate{w, lr, (float)P, scaling}, stream);
+}
+
+static int select_impl(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
+                       int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
+                       size_t ws_bytes, int32_t flags, uint32_t* d_window, FusedUpdate upd, void* stream) {
   if (!grad || !res_out || !sel_idx || !sel_val || !d_count || !d_status || !ws) return GTK_EINVAL;
   if (m < 1 || m >= (int64_t(1) << 31) || k < 1 || k > m) return GTK_EINVAL;
   const SelectLayout L = select_layout(m, k);
@@ -884,7 +919,11 @@ extern "C" int gtk_select_windowed(const float* res_in, const float* grad, float
                 d_count,
                 d_status,
                 trace_buffer() ? trace_buffer() + 48 : nullptr,
-                d_window};
+                d_window,
+                upd.w,
+                upd.lr,
+                upd.Pf,
+                upd.scaling};
 
 
   int G = coop_grid((const void*)select_finish_kernel, kFinishThreads, 0);

@@ -33,10 +33,6 @@ __device__ __forceinline__ bool sorted_contains(const int32_t* a, uint32_t n, in
   return lo < n && __ldg(a + lo) == x;
 }
 
-__device__ __forceinline__ float scale_u(float v, float Pf, int scaling) {
-  return scaling == 0 ? __fdiv_rn(v, Pf) : (scaling == 2 ? __fmul_rn(v, Pf) : v);
-}
-
 // sparse path: global entries update w; local entries outside the global set
 // return to the residual.
 __device__ __forceinline__ bool skipped(const uint32_t* d_skip) {

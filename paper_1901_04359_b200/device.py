@@ -166,6 +166,29 @@ def select(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, out: Devic
     )
 
 
+def sparse_update_fusable(lr: float, momentum: float) -> bool:
+    """K3's sparse-exact form applies (finite lr with the sign bit clear, no
+    momentum): the update can ride on the select at P = 1."""
+    lr32 = np.float32(lr)
+    return momentum == 0.0 and bool(np.isfinite(lr32)) and not bool(np.signbit(lr32))
+
+
+def select_update(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, out: DeviceList,
+                  status: torch.Tensor, window: torch.Tensor | None, w: torch.Tensor, lr: float, P_: int,
+                  scaling: int) -> None:
+    """K1 + K3 for P = 1 (gtk_select_update): the selection is the global
+    top-k, and every selected entry also updates w exactly like
+    scatter_update's sparse form."""
+    m = grad.numel()
+    dev = grad.device
+    ws = select_workspace(m, k, dev)
+    _lib.call(
+        "gtk_select_update", P(res_in), P(grad), P(res_out), m, k, P(out.idx), P(out.val), P(out.count),
+        P(status), P(ws), ctypes.c_size_t(ws.numel()), 0, P(window), P(w), ctypes.c_float(lr), P_, scaling,
+        stream_of(dev),
+    )
+
+
 def top_op(a: DeviceList, b: DeviceList, k: int, out: DeviceList) -> None:
     """K2: out = ⊤(a, b, k) (a = received, b = own).  out may be b."""
     dev = b.device

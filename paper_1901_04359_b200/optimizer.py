@@ -262,16 +262,21 @@ class _Timer:
         return self.ev[i].elapsed_time(self.ev[j])
 
 
-def _select_checked(state, g, k, sel: DeviceList, status) -> None:
+def _select_checked(state, g, k, sel: DeviceList, status, fused_update: bool = False) -> None:
     """K1 into the spare residual; raises FloatingPointError with the state
-    untouched (the live residual is never written)."""
+    untouched (the live residual is never written; with fused_update the
+    weights are only written when the input is finite)."""
     m = state.m
     if not 1 <= k <= m:
         raise ValueError(f"k must be in [1, {m}], got {k}")
     win = getattr(state, "_window", None)
     if win is None or win.device != g.device:
         win = state._window = _dev.new_window(g.device)  # this residual's key window (K1 hint)
-    _dev.select(state._res, g, state._res2, k, sel, status[0:1], window=win)
+    if fused_update:
+        _dev.select_update(state._res, g, state._res2, k, sel, status[0:1], win, state._w,
+                           float(np.float32(state.lr)), 1, _scaling_code(state))
+    else:
+        _dev.select(state._res, g, state._res2, k, sel, status[0:1], window=win)
 
 
 def _finish(status, count_src) -> tuple[int, int]:
@@ -293,6 +298,17 @@ def gtopk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float =
     sel = state._list("sel", k)
     tm = _Timer()
     tm.mark(0)
+    if P == 1 and not measure_divergence and _dev.sparse_update_fusable(state.lr, state.momentum):
+        # one rank: gtopk_allreduce is the identity (collectives.py:188-219), no
+        # extra residual can arise and K3 rides on K1's finish (gtk_select_update)
+        _select_checked(state, g, k, sel, status, fused_update=True)
+        tm.mark(1)
+        tm.mark(2)
+        word, gnnz = _finish(status, sel.n)
+        _dev.raise_status(word)
+        state._commit(swap_residual=True)
+        return StepReport(loss=loss, t_compute_ms=t_compute_ms, t_compress_ms=tm.ms(0, 1),
+                          t_communicate_ms=tm.ms(1, 2), selected_k=gnnz)
     _select_checked(state, g, k, sel, status)
     tm.mark(1)
     if hasattr(ep.group, "gtopk"):

@@ -73,6 +73,11 @@ class GTopKPipeline:
     def _enqueue(self, parity: int) -> None:
         grad = self.grads[parity % len(self.grads)]
         res_in, res_out = self.res[parity], self.res[1 - parity]
+        if self.P == 1 and _dev.sparse_update_fusable(self.lr, self.mom):
+            # one rank: the global top-k is the selection; K3 rides on K1's finish
+            _dev.select_update(res_in, grad, res_out, self.k, self.sel, self.status, self.window,
+                               self.state._w, self.lr, 1, self.scaling)
+            return
         _dev.select(res_in, grad, res_out, self.k, self.sel, self.status, window=self.window)
         if self.P > 1:
             self.group.enqueue_exchange(self.plan, self.sel, self.status)

@@ -311,3 +311,44 @@ def test_windowed_select_k_change(dev):
         i, v = lst.to_host()
         assert np.array_equal(i, wi) and np.array_equal(v.view(np.uint32), wv.view(np.uint32)), k
         assert int(st.item()) & 0x2 == 0, k
+
+
+@pytest.mark.parametrize("scaling", [0, 1])
+def test_select_update_matches_select_then_k3(dev, scaling):
+    """gtk_select_update (K1 + K3 fused for P = 1) == gtk_select followed by
+    gtk_scatter_update, bitwise: selection, residual and weights; a
+    non-finite input leaves the weights untouched."""
+    import torch
+
+    d = torch.device("cuda", 0)
+    rng = np.random.default_rng(17 + scaling)
+    m, k, lr = 1_000_003, 997, 0.0123
+    g = torch.from_numpy(rng.standard_normal(m).astype(F32)).to(d)
+    r = torch.from_numpy((0.3 * rng.standard_normal(m)).astype(F32)).to(d)
+    w0 = torch.from_numpy(rng.standard_normal(m).astype(F32)).to(d)
+    st = torch.zeros(1, dtype=torch.int32, device=d)
+    # reference composition
+    la, ra, wa = dev.DeviceList(m, k, d), torch.empty_like(g), w0.clone()
+    dev.select(r, g, ra, k, la, st)
+    dev.scatter_update(wa, ra, None, la, la, m, float(np.float32(lr)), 0.0, 1, scaling, skip=st)
+    # fused
+    lb, rb, wb = dev.DeviceList(m, k, d), torch.empty_like(g), w0.clone()
+    win = dev.new_window(d)
+    for _ in range(2):  # second call takes the carried window
+        st.zero_()
+        wb.copy_(w0)
+        dev.select_update(r, g, rb, k, lb, st, win, wb, float(np.float32(lr)), 1, scaling)
+    assert int(st.item()) & ~0x2 == 0
+    ia, va = la.to_host()
+    ib, vb = lb.to_host()
+    assert np.array_equal(ia, ib) and np.array_equal(va.view(np.uint32), vb.view(np.uint32))
+    assert torch.equal(ra.view(torch.int32), rb.view(torch.int32))
+    assert torch.equal(wa.view(torch.int32), wb.view(torch.int32))
+    # non-finite input: status says so, weights untouched
+    g2 = g.clone()
+    g2[12345] = float("nan")
+    st.zero_()
+    wc = w0.clone()
+    dev.select_update(r, g2, rb, k, lb, st, win, wc, float(np.float32(lr)), 1, scaling)
+    assert int(st.item()) & 0x1
+    assert torch.equal(wc.view(torch.int32), w0.view(torch.int32))
