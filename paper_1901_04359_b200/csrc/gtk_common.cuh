@@ -85,6 +85,14 @@ __device__ __forceinline__ void st_stream4(float* p, float4 v) {
   __stcs(reinterpret_cast<float4*>(p), v);
 }
 
+// ---- async global -> shared copies (cp.async, L1-bypassing for 16 B) -------
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ---- programmatic dependent launch (sm_90+) ---------------------------------
 // launch_dependents: let the next kernel in the stream (launched with the
 // programmatic-serialization attribute) start now; wait: block until the

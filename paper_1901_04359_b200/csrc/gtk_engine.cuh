@@ -227,6 +227,29 @@ __device__ bool engine_find_bin(const uint32_t* hist, bool in_smem, uint32_t t, 
 template <int NT, class Src, class Keep>
 __device__ void engine_write(const Src& src, uint32_t s0, uint32_t s1, uint32_t out_pos, const Keep& keep_fn,
                              EngineSmem<NT>& sm, const Sink& out) {
+  if (s1 - s0 <= 32u * NT) {
+    // one block scan: thread t owns the contiguous run [s0 + t*per, +per)
+    const uint32_t per = (s1 - s0 + NT - 1) / NT;
+    const uint32_t r0 = min(s1, s0 + threadIdx.x * per), r1 = min(s1, r0 + per);
+    uint32_t bits = 0;
+    for (uint32_t s = r0; s < r1; ++s) {
+      uint32_t key;
+      int32_t i;
+      float v;
+      if (src.get(s, key, i, v) && keep_fn(key, i, s - s0)) bits |= 1u << (s - r0);
+    }
+    uint32_t k_tot;
+    uint32_t p = out_pos + block_excl_scan<NT>(__popc(bits), sm.scan, &k_tot);
+    for (; bits; bits &= bits - 1) {
+      const uint32_t s = r0 + __ffs(bits) - 1;
+      uint32_t key;
+      int32_t i;
+      float v;
+      src.get(s, key, i, v);
+      sink_put(out, p++, i, v);
+    }
+    return;
+  }
   for (uint32_t base = s0; base < s1; base += NT) {
     const uint32_t s = base + threadIdx.x;
     uint32_t key = 0;

@@ -61,7 +61,7 @@ struct SelectCtl {
 };
 
 struct SelectLayout {
-  size_t ctl, sample_top, engine, tile_info, tile_ovf, slot_idx, slot_val, ovf_idx, ovf_val, ord_idx, ord_val,
+  size_t ctl, sample_top, group_cnt, engine, tile_info, tile_ovf, slot_idx, slot_val, ovf_idx, ovf_val, ord_idx, ord_val,
       total;
   uint32_t ntiles, slots, ovf_cap, ord_cap;
 };
@@ -89,6 +89,8 @@ static SelectLayout select_layout(int64_t m, int32_t k) {
   off = al(off + sizeof(SelectCtl));
   L.sample_top = off;
   off = al(off + sizeof(uint32_t) * kSampleMaxChunks * kSampleTop);
+  L.group_cnt = off;
+  off = al(off + sizeof(uint32_t) * kMaxBlocks);
   L.engine = off;
   off = al(off + sizeof(EngineWS));
   L.tile_info = off;
@@ -270,7 +272,8 @@ struct SampleArgs {
   uint32_t k;
   SelectCtl* ctl;
   EngineWS* ews;
-  int64_t* trace;  // optional stamps: [0..3] block 0 phases, [4..6] last block phases
+  uint32_t* group_cnt;  // [kMaxBlocks] per-finish-block candidate counts, zeroed here
+  int64_t* trace;       // optional stamps: [0..3] block 0 phases, [4..6] last block phases
 };
 
 __device__ __forceinline__ void sample_stamp(const SampleArgs& a, int i, bool who) {
@@ -290,7 +293,8 @@ __global__ void __launch_bounds__(kSampleThreads) select_sample_kernel(SampleArg
   pdl_launch_dependents();
   if (a.window && !a.force_exact && (__ldcg(a.window) & 1u) && __ldcg(a.window + 3) == a.k) {
     // the previous call of this parameter measured the window: no sampling
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
+    if (blockIdx.x == 0) {
+      for (int i = threadIdx.x; i < kMaxBlocks; i += kSampleThreads) a.group_cnt[i] = 0u;
       if (threadIdx.x < kRounds) a.ews->gather_n[threadIdx.x] = 0;
       if (threadIdx.x == 0) {
         SelectCtl* ctl = a.ctl;
@@ -375,6 +379,7 @@ __global__ void __launch_bounds__(kSampleThreads) select_sample_kernel(SampleArg
   }
   sample_stamp(a, 6, true);
   if (threadIdx.x < kRounds) a.ews->gather_n[threadIdx.x] = 0;  // the finish engine's counters
+  for (int i = threadIdx.x; i < kMaxBlocks; i += kSampleThreads) a.group_cnt[i] = 0u;
   if (threadIdx.x == 0) {
     uint32_t lo = kk[0];  // 0 when the sample holds fewer than r_lo nonzero keys: take all
     uint32_t hi = kk[1] >= lo ? kk[1] + 1 : lo + 1;
@@ -410,7 +415,9 @@ struct MainArgs {
   float* slot_val;
   int32_t* ovf_idx;
   float* ovf_val;
-  uint32_t* whist;  // engine round-0 histogram [kHistLen]
+  uint32_t* whist;      // engine round-0 histogram [kHistLen]
+  uint32_t* group_cnt;  // candidates per finish block (tiles_per_group tiles each)
+  uint32_t tiles_per_group;
 };
 
 // v[b >> 2][b & 3] without a dynamically indexed (local-memory) array
@@ -489,6 +496,7 @@ __device__ __forceinline__ void main_tile(const MainArgs& a, uint32_t tile, cons
     if (threadIdx.x == 0) a.tile_info[tile] = 0u;
     return;
   }
+  if (threadIdx.x == 0) atomicAdd(a.group_cnt + tile / a.tiles_per_group, total);
   int32_t* didx = a.slot_idx + (size_t)tile * a.slots;
   float* dval = a.slot_val + (size_t)tile * a.slots;
   const bool dense = total > a.slots;
@@ -639,6 +647,8 @@ struct FinishArgs {
   uint32_t* d_status;
   int64_t* trace;  // optional phase stamps (block 0): [0] start [1] scanned [2] copied [3..6] engine
   uint32_t* window;  // nullable: {valid | level << 8, lo, shift, k, tau} for the next call (written here)
+  const uint32_t* group_cnt;  // candidates per block, counted by the main pass
+  uint32_t tiles_per_group;
   float* upd_w;      // nullable: fused K3 at P = 1 (gtk_select_update)
   float upd_lr;
   float upd_Pf;
@@ -681,27 +691,25 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
                  a.window, wlevel, wtau, wtau2, a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling};
   finish_stamp(a, 0);
 
-  // my tile range and its place in the global (index-ordered) candidate list
-  const uint32_t per = (a.ntiles + G - 1) / G;
+  // the round-0 window histogram (main pass) -> sm.hist by async copies
+  // issued now and awaited after the candidate copy: their L2 latency hides
+  // behind it (the copy's scratch lives in the gather arrays instead)
+  for (int b = threadIdx.x; b < kHistLen; b += kFinishThreads) cp_async4(&sm.hist[b], a.ews->hist[0] + b);
+  // my tile range and its place in the global (index-ordered) candidate list:
+  // the main pass counted the candidates of every block's tile range
+  const uint32_t per = a.tiles_per_group;
   const uint32_t t0 = min(a.ntiles, blk * per), t1 = min(a.ntiles, t0 + per);
-  uint32_t before = 0, all = 0, own = 0;
-  // tile_info is padded to a multiple of 4 with zeros: 128-bit loads
-  const uint32_t n4 = (a.ntiles + 3) / 4;
-#pragma unroll 4
-  for (uint32_t t4 = threadIdx.x; t4 < n4; t4 += kFinishThreads) {
-    const uint4 q = __ldcg(reinterpret_cast<const uint4*>(a.tile_info) + t4);
-    const uint32_t c[4] = {q.x & ~kOvfBit, q.y & ~kOvfBit, q.z & ~kOvfBit, q.w & ~kOvfBit};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t t = 4 * t4 + j;
-      all += c[j];
-      before += t < t0 ? c[j] : 0u;
-      own += (t >= t0 && t < t1) ? c[j] : 0u;
+  uint32_t C;
+  {
+    const uint32_t c = threadIdx.x < G ? __ldcg(a.group_cnt + threadIdx.x) : 0u;
+    const uint32_t ex = block_excl_scan<kFinishThreads>(c, sm.scan, &C);
+    if (threadIdx.x == blk) {
+      sm.bcast[0] = ex;
+      sm.bcast[1] = c;
     }
+    __syncthreads();
   }
-  before = block_sum<kFinishThreads>(before, sm.scan);
-  own = block_sum<kFinishThreads>(own, sm.scan);
-  const uint32_t C = block_sum<kFinishThreads>(all, sm.scan);
+  const uint32_t before = sm.bcast[0], own = sm.bcast[1];
   const bool overflow = __ldcg(&a.ctl->overflow) != 0;
   finish_stamp(a, 1);
   if (!overflow && C >= a.k && C <= a.ord_cap) {
@@ -709,9 +717,10 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
     const bool in_smem = own <= (uint32_t)kSliceCap;
     int32_t* di = in_smem ? s_idx : a.ord_idx + before;
     float* dv = in_smem ? s_val : a.ord_val + before;
-    uint32_t* s_dst = sm.keys;                   // per-tile destination (local)
-    uint32_t* s_cnt = sm.hist;                   // per-tile info
-    uint32_t* s_ovf = sm.hist + kFinishThreads;  // per-tile overflow base
+    static_assert(kGatherCap >= kFinishThreads, "copy scratch");
+    uint32_t* s_dst = sm.keys;                               // per-tile destination (local)
+    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(sm.gidx);  // per-tile info
+    uint32_t* s_ovf = sm.gblk;                               // per-tile overflow base
     uint32_t run = 0;
     for (uint32_t tb = t0; tb < t1; tb += kFinishThreads) {
       const uint32_t t = tb + threadIdx.x;
@@ -753,12 +762,15 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
       __syncthreads();
     }
     finish_stamp(a, 2);
+    cp_async_wait_all();
+    __syncthreads();
     SliceSrc src{s_idx, s_val, a.ord_idx, a.ord_val, before, in_smem, false};
     if (engine_run<kFinishThreads>(src, before, before + own, a.k, false, __ldcg(&a.ctl->lo),
-                                   __ldcg(&a.ctl->shift), a.ews->hist[0], false, a.ews, sm, out, G))
+                                   __ldcg(&a.ctl->shift), sm.hist, true, a.ews, sm, out, G))
       return;
   }
   // exact dense fallback over acc (= res_out, untouched so far)
+  cp_async_wait_all();  // the histogram prefetch must land before sm.hist is reused
   grid_sync(&a.ews->bar, G);
   if (blk == 0) {
     for (int r = 0; r < kRounds; ++r)
@@ -870,10 +882,26 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
     const double rh = mu - 4.0 * sd - 4.0;
     r_hi = rh < 1.0 ? 1u : (uint32_t)rh;
   }
+  // the finish grid (cooperative): fixed before the main pass, which counts
+  // the candidates of each finish block's tile range
+  int G = coop_grid((const void*)select_finish_kernel, kFinishThreads, 0);
+  if (G <= 0) return GTK_ECUDA;
+  {
+    int want = (int)((L.ntiles + 39) / 40);  // ~40 tiles per block (measured best of 22..150)
+    if ((int64_t)want * kSliceCap < (int64_t)k * 2) want = (int)(((int64_t)k * 2 + kSliceCap - 1) / kSliceCap);
+    if (want < 8) want = 8;
+    if ((uint32_t)want > L.ntiles) want = (int)L.ntiles;
+    if (G > want) G = want;
+    if (G > num_sms()) G = num_sms();
+    if (G > kMaxBlocks) G = kMaxBlocks;
+  }
+  const uint32_t tiles_per_group = (L.ntiles + G - 1) / G;
+  uint32_t* group_cnt = (uint32_t*)(base + L.group_cnt);
+
   ProfScope prof_all(kProfSelect, st);
   SampleArgs sa{res_in, grad, (uint32_t)m, stride, nchunks, r_lo, r_hi,
                 (uint32_t)((flags & GTK_SELECT_FORCE_EXACT) ? 1 : 0), stop, d_window, (uint32_t)k, ctl, ews,
-                trace_buffer() ? trace_buffer() + 64 : nullptr};
+                group_cnt, trace_buffer() ? trace_buffer() + 64 : nullptr};
   GTK_CUDA(launch_pdl(select_sample_kernel, dim3(nchunks), dim3(kSampleThreads), 0, st, sa));
   GTK_CHECK_LAUNCH();
 
@@ -890,7 +918,9 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
               (float*)(base + L.slot_val),
               (int32_t*)(base + L.ovf_idx),
               (float*)(base + L.ovf_val),
-              ews->hist[0]};
+              ews->hist[0],
+              group_cnt,
+              tiles_per_group};
   {
     ProfScope prof_main(kProfSelectMain, st);
     const uint32_t gmain = (L.ntiles + kMainTilesPerBlock - 1) / kMainTilesPerBlock;
@@ -920,21 +950,14 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
                 d_status,
                 trace_buffer() ? trace_buffer() + 48 : nullptr,
                 d_window,
+                group_cnt,
+                tiles_per_group,
                 upd.w,
                 upd.lr,
                 upd.Pf,
                 upd.scaling};
 
 
-  int G = coop_grid((const void*)select_finish_kernel, kFinishThreads, 0);
-  if (G <= 0) return GTK_ECUDA;
-  int want = (int)((L.ntiles + 39) / 40);  // ~40 tiles (~350 candidates) per block
-  if ((int64_t)want * kSliceCap < (int64_t)k * 2) want = (int)(((int64_t)k * 2 + kSliceCap - 1) / kSliceCap);
-  if (want < 8) want = 8;
-  if ((uint32_t)want > L.ntiles) want = (int)L.ntiles;
-  if (G > want) G = want;
-  if (G > num_sms()) G = num_sms();
-  if (G > kMaxBlocks) G = kMaxBlocks;
   void* args[] = {&fa};
   return coop_launch((const void*)select_finish_kernel, G, kFinishThreads, args, 0, st, true);
 }

@@ -1,0 +1,29 @@
+"""Phase stamps (block 0, %globaltimer) of the finish kernel in the steady
+state (carried window), plus the sample kernel's publish."""
+import sys, os, ctypes
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_1901_04359_b200 as gk
+from paper_1901_04359_b200 import optimizer as opt, _lib
+from paper_1901_04359_b200.pipeline import GTopKPipeline
+lib = _lib.load()
+d = torch.device("cuda", 0)
+m, k = 25_600_000, 25_600
+gen = torch.Generator(device=d).manual_seed(5)
+grads = [torch.randn(m, device=d, generator=gen) for _ in range(2)]
+ep = gk.create_local_cluster(1)[0]
+st = opt.make_state(torch.zeros(m, device=d), lr=0.01)
+pipe = GTopKPipeline(ep, st, k, grads)
+pipe.capture()
+pipe.run(1500)
+torch.cuda.synchronize()
+tr = torch.zeros(128, dtype=torch.int64, device=d)
+lib.gtk_exchange_set_trace(ctypes.c_void_p(tr.data_ptr()))
+names = ["start", "scanned", "copied", "bin", "gather_bar", "ranked", "written"]
+for rep in range(4):
+    tr.zero_(); torch.cuda.synchronize()
+    pipe.step_eager(); torch.cuda.synchronize()
+    t = tr.cpu().tolist()
+    f = t[48:55]
+    print(f"finish rep{rep}: " + " ".join(f"{n}={(v - f[0]) / 1e3:.1f}" for n, v in zip(names, f) if v), flush=True)
+lib.gtk_exchange_set_trace(None)
