@@ -298,8 +298,17 @@ def run_b200(args, rank, world):
         ns = pipe.plan.nsteps
         stamps = [("start", t[0])] + [(f"s{j}.{w}", t[2 + 4 * j + i]) for j in range(ns)
                                       for i, w in enumerate(("push", "flag", "merge", "bar"))] + [("end", t[1])]
-        stamps += [(f"s{j}.copied", t[56 + j]) for j in range(min(ns, 4))]
-        stamps += [(f"s{j}.released", t[60 + j]) for j in range(min(ns, 4))]
+        stamps += [(f"s{j}.copied", t[96 + j]) for j in range(min(ns, 4))]
+        stamps += [(f"s{j}.released", t[100 + j]) for j in range(min(ns, 4))]
+        mnames = ["path", "slots", "hist_bar", "engine_end", "bin", "gather_bar", "ranked", "written"]
+        for j in range(min(ns, 2)):
+            mt = t[32 + 16 * j:32 + 16 * j + 9]
+            if mt[0]:
+                stamps += [(f"s{j}.m.{n}", v) for n, v in zip(mnames, mt[1:]) if v]
+                b = 32 + 16 * j
+                print(f"[rank {rank}] merge step {j} window lo={t[b + 14]} shift={t[b + 15]} rec0={t[b + 10]} "
+                      f"tau={t[b + 11]} tau2={t[b + 12]} -> next lo={t[b + 13]}; round-0 in_bin={t[b + 9]}",
+                      flush=True)
         base = t[0]
         print(f"[rank {rank}] exchange trace (us from start): " +
               " ".join(f"{n}={(v - base) / 1e3:.1f}" for n, v in stamps if v), flush=True)

@@ -54,6 +54,7 @@ struct ExchangeArgs {
   const int32_t* in_idx; // optional input list copied into acc first (keeps the
   const float* in_val;   // caller's local selection intact for K3)
   const int32_t* d_in_n;
+  uint32_t* windows;     // [kMergeWindowSlots][8] carried merge key windows, one per step
   MergeArgs merge;       // workspace pointers; list pointers filled per step
 };
 
@@ -134,12 +135,12 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
       // bar.sync orders every thread's peer stores before thread 0's
       // system-scope release, which publishes them all (cumulativity)
       __syncthreads();
-      if (tr) a.trace[56 + s] = (int64_t)globaltimer();
+      if (tr) a.trace[96 + s] = (int64_t)globaltimer();
       if (threadIdx.x == 0) {
         // (no separate fence.sc.sys: the release add orders the block's peer
         // stores before the flag by itself -- measured 3-4 us cheaper)
         red_release_sys_add_u64(a.flags[st.send_to] + s, 1ull);
-        if (tr) a.trace[60 + s] = (int64_t)globaltimer();
+        if (tr) a.trace[100 + s] = (int64_t)globaltimer();
       }
       if (tr) a.trace[2 + 4 * s] = (int64_t)globaltimer();
     }
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
         m.o_val = a.acc_val;
         m.d_no = a.d_acc_n;
         m.trace = a.trace ? a.trace + 32 + 16 * s : nullptr;
-        merge_device(m, n_in, n_own, hint_in, hint_own, G, S);
+        merge_device(m, n_in, n_own, hint_in, hint_own, G, S, s < kMergeWindowSlots ? a.windows + 8 * s : nullptr);
       } else {
         const uint32_t per = (n_in + G - 1) / G;
         const uint32_t e0 = min(n_in, blk * per), e1 = min(n_in, e0 + per);
@@ -330,6 +331,7 @@ extern "C" int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedu
   a.in_idx = in_idx;
   a.in_val = in_val;
   a.d_in_n = d_in_n;
+  a.windows = (uint32_t*)((char*)ws + L.windows);
   char* base = (char*)ws;
   a.merge = MergeArgs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, (uint32_t)k, nullptr, nullptr,
                       nullptr, (MergeCtl*)(base + L.ctl), (EngineWS*)(base + L.engine),

@@ -104,6 +104,7 @@ struct Sink {
   uint32_t window_level;  // margin level L >= 1: the next window admits ~k (1 + 2^L / 2) keys
   uint32_t prev_tau;      // the previous call's approximate k-th key (0: none)
   uint32_t prev_tau2;     // ... and the one before
+  uint32_t window_rank_shift;  // lo' sits at rank kt (1 + 2^L >> shift): select 1, merge 3 (a union holds <= 2 kt)
   // select + K3 at P = 1 (gtk_select_update): w[idx] -= FLOAT(lr) * u(val) for
   // every kept entry, the sparse update of gtk_scatter_update (nullable)
   float* upd_w;
@@ -327,7 +328,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       // about that many candidates pass lo' (a miss costs one exact dense
       // fallback and raises L)
       uint32_t b2, b3;
-      const uint64_t t2w = (uint64_t)kt + (((uint64_t)kt << out.window_level) >> 1);
+      const uint64_t t2w = (uint64_t)kt + (((uint64_t)kt << out.window_level) >> out.window_rank_shift);
       const uint32_t t2 = (uint32_t)min(t2w, (uint64_t)0xFFFFFFFFu), t3 = max(1u, kt / 2);
       if (!engine_find_bin<NT>(hist, hsm, t, sm, bin, above, in_bin, t2, t3, &b2, &b3)) return false;
       if (blk == 0 && threadIdx.x == 0) {
@@ -357,8 +358,24 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
         }
         if (hi_n <= lo_n) hi_n = lo_n + 1;
         const uint64_t width = hi_n - lo_n;
+        uint32_t shift_n = width <= (uint64_t)kBins ? 0u : ceil_log2_u64((width + kBins - 1) / kBins);
+        if (out.window_rank_shift >= 3 && bin < (uint32_t)kBins && in_bin > 0) {
+          // merge: every union entry is processed whatever the window, so aim
+          // for resolution instead -- bins narrow enough that the k-th key's
+          // bin holds ~64 entries at the measured density, the k-th key in
+          // the middle of the 2048 bins (>= 1024 bins of room to move down)
+          const uint64_t dens_w = ((uint64_t)64 << shift) / in_bin;  // key units per ~64 entries
+          uint32_t sd = 0;
+          while (sd < 31 && (2ull << sd) <= dens_w) ++sd;
+          sd += out.window_level - 2;  // a miss widens
+          if (sd < shift_n) {
+            shift_n = sd;
+            const uint64_t half = (uint64_t)(kBins / 2) << shift_n;
+            lo_n = tau_n > half ? tau_n - half : 0u;
+          }
+        }
         out.next_window[1] = (uint32_t)lo_n;
-        out.next_window[2] = width <= (uint64_t)kBins ? 0u : ceil_log2_u64((width + kBins - 1) / kBins);
+        out.next_window[2] = shift_n;
         out.next_window[3] = kt;
         out.next_window[4] = tau_n;
         out.next_window[5] = p1;
@@ -368,6 +385,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       return false;
     }
     sink_stamp(out, 0);
+    if (out.trace && r == 0 && blk == 0 && threadIdx.x == 0) out.trace[4] = in_bin;  // diagnostics
     uint64_t blo, bhi;
     if (bin < (uint32_t)kBins) {
       blo = (uint64_t)lo + ((uint64_t)bin << shift);

@@ -37,8 +37,9 @@ struct MergeCtl {
 };
 
 struct MergeLayout {
-  size_t ctl, engine, u_idx, u_val, total;
+  size_t ctl, engine, u_idx, u_val, windows, total;
 };
+constexpr int kMergeWindowSlots = 64;  // carried key windows (exchange steps), 8 words each
 
 static inline MergeLayout merge_layout(int32_t cap) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -52,6 +53,8 @@ static inline MergeLayout merge_layout(int32_t cap) {
   off = al(off + sizeof(int32_t) * 2 * (size_t)cap);
   L.u_val = off;
   off = al(off + sizeof(float) * 2 * (size_t)cap);
+  L.windows = off;
+  off = al(off + sizeof(uint32_t) * 8 * kMergeWindowSlots);
   L.total = off;
   return L;
 }
@@ -154,9 +157,13 @@ static __device__ __forceinline__ uint32_t upper_bound_s(const int32_t* s, uint3
 constexpr uint32_t kMergeWinShift = 13;  // 2048 << 13 = 2^24 keys = 2 octaves
 
 // na/nb and the hints are passed by value: the caller read them before any
-// output write.
+// output write.  rec (nullable): a key window carried from this merge's
+// previous call (the same exchange step of the same parameter, same record
+// format as gtk_select_windowed); used when valid, rewritten by block 0
+// after the histogram barrier (every block has read it by then).
 static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t na, uint32_t nb, uint32_t hint_a,
-                                                    uint32_t hint_b, unsigned G, MergeSmem& S) {
+                                                    uint32_t hint_b, unsigned G, MergeSmem& S,
+                                                    uint32_t* rec = nullptr) {
   EngineSmem<kMergeThreads>& esm = S.esm;
   const unsigned blk = blockIdx.x;
   const uint32_t N = na + nb;
@@ -171,7 +178,27 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   uint32_t win_lo = 0;
   if (na >= a.k && hint_a < kInfKey) win_lo = max(win_lo, hint_a);
   if (nb >= a.k && hint_b < kInfKey) win_lo = max(win_lo, hint_b);
-  const uint32_t win_shift = win_lo ? kMergeWinShift : 20u;
+  uint32_t win_shift = win_lo ? kMergeWinShift : 20u;
+  uint32_t rec_level = 2u, rec_tau = 0u, rec_tau2 = 0u;
+  if (rec) {
+    const uint32_t r0 = __ldcg(rec);
+    rec_level = min(4u, max(2u, r0 >> 8));
+    if (__ldcg(rec + 3) == a.k) {
+      rec_tau = __ldcg(rec + 4);
+      rec_tau2 = __ldcg(rec + 5);
+      if (r0 & 1u) {  // the previous call measured the window of this step
+        win_lo = __ldcg(rec + 1);
+        win_shift = __ldcg(rec + 2);
+      }
+    }
+  }
+  if (a.trace && blk == 0 && threadIdx.x == 0) {  // window used (diagnostics)
+    a.trace[14] = win_lo;
+    a.trace[15] = win_shift;
+    a.trace[10] = rec ? (int64_t)__ldcg(rec) : -1;
+    a.trace[11] = rec_tau;
+    a.trace[12] = rec_tau2;
+  }
   for (int b = threadIdx.x; b < kHistLen; b += kMergeThreads) esm.hist[b] = 0;
   if (threadIdx.x == 0) S.s_valid = 0;
   if (blk == 0 && threadIdx.x < kRounds) a.ews->gather_n[threadIdx.x] = 0;  // read only after a barrier
@@ -293,12 +320,18 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   merge_stamp(a, 3);  // after the histogram barrier
   const bool keep_all = n_valid <= a.k;
   const SliceSrc src{S.slice_idx, S.slice_val, a.u_idx, a.u_val, d0, in_smem, true};
-  const Sink out{a.o_idx, a.o_val, a.d_no, nullptr, true, a.trace ? a.trace + 5 : nullptr, nullptr, 0u, 0u, 0u};
+  const Sink out{a.o_idx, a.o_val, a.d_no, nullptr, true, a.trace ? a.trace + 5 : nullptr,
+                 keep_all ? nullptr : rec, rec_level, rec_tau, rec_tau2, 3u};
   const uint32_t* h0 = solo ? esm.hist : a.ews->hist[0];
   bool ok = engine_run<kMergeThreads>(src, d0, d1, keep_all ? n_valid : a.k, keep_all, win_lo, win_shift, h0, solo,
                                       a.ews, esm, out, G);
   merge_stamp(a, 4);  // engine done
-  if (!ok) {  // the hint window missed (cancellation): full key range
+  if (a.trace && rec && blk == 0 && threadIdx.x == 0) a.trace[13] = __ldcg(rec + 1);
+  if (!ok) {  // the window missed (hint: cancellation; carried: a shift): full key range
+    if (rec && blk == 0 && threadIdx.x == 0) {
+      rec[0] = min(4u, rec_level + 1) << 8;  // invalid, wider margin next time
+      rec[4] = rec[5] = 0u;
+    }
     if (!solo) {
       grid_sync(&a.ews->bar, G);
       if (blk == 0) {

@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
     return;
   }
   const Sink out{a.sel_idx, a.sel_val, a.d_count, a.res_out, true, a.trace ? a.trace + 3 : nullptr,
-                 a.window, wlevel, wtau, wtau2, a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling};
+                 a.window, wlevel, wtau, wtau2, 1u, a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling};
   finish_stamp(a, 0);
 
   // the round-0 window histogram (main pass) -> sm.hist by async copies
