@@ -58,6 +58,7 @@ EXPORTS = (
     "gtk_ipc_open_handle",
     "gtk_ipc_close_handle",
     "gtk_gtopk_exchange",
+    "gtk_gtopk_exchange_update",
     "gtk_prof_enable",
     "gtk_prof_read",
     "gtk_prof_reset",
@@ -102,6 +103,11 @@ _SIGS = {
     "gtk_ipc_close_handle": ([_P], _I32),
     "gtk_gtopk_exchange": (
         [_I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P],
+        _I32,
+    ),
+    "gtk_gtopk_exchange_update": (
+        [_I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P, _P, _F,
+         _I32, _P],
         _I32,
     ),
     "gtk_prof_enable": ([_I32], _I32),

@@ -23,6 +23,8 @@
 // overwritten while its reader is still merging.
 #include <cuda_runtime.h>
 
+#include <cmath>
+
 #include <cstring>
 
 #include "gtk_internal.h"
@@ -55,8 +57,36 @@ struct ExchangeArgs {
   const float* in_val;   // caller's local selection intact for K3)
   const int32_t* d_in_n;
   uint32_t* windows;     // [kMergeWindowSlots][8] carried merge key windows, one per step
+  // fused K3 (gtk_gtopk_exchange_update; upd_w null = exchange only): the
+  // global list updates w, local (in_*) entries missing from it return to res
+  float* upd_w;
+  float* upd_res;
+  float upd_lr;
+  int upd_scaling;
   MergeArgs merge;       // workspace pointers; list pointers filled per step
 };
+
+// first position in the sorted a[0, n) with a[pos] >= x (strict: > x), one full
+// warp, 33-ary: ceil(log33 n) dependent round trips instead of log2 n
+__device__ __forceinline__ uint32_t warp_search(const int32_t* a, uint32_t n, int32_t x, bool strict) {
+  uint32_t L = 0, H = n;  // answer in [L, H]
+  const unsigned lane = lane_id();
+  while (H > L) {
+    const uint32_t len = H - L;
+    if (len <= 32) {
+      const bool lt = lane < len && (strict ? __ldcg(a + L + lane) <= x : __ldcg(a + L + lane) < x);
+      return L + __popc(__ballot_sync(kFull, lt));
+    }
+    const uint32_t p = L + (uint32_t)(((uint64_t)len * (lane + 1)) / 33);  // probes, ascending
+    const bool lt = strict ? __ldcg(a + p) <= x : __ldcg(a + p) < x;
+    const int t = __popc(__ballot_sync(kFull, lt));  // probes below the answer
+    const uint32_t p_prev = __shfl_sync(kFull, p, t > 0 ? t - 1 : 0);
+    const uint32_t p_t = __shfl_sync(kFull, p, t < 32 ? t : 31);
+    if (t > 0) L = p_prev + 1;
+    if (t < 32) H = p_t;
+  }
+  return L;
+}
 
 // inbox slot: 16 B header {count, hint} | idx[k4] | val[k4], k4 = k rounded up
 // to 4 so both arrays are 16-byte aligned for 128-bit peer stores
@@ -145,6 +175,17 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
       if (tr) a.trace[2 + 4 * s] = (int64_t)globaltimer();
     }
     if (st.recv_from >= 0) {
+      // everything local the merge needs is loaded before the wait
+      uint32_t* wrec = (st.merge && s < kMergeWindowSlots) ? a.windows + 8 * s : nullptr;
+      const MergeWindowRec wv = load_window_rec(wrec);
+      uint32_t n_own = 0, hint_own = 0;
+      if (st.merge) {
+        // every block reads the own count before the merge's first barrier;
+        // the merge writes acc (and its count) only after that barrier
+        n_own = self_poison ? 0u : (uint32_t)__ldcg(cur_n);
+        if (n_own > (uint32_t)a.k) n_own = a.k;
+        hint_own = self_poison ? 0u : (uint32_t)__ldcg(cur_n + 1);
+      }
       if (threadIdx.x == 0) {
         const uint64_t t0 = globaltimer();
         uint32_t spins = 0;
@@ -178,11 +219,6 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
       const uint32_t n_in = s_n, hint_in = s_hint;
       if (blk == 0 && threadIdx.x == 0 && a.step_counts) a.step_counts[2 * s + 1] = (int32_t)n_in;
       if (st.merge) {
-        // every block reads the own count before the merge's first barrier;
-        // the merge writes acc (and its count) only after that barrier
-        uint32_t n_own = self_poison ? 0u : (uint32_t)__ldcg(cur_n);
-        if (n_own > (uint32_t)a.k) n_own = a.k;
-        const uint32_t hint_own = self_poison ? 0u : (uint32_t)__ldcg(cur_n + 1);
         MergeArgs m = a.merge;
         m.a_idx = in_idx;
         m.a_val = in_val;
@@ -192,7 +228,7 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
         m.o_val = a.acc_val;
         m.d_no = a.d_acc_n;
         m.trace = a.trace ? a.trace + 32 + 16 * s : nullptr;
-        merge_device(m, n_in, n_own, hint_in, hint_own, G, S, s < kMergeWindowSlots ? a.windows + 8 * s : nullptr);
+        merge_device(m, n_in, n_own, hint_in, hint_own, G, S, wrec, wv);
       } else {
         const uint32_t per = (n_in + G - 1) / G;
         const uint32_t e0 = min(n_in, blk * per), e1 = min(n_in, e0 + per);
@@ -227,6 +263,50 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
     if (blk == 0 && threadIdx.x == 0) {
       a.d_acc_n[0] = (int32_t)n;
       a.d_acc_n[1] = __ldcg(a.d_in_n + 1);
+    }
+  }
+  if (a.upd_w) {
+    // K3 (gtk_update.cu, sparse-exact form) on the final global list
+    grid_sync(&a.merge.ews->bar, G);  // acc complete; status final
+    if (!(__ldcg(a.d_status) & GTK_DEV_ERROR_MASK)) {
+      const uint32_t gn = min((uint32_t)__ldcg(a.d_acc_n), (uint32_t)a.k);
+      const float Pf = (float)a.P;
+      for (uint32_t e = blk * kMergeThreads + threadIdx.x; e < gn; e += G * kMergeThreads) {
+        const int32_t i = __ldcg(a.acc_idx + e);
+        const float u = scale_u(__ldcg(a.acc_val + e), Pf, a.upd_scaling);
+        a.upd_w[i] = __fsub_rn(a.upd_w[i], __fmul_rn(a.upd_lr, u));
+      }
+      // extra residual: my slice of the local list, membership by a search of
+      // the slice's index range in the global list, then in shared memory
+      uint32_t ln = min((uint32_t)__ldcg(a.d_in_n), (uint32_t)a.k);
+      const uint32_t per = (ln + G - 1) / G;
+      const uint32_t l0 = min(ln, blk * per), l1 = min(ln, l0 + per);
+      if (l0 < l1) {
+        int32_t* s_g = S.slice_idx;  // free after the merges
+        if (warp_id() < 2) {
+          const int32_t x = __ldcg(a.in_idx + (warp_id() == 0 ? l0 : l1 - 1));
+          const uint32_t pos = warp_search(a.acc_idx, gn, x, warp_id() == 1);
+          if (lane_id() == 0) (warp_id() == 0 ? s_n : s_hint) = pos;
+        }
+        __syncthreads();
+        const uint32_t g0 = s_n, g1 = s_hint, gl = g1 - g0;
+        const bool fits = gl <= (uint32_t)kMergeSliceCap;
+        if (fits)
+          for (uint32_t j = threadIdx.x; j < gl; j += kMergeThreads) s_g[j] = __ldcg(a.acc_idx + g0 + j);
+        __syncthreads();
+        for (uint32_t e = l0 + threadIdx.x; e < l1; e += kMergeThreads) {
+          const int32_t x = __ldcg(a.in_idx + e);
+          uint32_t lo = 0, hi = gl;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            const int32_t y = fits ? s_g[mid] : __ldcg(a.acc_idx + g0 + mid);
+            if (y < x) lo = mid + 1;
+            else hi = mid;
+          }
+          const bool found = lo < gl && (fits ? s_g[lo] : __ldcg(a.acc_idx + g0 + lo)) == x;
+          if (!found) a.upd_res[x] = __fadd_rn(a.upd_res[x], __ldcg(a.in_val + e));
+        }
+      }
     }
   }
   if (blk == 0 && threadIdx.x == 0) {
@@ -291,12 +371,45 @@ extern "C" int gtk_ipc_close_handle(void* dptr) {
   return GTK_OK;
 }
 
+static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps, void* const* peer_inbox,
+                         uint64_t* const* peer_flags, uint64_t* d_epoch, int32_t* acc_idx, float* acc_val,
+                         int32_t* d_acc_n, int32_t k, uint32_t* d_status, const uint32_t* d_abort,
+                         int64_t timeout_ns, int32_t* step_counts, const int32_t* in_idx, const float* in_val,
+                         const int32_t* d_in_n, void* ws, size_t ws_bytes, float* upd_w, float* upd_res,
+                         float upd_lr, int32_t upd_scaling, void* stream);
+
 extern "C" int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
                                   void* const* peer_inbox, uint64_t* const* peer_flags, uint64_t* d_epoch,
                                   int32_t* acc_idx, float* acc_val, int32_t* d_acc_n, int32_t k,
                                   uint32_t* d_status, const uint32_t* d_abort, int64_t timeout_ns,
                                   int32_t* step_counts, const int32_t* in_idx, const float* in_val,
                                   const int32_t* d_in_n, void* ws, size_t ws_bytes, void* stream) {
+  return exchange_impl(rank, P, schedule, nsteps, peer_inbox, peer_flags, d_epoch, acc_idx, acc_val, d_acc_n, k,
+                       d_status, d_abort, timeout_ns, step_counts, in_idx, in_val, d_in_n, ws, ws_bytes, nullptr,
+                       nullptr, 0.0f, 0, stream);
+}
+
+extern "C" int gtk_gtopk_exchange_update(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
+                                         void* const* peer_inbox, uint64_t* const* peer_flags, uint64_t* d_epoch,
+                                         int32_t* acc_idx, float* acc_val, int32_t* d_acc_n, int32_t k,
+                                         uint32_t* d_status, const uint32_t* d_abort, int64_t timeout_ns,
+                                         int32_t* step_counts, const int32_t* in_idx, const float* in_val,
+                                         const int32_t* d_in_n, void* ws, size_t ws_bytes, float* w, float* res,
+                                         float lr, int32_t scaling, void* stream) {
+  if (!w || !res || !in_idx || scaling < 0 || scaling > 2 || !std::isfinite(lr) || std::signbit(lr))
+    return GTK_EINVAL;
+  if (nsteps == 0) return GTK_EINVAL;  // one rank: gtk_select_update
+  return exchange_impl(rank, P, schedule, nsteps, peer_inbox, peer_flags, d_epoch, acc_idx, acc_val, d_acc_n, k,
+                       d_status, d_abort, timeout_ns, step_counts, in_idx, in_val, d_in_n, ws, ws_bytes, w, res, lr,
+                       scaling, stream);
+}
+
+static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps, void* const* peer_inbox,
+                         uint64_t* const* peer_flags, uint64_t* d_epoch, int32_t* acc_idx, float* acc_val,
+                         int32_t* d_acc_n, int32_t k, uint32_t* d_status, const uint32_t* d_abort,
+                         int64_t timeout_ns, int32_t* step_counts, const int32_t* in_idx, const float* in_val,
+                         const int32_t* d_in_n, void* ws, size_t ws_bytes, float* upd_w, float* upd_res,
+                         float upd_lr, int32_t upd_scaling, void* stream) {
   if (P < 1 || P > kMaxRanks || rank < 0 || rank >= P || nsteps < 0 || nsteps > kMaxSteps || k < 1)
     return GTK_EINVAL;
   if (!acc_idx || !acc_val || !d_acc_n || !d_status || !ws || !d_epoch) return GTK_EINVAL;
@@ -332,6 +445,10 @@ extern "C" int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedu
   a.in_val = in_val;
   a.d_in_n = d_in_n;
   a.windows = (uint32_t*)((char*)ws + L.windows);
+  a.upd_w = upd_w;
+  a.upd_res = upd_res;
+  a.upd_lr = upd_lr;
+  a.upd_scaling = upd_scaling;
   char* base = (char*)ws;
   a.merge = MergeArgs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, (uint32_t)k, nullptr, nullptr,
                       nullptr, (MergeCtl*)(base + L.ctl), (EngineWS*)(base + L.engine),

@@ -161,9 +161,25 @@ constexpr uint32_t kMergeWinShift = 13;  // 2048 << 13 = 2^24 keys = 2 octaves
 // previous call (the same exchange step of the same parameter, same record
 // format as gtk_select_windowed); used when valid, rewritten by block 0
 // after the histogram barrier (every block has read it by then).
+struct MergeWindowRec {  // a carried window record, loaded ahead of the merge
+  uint32_t w0, lo, shift, k, tau, tau2;
+};
+__device__ __forceinline__ MergeWindowRec load_window_rec(const uint32_t* rec) {
+  MergeWindowRec r{0u, 0u, 0u, 0u, 0u, 0u};
+  if (rec) {
+    r.w0 = __ldcg(rec);
+    r.lo = __ldcg(rec + 1);
+    r.shift = __ldcg(rec + 2);
+    r.k = __ldcg(rec + 3);
+    r.tau = __ldcg(rec + 4);
+    r.tau2 = __ldcg(rec + 5);
+  }
+  return r;
+}
+
 static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t na, uint32_t nb, uint32_t hint_a,
                                                     uint32_t hint_b, unsigned G, MergeSmem& S,
-                                                    uint32_t* rec = nullptr) {
+                                                    uint32_t* rec = nullptr, MergeWindowRec rv = {}) {
   EngineSmem<kMergeThreads>& esm = S.esm;
   const unsigned blk = blockIdx.x;
   const uint32_t N = na + nb;
@@ -181,21 +197,20 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   uint32_t win_shift = win_lo ? kMergeWinShift : 20u;
   uint32_t rec_level = 2u, rec_tau = 0u, rec_tau2 = 0u;
   if (rec) {
-    const uint32_t r0 = __ldcg(rec);
-    rec_level = min(4u, max(2u, r0 >> 8));
-    if (__ldcg(rec + 3) == a.k) {
-      rec_tau = __ldcg(rec + 4);
-      rec_tau2 = __ldcg(rec + 5);
-      if (r0 & 1u) {  // the previous call measured the window of this step
-        win_lo = __ldcg(rec + 1);
-        win_shift = __ldcg(rec + 2);
+    rec_level = min(4u, max(2u, rv.w0 >> 8));
+    if (rv.k == a.k) {
+      rec_tau = rv.tau;
+      rec_tau2 = rv.tau2;
+      if (rv.w0 & 1u) {  // the previous call measured the window of this step
+        win_lo = rv.lo;
+        win_shift = rv.shift;
       }
     }
   }
   if (a.trace && blk == 0 && threadIdx.x == 0) {  // window used (diagnostics)
     a.trace[14] = win_lo;
     a.trace[15] = win_shift;
-    a.trace[10] = rec ? (int64_t)__ldcg(rec) : -1;
+    a.trace[10] = rec ? (int64_t)rv.w0 : -1;
     a.trace[11] = rec_tau;
     a.trace[12] = rec_tau2;
   }

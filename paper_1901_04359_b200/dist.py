@@ -123,20 +123,24 @@ class DistDeviceGroup:
         return p
 
     # -- gTopKAllReduce ----------------------------------------------------
-    def gtopk(self, ep: Endpoint, lst: DeviceList, k: int, status: torch.Tensor | None = None) -> DeviceList:
+    def gtopk(self, ep: Endpoint, lst: DeviceList, k: int, status: torch.Tensor | None = None,
+              update=None) -> DeviceList:
         """Fused NVLink exchange; returns the plan's accumulator (valid until
-        the next gtopk call with the same k)."""
+        the next gtopk call with the same k).  update: see enqueue_exchange."""
         if self.aborted:
             raise TransportError("cluster aborted")
         plan = self.plan(k, lst.dim)
         if self.world == 1:
             if lst is not plan.acc:
                 plan.acc.copy_from(lst)
+            if update is not None:
+                w, res, lr, scaling = update
+                _dev.scatter_update(w, res, None, plan.acc, lst, lst.dim, lr, 0.0, 1, scaling, skip=status)
             return plan.acc
         st = status if status is not None else plan.status
         if status is None:
             st.zero_()
-        self.enqueue_exchange(plan, lst, st)
+        self.enqueue_exchange(plan, lst, st, update=update)
         counts = plan.step_counts.clone()  # snapshot for lazy byte accounting
         for j, (s, r, _mg) in enumerate(plan.steps):
             if s >= 0:
@@ -148,18 +152,28 @@ class DistDeviceGroup:
             _dev.raise_status(word)
         return plan.acc
 
-    def enqueue_exchange(self, plan: _ExchangePlan, lst: DeviceList, status: torch.Tensor) -> None:
+    def enqueue_exchange(self, plan: _ExchangePlan, lst: DeviceList, status: torch.Tensor,
+                         update=None) -> None:
         """Launch the fused exchange kernel on the current stream: plan.acc
         becomes the global top-k of every rank's `lst`.  No host sync; the
-        launch is CUDA-graph capturable (device-side epoch)."""
+        launch is CUDA-graph capturable (device-side epoch).  update = (w,
+        res, lr, scaling): K3's sparse form runs in the same kernel
+        (gtk_gtopk_exchange_update; `lst` must not be plan.acc)."""
         src = None if lst is plan.acc else lst
-        _lib.call(
-            "gtk_gtopk_exchange", self.rank, self.world, plan.schedule, plan.nsteps, plan.peer_inbox,
-            plan.peer_flags, P(plan.epoch), P(plan.acc.idx), P(plan.acc.val), P(plan.acc.count),
-            plan.k, P(status), None, ctypes.c_int64(int(self.timeout * 1e9)), P(plan.step_counts),
-            P(src.idx if src else None), P(src.val if src else None), P(src.count if src else None),
-            P(plan.ws), ctypes.c_size_t(plan.ws.numel()), _dev.stream_of(self.device),
-        )
+        args = [self.rank, self.world, plan.schedule, plan.nsteps, plan.peer_inbox,
+                plan.peer_flags, P(plan.epoch), P(plan.acc.idx), P(plan.acc.val), P(plan.acc.count),
+                plan.k, P(status), None, ctypes.c_int64(int(self.timeout * 1e9)), P(plan.step_counts),
+                P(src.idx if src else None), P(src.val if src else None), P(src.count if src else None),
+                P(plan.ws), ctypes.c_size_t(plan.ws.numel())]
+        if update is not None and src is not None and plan.nsteps > 0:
+            w, res, lr, scaling = update
+            _lib.call("gtk_gtopk_exchange_update", *args, P(w), P(res), ctypes.c_float(lr), scaling,
+                      _dev.stream_of(self.device))
+            return
+        _lib.call("gtk_gtopk_exchange", *args, _dev.stream_of(self.device))
+        if update is not None:  # (no exchange steps or in-place list: separate K3)
+            w, res, lr, scaling = update
+            _dev.scatter_update(w, res, None, plan.acc, lst, lst.dim, lr, 0.0, self.world, scaling, skip=status)
 
     # -- TopKAllReduce baseline: NCCL allgather + rank-order accumulation -----
     def topk(self, ep: Endpoint, lst: DeviceList, divide: bool = True) -> torch.Tensor:

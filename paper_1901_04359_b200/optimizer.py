@@ -311,11 +311,15 @@ def gtopk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float =
                           t_communicate_ms=tm.ms(1, 2), selected_k=gnnz)
     _select_checked(state, g, k, sel, status)
     tm.mark(1)
+    fused_k3 = False
     if hasattr(ep.group, "gtopk"):
         # one process per GPU: the fused exchange kernel carries the select's
         # status (poison) to every rank, K3 skips on any error bit, and the
-        # single status read below raises -- no mid-step host sync
-        glist = ep.group.gtopk(ep, sel, k, status=status[0:1])
+        # single status read below raises -- no mid-step host sync; with the
+        # sparse-exact update K3 runs inside the same kernel
+        fused_k3 = _dev.sparse_update_fusable(state.lr, state.momentum)
+        upd = ((state._w, state._res2, float(np.float32(state.lr)), _scaling_code(state)) if fused_k3 else None)
+        glist = ep.group.gtopk(ep, sel, k, status=status[0:1], update=upd)
     else:
         # in-process cluster: surface a local FloatingPointError before the
         # collective, exactly like the reference (other ranks then see the
@@ -328,8 +332,9 @@ def gtopk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float =
     lost_mass, divergence = 0.0, None
     if measure_divergence:
         lost_mass, divergence = _divergence(ep, sel, glist, k, state.m)
-    _dev.scatter_update(state._w, state._res2, state._vel, glist, sel, state.m, float(np.float32(state.lr)),
-                        float(np.float32(state.momentum)), P, _scaling_code(state), skip=status[0:1])
+    if not fused_k3:
+        _dev.scatter_update(state._w, state._res2, state._vel, glist, sel, state.m, float(np.float32(state.lr)),
+                            float(np.float32(state.momentum)), P, _scaling_code(state), skip=status[0:1])
     word, gnnz = _finish(status, glist.n)
     _dev.raise_status(word)
     state._commit(swap_residual=True)

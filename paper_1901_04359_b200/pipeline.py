@@ -79,6 +79,11 @@ class GTopKPipeline:
                                self.state._w, self.lr, 1, self.scaling)
             return
         _dev.select(res_in, grad, res_out, self.k, self.sel, self.status, window=self.window)
+        if self.P > 1 and _dev.sparse_update_fusable(self.lr, self.mom):
+            # K3 rides on the exchange kernel (one launch fewer, no membership pass)
+            self.group.enqueue_exchange(self.plan, self.sel, self.status,
+                                        update=(self.state._w, res_out, self.lr, self.scaling))
+            return
         if self.P > 1:
             self.group.enqueue_exchange(self.plan, self.sel, self.status)
             glist = self.plan.acc

@@ -25,5 +25,6 @@ for rep in range(4):
     pipe.step_eager(); torch.cuda.synchronize()
     t = tr.cpu().tolist()
     f = t[48:55]
-    print(f"finish rep{rep}: " + " ".join(f"{n}={(v - f[0]) / 1e3:.1f}" for n, v in zip(names, f) if v), flush=True)
+    print(f"finish rep{rep}: " + " ".join(f"{n}={(v - f[0]) / 1e3:.1f}" for n, v in zip(names, f) if v)
+          + f" | round-0 in_bin={t[55]}", flush=True)
 lib.gtk_exchange_set_trace(None)
