@@ -235,9 +235,15 @@ def run_b200(args, rank, world):
     m, rho = args.m, args.rho
     k = k_from_density(rho, m)
 
-    # synthetic gradients, two per rank (cli.run_bench style: seeded normal draws)
-    rng = np.random.default_rng(1000 + rank)
-    host_grads = [rng.standard_normal(m).astype(np.float32) for _ in range(2)]
+    # synthetic gradients, cli.run_bench's stream (cli.py:249-250): seed 0,
+    # rank r's gradient is the r-th sequential draw; the pipeline alternates it
+    # with the (P + r)-th draw as the next batch's gradient
+    rng = np.random.default_rng(0)
+    host_grads = []
+    for j in range(P + rank + 1):
+        x = rng.standard_normal(m).astype(np.float32)
+        if j == rank or j == P + rank:
+            host_grads.append(x)
     dgrads = [torch.from_numpy(g).to(dev) for g in host_grads]
 
     def barrier():
@@ -368,7 +374,7 @@ def run_b200(args, rank, world):
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "f32",
-            "data": "synthetic",
+            "data": "synthetic: cli.run_bench draws (seed 0, rank r = draw r; next batch = draw P + r)",
             "config": {
                 "workload": f"resnet50-size gradient m={m} rho={rho} (k={k}), P={P} ranks, one per GPU",
                 "m": m, "k": k, "rho": rho, "P": P, "exchange": exch,
@@ -382,6 +388,13 @@ def run_b200(args, rank, world):
                          "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                          "algorithmic_bytes_per_launch": algo_bytes, "launch_ms": round(main_ms, 5)},
             "stages_ms": {k_: (round(v, 5) if v is not None else None) for k_, v in stage.items()},
+            "exchange_rounds": None if P == 1 else {
+                "rounds": pipe.plan.nsteps,
+                "us_per_round": (round(stage["exchange"] * 1e3 / pipe.plan.nsteps, 2)
+                                 if stage.get("exchange") else None),
+                # k (i32 idx + f32 val) per round over 900 GB/s NVLink 5
+                "nvlink_floor_us_per_round": round(8 * k / 900e3, 3),
+                "note": "per round: push + partner flag + merge (+ K3 after the last round); latency-bound"},
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": 4 * m,
                     "d2h_bytes_per_step": 8},
             "gpu_launches": gpu_launches,
