@@ -273,13 +273,20 @@ __device__ void engine_write(const Src& src, uint32_t s0, uint32_t s1, uint32_t 
 // Returns false (consistently in all blocks) if round 0 holds fewer than kt
 // entries (select: fallback needed; merge: widen the window).
 // keep_all keeps every valid slot (kt = number of valid slots).
+// slice_async: the slice is still landing by cp.async (the caller committed
+// it as the last group); it is awaited after the round-0 bin is found.
 template <int NT, class Src>
 __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt, bool keep_all, uint32_t lo0,
                            uint32_t shift0, const uint32_t* hist0, bool hist0_smem, EngineWS* ws,
-                           EngineSmem<NT>& sm, const Sink& out, unsigned G) {
+                           EngineSmem<NT>& sm, const Sink& out, unsigned G, bool slice_async = false) {
   const unsigned blk = blockIdx.x;
   const bool solo = G == 1;
 
+  if (slice_async && (keep_all || hist0 == nullptr)) {
+    cp_async_wait_all();
+    __syncthreads();
+    slice_async = false;
+  }
   if (keep_all) {
     uint32_t c = 0;
     for (uint32_t s = s0 + threadIdx.x; s < s1; s += NT) {
@@ -386,6 +393,10 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
     }
     sink_stamp(out, 0);
     if (out.trace && r == 0 && blk == 0 && threadIdx.x == 0) out.trace[4] = in_bin;  // diagnostics
+    if (r == 0 && slice_async) {
+      cp_async_wait_all();
+      __syncthreads();
+    }
     uint64_t blo, bhi;
     if (bin < (uint32_t)kBins) {
       blo = (uint64_t)lo + ((uint64_t)bin << shift);

@@ -695,6 +695,7 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
   // issued now and awaited after the candidate copy: their L2 latency hides
   // behind it (the copy's scratch lives in the gather arrays instead)
   for (int b = threadIdx.x; b < kHistLen; b += kFinishThreads) cp_async4(&sm.hist[b], a.ews->hist[0] + b);
+  cp_async_commit();  // group: histogram
   // my tile range and its place in the global (index-ordered) candidate list:
   // the main pass counted the candidates of every block's tile range
   const uint32_t per = a.tiles_per_group;
@@ -746,27 +747,39 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
         const uint32_t inf = s_cnt[lo];
         if (inf & kOvfBit) continue;  // dense tiles are copied below
         const size_t src = (size_t)(tb + lo) * a.slots + (jj - s_dst[lo]);
-        di[jj] = __ldcg(a.slot_idx + src);
-        dv[jj] = __ldcg(a.slot_val + src);
+        if (in_smem) {  // async: lands while the k-th key's bin is found
+          cp_async4(di + jj, a.slot_idx + src);
+          cp_async4(dv + jj, a.slot_val + src);
+        } else {
+          di[jj] = __ldcg(a.slot_idx + src);
+          dv[jj] = __ldcg(a.slot_val + src);
+        }
       }
       for (uint32_t q = warp_id(); q < nt; q += kFinishThreads / 32) {  // dense tiles
         const uint32_t inf = s_cnt[q];
         if (!(inf & kOvfBit)) continue;
         const uint32_t cnt = inf & ~kOvfBit, ob = s_ovf[q], dst = s_dst[q];
         for (uint32_t e = lane_id(); e < cnt; e += 32) {
-          di[dst + e] = __ldcg(a.ovf_idx + ob + e);
-          dv[dst + e] = __ldcg(a.ovf_val + ob + e);
+          if (in_smem) {
+            cp_async4(di + dst + e, a.ovf_idx + ob + e);
+            cp_async4(dv + dst + e, a.ovf_val + ob + e);
+          } else {
+            di[dst + e] = __ldcg(a.ovf_idx + ob + e);
+            dv[dst + e] = __ldcg(a.ovf_val + ob + e);
+          }
         }
       }
       run += tot;
       __syncthreads();
     }
     finish_stamp(a, 2);
-    cp_async_wait_all();
+    cp_async_commit();    // group: the slice
+    cp_async_wait<1>();   // the histogram has landed; the slice may still be in flight
     __syncthreads();
     SliceSrc src{s_idx, s_val, a.ord_idx, a.ord_val, before, in_smem, false};
     if (engine_run<kFinishThreads>(src, before, before + own, a.k, false, __ldcg(&a.ctl->lo),
-                                   __ldcg(&a.ctl->shift), sm.hist, true, a.ews, sm, out, G))
+                                   __ldcg(&a.ctl->shift), sm.hist, true, a.ews, sm, out, G,
+                                   /*slice_async=*/true))
       return;
   }
   // exact dense fallback over acc (= res_out, untouched so far)
