@@ -199,20 +199,22 @@ int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedule, int32_t
                        int32_t* step_counts, const int32_t* in_idx, const float* in_val,
                        const int32_t* d_in_n, void* ws, size_t ws_bytes, void* stream);
 
-/* gtk_gtopk_exchange + K3 in the same kernel (P > 1): after the last step the
- * final global list updates w (w[i] -= FLOAT(lr) * u(v), u as in
- * gtk_scatter_update) and every entry of the local selection in_* that is not
- * in the global list returns to res (res[i] += v) -- optimizer.py:227-230,
+/* gtk_gtopk_exchange + K3 in the same kernel (P > 1): the writer of the final
+ * global list also updates w (w[i] -= FLOAT(lr) * u(v), u as in
+ * gtk_scatter_update) and tags its members (d_tags[i] = low 32 bits of the
+ * device epoch); after one grid barrier every entry of the local selection
+ * in_* whose tag is stale returns to res (res[i] += v) -- optimizer.py:227-230,
  * :243.  Skipped on any GTK_DEV_* error bit, like gtk_scatter_update's d_skip.
  * Sparse-exact form only (finite lr, sign bit clear; no momentum); in_* is
- * required; nsteps > 0 (one rank: gtk_select_update). */
+ * required; nsteps > 0 (one rank: gtk_select_update).
+ *   d_tags: device uint32[m], zeroed once, owned per exchange plan. */
 int gtk_gtopk_exchange_update(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
                               void* const* peer_inbox, uint64_t* const* peer_flags, uint64_t* d_epoch,
                               int32_t* acc_idx, float* acc_val, int32_t* d_acc_n, int32_t k,
                               uint32_t* d_status, const uint32_t* d_abort, int64_t timeout_ns,
                               int32_t* step_counts, const int32_t* in_idx, const float* in_val,
                               const int32_t* d_in_n, void* ws, size_t ws_bytes, float* w, float* res,
-                              float lr, int32_t scaling, void* stream);
+                              float lr, int32_t scaling, uint32_t* d_tags, void* stream);
 
 /* ------------------------------------------------------------------------
  * Profiling hooks (bench.py; not part of the reference interface).

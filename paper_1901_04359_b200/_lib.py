@@ -107,7 +107,7 @@ _SIGS = {
     ),
     "gtk_gtopk_exchange_update": (
         [_I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P, _P, _F,
-         _I32, _P],
+         _I32, _P, _P],
         _I32,
     ),
     "gtk_prof_enable": ([_I32], _I32),

@@ -63,30 +63,10 @@ struct ExchangeArgs {
   float* upd_res;
   float upd_lr;
   int upd_scaling;
+  uint32_t* upd_tags;    // u32[m]: tags[i] = low 32 bits of the epoch when i is in this call's global list
   MergeArgs merge;       // workspace pointers; list pointers filled per step
 };
 
-// first position in the sorted a[0, n) with a[pos] >= x (strict: > x), one full
-// warp, 33-ary: ceil(log33 n) dependent round trips instead of log2 n
-__device__ __forceinline__ uint32_t warp_search(const int32_t* a, uint32_t n, int32_t x, bool strict) {
-  uint32_t L = 0, H = n;  // answer in [L, H]
-  const unsigned lane = lane_id();
-  while (H > L) {
-    const uint32_t len = H - L;
-    if (len <= 32) {
-      const bool lt = lane < len && (strict ? __ldcg(a + L + lane) <= x : __ldcg(a + L + lane) < x);
-      return L + __popc(__ballot_sync(kFull, lt));
-    }
-    const uint32_t p = L + (uint32_t)(((uint64_t)len * (lane + 1)) / 33);  // probes, ascending
-    const bool lt = strict ? __ldcg(a + p) <= x : __ldcg(a + p) < x;
-    const int t = __popc(__ballot_sync(kFull, lt));  // probes below the answer
-    const uint32_t p_prev = __shfl_sync(kFull, p, t > 0 ? t - 1 : 0);
-    const uint32_t p_t = __shfl_sync(kFull, p, t < 32 ? t : 31);
-    if (t > 0) L = p_prev + 1;
-    if (t < 32) H = p_t;
-  }
-  return L;
-}
 
 // inbox slot: 16 B header {count, hint} | idx[k4] | val[k4], k4 = k rounded up
 // to 4 so both arrays are 16-byte aligned for 128-bit peer stores
@@ -138,6 +118,11 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   const bool self_poison = (__ldcg(a.d_status) & GTK_DEV_NONFINITE) != 0;
   const bool tr = a.trace && blk == 0 && threadIdx.x == 0;
   if (tr) a.trace[0] = (int64_t)globaltimer();
+
+  // the step whose receive writes the final global list into acc (K3's tags)
+  int last_recv = -1;
+  for (int s = 0; s < a.nsteps; ++s)
+    if (a.steps[s].recv_from >= 0) last_recv = s;
 
   // the current list: the caller's input until the first merge/copy writes acc
   const int32_t* cur_idx = a.in_idx ? a.in_idx : a.acc_idx;
@@ -228,13 +213,20 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
         m.o_val = a.acc_val;
         m.d_no = a.d_acc_n;
         m.trace = a.trace ? a.trace + 32 + 16 * s : nullptr;
+        if (a.upd_w && s == last_recv) {  // the final global list: K3's membership tags
+          m.tag = a.upd_tags;
+          m.tag_val = (uint32_t)epoch;
+        }
         merge_device(m, n_in, n_own, hint_in, hint_own, G, S, wrec, wv);
       } else {
         const uint32_t per = (n_in + G - 1) / G;
         const uint32_t e0 = min(n_in, blk * per), e1 = min(n_in, e0 + per);
+        const bool k3 = a.upd_w && s == last_recv;  // the broadcast's copy is the final global list
         for (uint32_t e = e0 + threadIdx.x; e < e1; e += kMergeThreads) {
-          a.acc_idx[e] = __ldcg(in_idx + e);
+          const int32_t i = __ldcg(in_idx + e);
+          a.acc_idx[e] = i;
           a.acc_val[e] = __ldcg(in_val + e);
+          if (k3) a.upd_tags[i] = (uint32_t)epoch;
         }
         if (blk == 0 && threadIdx.x == 0) {
           a.d_acc_n[0] = (int32_t)n_in;
@@ -257,8 +249,10 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
     const uint32_t per = (n + G - 1) / G;
     const uint32_t e0 = min(n, blk * per), e1 = min(n, e0 + per);
     for (uint32_t e = e0 + threadIdx.x; e < e1; e += kMergeThreads) {
-      a.acc_idx[e] = __ldcg(a.in_idx + e);
+      const int32_t i = __ldcg(a.in_idx + e);
+      a.acc_idx[e] = i;
       a.acc_val[e] = __ldcg(a.in_val + e);
+      if (a.upd_w) a.upd_tags[i] = (uint32_t)epoch;
     }
     if (blk == 0 && threadIdx.x == 0) {
       a.d_acc_n[0] = (int32_t)n;
@@ -266,45 +260,26 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
     }
   }
   if (a.upd_w) {
-    // K3 (gtk_update.cu, sparse-exact form) on the final global list
-    grid_sync(&a.merge.ews->bar, G);  // acc complete; status final
+    // K3 once the status is final (a failed step must leave the state
+    // untouched on every rank): the global list updates w; local entries
+    // whose membership tag (set by the final list's writer) is not this
+    // call's epoch missed the global list and return to the residual
+    grid_sync(&a.merge.ews->bar, G);  // every tag and the status word final
     if (!(__ldcg(a.d_status) & GTK_DEV_ERROR_MASK)) {
       const uint32_t gn = min((uint32_t)__ldcg(a.d_acc_n), (uint32_t)a.k);
+      const uint32_t ln = min((uint32_t)__ldcg(a.d_in_n), (uint32_t)a.k);
+      const uint32_t ep32 = (uint32_t)epoch;
       const float Pf = (float)a.P;
-      for (uint32_t e = blk * kMergeThreads + threadIdx.x; e < gn; e += G * kMergeThreads) {
-        const int32_t i = __ldcg(a.acc_idx + e);
-        const float u = scale_u(__ldcg(a.acc_val + e), Pf, a.upd_scaling);
-        a.upd_w[i] = __fsub_rn(a.upd_w[i], __fmul_rn(a.upd_lr, u));
-      }
-      // extra residual: my slice of the local list, membership by a search of
-      // the slice's index range in the global list, then in shared memory
-      uint32_t ln = min((uint32_t)__ldcg(a.d_in_n), (uint32_t)a.k);
-      const uint32_t per = (ln + G - 1) / G;
-      const uint32_t l0 = min(ln, blk * per), l1 = min(ln, l0 + per);
-      if (l0 < l1) {
-        int32_t* s_g = S.slice_idx;  // free after the merges
-        if (warp_id() < 2) {
-          const int32_t x = __ldcg(a.in_idx + (warp_id() == 0 ? l0 : l1 - 1));
-          const uint32_t pos = warp_search(a.acc_idx, gn, x, warp_id() == 1);
-          if (lane_id() == 0) (warp_id() == 0 ? s_n : s_hint) = pos;
+      const uint32_t stride = G * kMergeThreads;
+      for (uint32_t e = blk * kMergeThreads + threadIdx.x; e < max(gn, ln); e += stride) {
+        if (e < gn) {
+          const int32_t i = __ldcg(a.acc_idx + e);
+          const float u = scale_u(__ldcg(a.acc_val + e), Pf, a.upd_scaling);
+          a.upd_w[i] = __fsub_rn(a.upd_w[i], __fmul_rn(a.upd_lr, u));
         }
-        __syncthreads();
-        const uint32_t g0 = s_n, g1 = s_hint, gl = g1 - g0;
-        const bool fits = gl <= (uint32_t)kMergeSliceCap;
-        if (fits)
-          for (uint32_t j = threadIdx.x; j < gl; j += kMergeThreads) s_g[j] = __ldcg(a.acc_idx + g0 + j);
-        __syncthreads();
-        for (uint32_t e = l0 + threadIdx.x; e < l1; e += kMergeThreads) {
-          const int32_t x = __ldcg(a.in_idx + e);
-          uint32_t lo = 0, hi = gl;
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            const int32_t y = fits ? s_g[mid] : __ldcg(a.acc_idx + g0 + mid);
-            if (y < x) lo = mid + 1;
-            else hi = mid;
-          }
-          const bool found = lo < gl && (fits ? s_g[lo] : __ldcg(a.acc_idx + g0 + lo)) == x;
-          if (!found) a.upd_res[x] = __fadd_rn(a.upd_res[x], __ldcg(a.in_val + e));
+        if (e < ln) {
+          const int32_t i = __ldcg(a.in_idx + e);
+          if (__ldcg(a.upd_tags + i) != ep32) a.upd_res[i] = __fadd_rn(a.upd_res[i], __ldcg(a.in_val + e));
         }
       }
     }
@@ -376,7 +351,7 @@ static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32
                          int32_t* d_acc_n, int32_t k, uint32_t* d_status, const uint32_t* d_abort,
                          int64_t timeout_ns, int32_t* step_counts, const int32_t* in_idx, const float* in_val,
                          const int32_t* d_in_n, void* ws, size_t ws_bytes, float* upd_w, float* upd_res,
-                         float upd_lr, int32_t upd_scaling, void* stream);
+                         float upd_lr, int32_t upd_scaling, uint32_t* upd_tags, void* stream);
 
 extern "C" int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
                                   void* const* peer_inbox, uint64_t* const* peer_flags, uint64_t* d_epoch,
@@ -386,7 +361,7 @@ extern "C" int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedu
                                   const int32_t* d_in_n, void* ws, size_t ws_bytes, void* stream) {
   return exchange_impl(rank, P, schedule, nsteps, peer_inbox, peer_flags, d_epoch, acc_idx, acc_val, d_acc_n, k,
                        d_status, d_abort, timeout_ns, step_counts, in_idx, in_val, d_in_n, ws, ws_bytes, nullptr,
-                       nullptr, 0.0f, 0, stream);
+                       nullptr, 0.0f, 0, nullptr, stream);
 }
 
 extern "C" int gtk_gtopk_exchange_update(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
@@ -395,13 +370,13 @@ extern "C" int gtk_gtopk_exchange_update(int32_t rank, int32_t P, const int32_t*
                                          uint32_t* d_status, const uint32_t* d_abort, int64_t timeout_ns,
                                          int32_t* step_counts, const int32_t* in_idx, const float* in_val,
                                          const int32_t* d_in_n, void* ws, size_t ws_bytes, float* w, float* res,
-                                         float lr, int32_t scaling, void* stream) {
-  if (!w || !res || !in_idx || scaling < 0 || scaling > 2 || !std::isfinite(lr) || std::signbit(lr))
+                                         float lr, int32_t scaling, uint32_t* d_tags, void* stream) {
+  if (!w || !res || !in_idx || !d_tags || scaling < 0 || scaling > 2 || !std::isfinite(lr) || std::signbit(lr))
     return GTK_EINVAL;
   if (nsteps == 0) return GTK_EINVAL;  // one rank: gtk_select_update
   return exchange_impl(rank, P, schedule, nsteps, peer_inbox, peer_flags, d_epoch, acc_idx, acc_val, d_acc_n, k,
                        d_status, d_abort, timeout_ns, step_counts, in_idx, in_val, d_in_n, ws, ws_bytes, w, res, lr,
-                       scaling, stream);
+                       scaling, d_tags, stream);
 }
 
 static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps, void* const* peer_inbox,
@@ -409,7 +384,7 @@ static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32
                          int32_t* d_acc_n, int32_t k, uint32_t* d_status, const uint32_t* d_abort,
                          int64_t timeout_ns, int32_t* step_counts, const int32_t* in_idx, const float* in_val,
                          const int32_t* d_in_n, void* ws, size_t ws_bytes, float* upd_w, float* upd_res,
-                         float upd_lr, int32_t upd_scaling, void* stream) {
+                         float upd_lr, int32_t upd_scaling, uint32_t* upd_tags, void* stream) {
   if (P < 1 || P > kMaxRanks || rank < 0 || rank >= P || nsteps < 0 || nsteps > kMaxSteps || k < 1)
     return GTK_EINVAL;
   if (!acc_idx || !acc_val || !d_acc_n || !d_status || !ws || !d_epoch) return GTK_EINVAL;
@@ -449,6 +424,7 @@ static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32
   a.upd_res = upd_res;
   a.upd_lr = upd_lr;
   a.upd_scaling = upd_scaling;
+  a.upd_tags = upd_tags;
   char* base = (char*)ws;
   a.merge = MergeArgs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, (uint32_t)k, nullptr, nullptr,
                       nullptr, (MergeCtl*)(base + L.ctl), (EngineWS*)(base + L.engine),

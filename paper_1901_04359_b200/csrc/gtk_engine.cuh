@@ -111,6 +111,8 @@ struct Sink {
   float upd_lr;
   float upd_Pf;
   int upd_scaling;
+  uint32_t* tag;      // exchange + K3: tag[idx] = tag_val marks membership of the final global list (nullable)
+  uint32_t tag_val;
 };
 
 // one kept entry to the output list (+ the select's side effects)
@@ -119,6 +121,7 @@ __device__ __forceinline__ void sink_put(const Sink& out, uint32_t p, int32_t i,
   out.o_val[p] = v;
   if (out.zero_at) out.zero_at[i] = 0.0f;
   if (out.upd_w) out.upd_w[i] = __fsub_rn(out.upd_w[i], __fmul_rn(out.upd_lr, scale_u(v, out.upd_Pf, out.upd_scaling)));
+  if (out.tag) out.tag[i] = out.tag_val;
 }
 
 __device__ __forceinline__ void sink_stamp(const Sink& out, int i) {

@@ -75,6 +75,13 @@ struct MergeArgs {
   int32_t* u_idx;  // global slot scratch for slices larger than kMergeSliceCap
   float* u_val;
   int64_t* trace;  // optional %globaltimer stamps of block 0 (phase boundaries)
+  // fused K3 on the output (the exchange's last step): w update + membership tags
+  float* upd_w;
+  float upd_lr;
+  float upd_Pf;
+  int upd_scaling;
+  uint32_t* tag;
+  uint32_t tag_val;
 };
 
 __device__ __forceinline__ void merge_stamp(const MergeArgs& a, int i) {
@@ -336,7 +343,8 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   const bool keep_all = n_valid <= a.k;
   const SliceSrc src{S.slice_idx, S.slice_val, a.u_idx, a.u_val, d0, in_smem, true};
   const Sink out{a.o_idx, a.o_val, a.d_no, nullptr, true, a.trace ? a.trace + 5 : nullptr,
-                 keep_all ? nullptr : rec, rec_level, rec_tau, rec_tau2, 3u};
+                 keep_all ? nullptr : rec, rec_level, rec_tau, rec_tau2, 3u,
+                 a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling, a.tag, a.tag_val};
   const uint32_t* h0 = solo ? esm.hist : a.ews->hist[0];
   bool ok = engine_run<kMergeThreads>(src, d0, d1, keep_all ? n_valid : a.k, keep_all, win_lo, win_shift, h0, solo,
                                       a.ews, esm, out, G);

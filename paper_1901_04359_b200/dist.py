@@ -83,6 +83,7 @@ class _ExchangePlan:
         self.step_counts = torch.zeros(max(2 * self.nsteps, 2), dtype=torch.int32, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.epoch = torch.zeros(1, dtype=torch.int64, device=dev)  # advanced by the kernel
+        self.tags = None  # u32[m] K3 membership tags (gtk_gtopk_exchange_update), allocated on first use
         dist.barrier(group=group.gloo)  # every rank mapped every peer before first use
 
     def close(self):
@@ -167,7 +168,9 @@ class DistDeviceGroup:
                 P(plan.ws), ctypes.c_size_t(plan.ws.numel())]
         if update is not None and src is not None and plan.nsteps > 0:
             w, res, lr, scaling = update
-            _lib.call("gtk_gtopk_exchange_update", *args, P(w), P(res), ctypes.c_float(lr), scaling,
+            if plan.tags is None or plan.tags.numel() < lst.dim:
+                plan.tags = torch.zeros(lst.dim, dtype=torch.int32, device=self.device)  # membership tags
+            _lib.call("gtk_gtopk_exchange_update", *args, P(w), P(res), ctypes.c_float(lr), scaling, P(plan.tags),
                       _dev.stream_of(self.device))
             return
         _lib.call("gtk_gtopk_exchange", *args, _dev.stream_of(self.device))
