@@ -429,10 +429,12 @@ static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32
   a.merge = MergeArgs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, (uint32_t)k, nullptr, nullptr,
                       nullptr, (MergeCtl*)(base + L.ctl), (EngineWS*)(base + L.engine),
                       (int32_t*)(base + L.u_idx), (float*)(base + L.u_val)};
-  int G = merge_grid_for((const void*)exchange_kernel, k);
+  uint32_t sc = 0;
+  int G = merge_grid_for((const void*)exchange_kernel, k, &sc);
   if (G <= 0) return GTK_ECUDA;
+  a.merge.slice_cap = sc;
   void* args[] = {&a};
   ProfScope prof(kProfExchange, (cudaStream_t)stream);
-  return coop_launch((const void*)exchange_kernel, G, kMergeThreads, args, sizeof(MergeSmem), (cudaStream_t)stream,
+  return coop_launch((const void*)exchange_kernel, G, kMergeThreads, args, merge_smem_bytes(sc), (cudaStream_t)stream,
                      true);
 }

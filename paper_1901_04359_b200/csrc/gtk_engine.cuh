@@ -27,7 +27,8 @@ constexpr int kHistLen = kBins + 1;         // + OVER
 constexpr int kHistStride = 2056;           // padded
 constexpr int kRounds = 4;
 constexpr int kGatherCap = 1024;  // gather buffer size
-constexpr int kGatherMax = 384;   // gather (O(n^2) ranking) only bins this small; else refine
+constexpr int kGatherMax = 384;   // gathered entries loaded speculatively with the count after the barrier
+constexpr int kRankDirect = 96;   // gathers up to this size are ranked O(n^2) directly; larger via a sub-histogram
 constexpr int kMaxBlocks = 1024;
 
 struct EngineWS {
@@ -42,7 +43,7 @@ struct EngineWS {
   uint32_t cta_b[kMaxBlocks];
 };
 
-constexpr uint32_t kKeptBits = 8192;  // slice slots covered by the kept bitmap
+constexpr uint32_t kKeptBits = 32768;  // slice slots covered by the kept bitmap (a finish slice is <= 20480)
 constexpr uint32_t kSlotBits = 22;    // gather record: (block << 22) | slot within the block's slice
 
 template <int NT>
@@ -52,6 +53,8 @@ struct EngineSmem {
   int32_t gidx[kGatherCap];
   uint32_t gblk[kGatherCap];
   uint32_t kept_bits[kKeptBits / 32];  // my slice's in-bin winners
+  uint32_t wcnt[NT];                    // engine_write: kept per (row, warp), then their exclusive scan
+  uint32_t wbal[NT];                    // engine_write: kept ballot per (row, warp)
   uint32_t scan[NT / 32 + 2];
   uint32_t bcast[8];
   uint32_t ng;
@@ -226,45 +229,90 @@ __device__ bool engine_find_bin(const uint32_t* hist, bool in_smem, uint32_t t, 
   return tot >= t && bin != 0xFFFFFFFFu;
 }
 
+// Up to kSinkBatch kept entries (bi, bv) to output positions bp: every
+// dependent load (w[idx] of the fused update) is issued before the first
+// store, so a thread with many winners pays one memory round trip per batch,
+// not one per entry (the stores could alias the next entry's load as far as
+// the compiler knows, so a plain loop of sink_put serialises them).
+constexpr int kSinkBatch = 4;
+__device__ __forceinline__ void sink_put_batch(const Sink& out, const uint32_t (&bp)[kSinkBatch],
+                                               const int32_t (&bi)[kSinkBatch], const float (&bv)[kSinkBatch],
+                                               int n) {
+  float wv[kSinkBatch];
+  if (out.upd_w) {
+#pragma unroll
+    for (int j = 0; j < kSinkBatch; ++j)
+      if (j < n) wv[j] = out.upd_w[bi[j]];
+  }
+#pragma unroll
+  for (int j = 0; j < kSinkBatch; ++j) {
+    if (j >= n) break;
+    const int32_t i = bi[j];
+    const float v = bv[j];
+    out.o_idx[bp[j]] = i;
+    out.o_val[bp[j]] = v;
+    if (out.zero_at) out.zero_at[i] = 0.0f;
+    if (out.upd_w) out.upd_w[i] = __fsub_rn(wv[j], __fmul_rn(out.upd_lr, scale_u(v, out.upd_Pf, out.upd_scaling)));
+    if (out.tag) out.tag[i] = out.tag_val;
+  }
+}
+
 // Stable index-order write of my slice's kept entries at out_pos.. .
-// keep(key, idx) decides; returns nothing (positions via block scans).
+// keep(key, idx, slot) decides; positions via one block scan per chunk.
+// A chunk is 32 rows of NT slots, thread t reading slot row * NT + t of
+// each row (conflict-free shared-memory reads, consecutive lanes writing
+// consecutive output positions); the per-(row, warp) kept counts -- 32 x
+// NT/32 = NT of them -- are scanned in one block scan.
 template <int NT, class Src, class Keep>
 __device__ void engine_write(const Src& src, uint32_t s0, uint32_t s1, uint32_t out_pos, const Keep& keep_fn,
                              EngineSmem<NT>& sm, const Sink& out) {
-  if (s1 - s0 <= 32u * NT) {
-    // one block scan: thread t owns the contiguous run [s0 + t*per, +per)
-    const uint32_t per = (s1 - s0 + NT - 1) / NT;
-    const uint32_t r0 = min(s1, s0 + threadIdx.x * per), r1 = min(s1, r0 + per);
-    uint32_t bits = 0;
-    for (uint32_t s = r0; s < r1; ++s) {
+  constexpr int NW = NT / 32;
+  const unsigned lane = lane_id(), w = warp_id();
+  for (uint32_t c0 = s0; c0 < s1; c0 += 32u * NT) {
+    const uint32_t nrows = min(32u, (s1 - c0 + NT - 1) / NT);
+    uint32_t kbits = 0;
+    for (uint32_t r = 0; r < nrows; ++r) {
+      const uint32_t s = c0 + r * NT + threadIdx.x;
       uint32_t key;
       int32_t i;
       float v;
-      if (src.get(s, key, i, v) && keep_fn(key, i, s - s0)) bits |= 1u << (s - r0);
+      const bool kept = s < s1 && src.get(s, key, i, v) && keep_fn(key, i, s - s0);
+      const unsigned bal = __ballot_sync(kFull, kept);
+      if (lane == 0) {
+        sm.wcnt[r * NW + w] = __popc(bal);
+        sm.wbal[r * NW + w] = bal;
+      }
+      kbits |= (uint32_t)kept << r;
     }
+    __syncthreads();
     uint32_t k_tot;
-    uint32_t p = out_pos + block_excl_scan<NT>(__popc(bits), sm.scan, &k_tot);
-    for (; bits; bits &= bits - 1) {
-      const uint32_t s = r0 + __ffs(bits) - 1;
-      uint32_t key;
-      int32_t i;
-      float v;
-      src.get(s, key, i, v);
-      sink_put(out, p++, i, v);
+    const uint32_t cnt = threadIdx.x < nrows * NW ? sm.wcnt[threadIdx.x] : 0u;
+    const uint32_t ex = block_excl_scan<NT>(cnt, sm.scan, &k_tot);
+    sm.wcnt[threadIdx.x] = ex;
+    __syncthreads();
+    if (c0 == s0) sink_stamp(out, 5);
+    const unsigned lt = lanemask_lt();
+    while (kbits) {
+      uint32_t bp[kSinkBatch];
+      int32_t bi[kSinkBatch];
+      float bv[kSinkBatch];
+      int n = 0;
+#pragma unroll
+      for (int j = 0; j < kSinkBatch; ++j) {
+        if (kbits) {
+          const uint32_t r = __ffs(kbits) - 1;
+          kbits &= kbits - 1;
+          uint32_t key;
+          src.get(c0 + r * NT + threadIdx.x, key, bi[j], bv[j]);
+          bp[j] = out_pos + sm.wcnt[r * NW + w] + __popc(sm.wbal[r * NW + w] & lt);
+          n = j + 1;
+        }
+      }
+      sink_put_batch(out, bp, bi, bv, n);
     }
-    return;
-  }
-  for (uint32_t base = s0; base < s1; base += NT) {
-    const uint32_t s = base + threadIdx.x;
-    uint32_t key = 0;
-    int32_t i = 0;
-    float v = 0.f;
-    bool keep = false;
-    if (s < s1 && src.get(s, key, i, v)) keep = keep_fn(key, i, s - s0);
-    uint32_t k_tot;
-    const uint32_t k_rank = block_excl_scan<NT>(keep ? 1u : 0u, sm.scan, &k_tot);
-    if (keep) sink_put(out, out_pos + k_rank, i, v);
     out_pos += k_tot;
+    __syncthreads();  // sm.wcnt is reused by the next chunk
+    if (c0 == s0) sink_stamp(out, 6);
   }
 }
 
@@ -412,26 +460,34 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
     const uint32_t t_in = t - above;  // rank of the target inside the bin
     const bool single_key = (bhi - blo == 1);
     // the last round always gathers if it can (a bin is then at most 8 keys wide)
-    if (in_bin <= (uint32_t)kGatherMax || (in_bin <= (uint32_t)kGatherCap && (r == kRounds - 1 || shift <= 3))) {
+    if (in_bin <= (uint32_t)kGatherCap) {
       // ---- finish with one barrier: gather (key, idx, block) of the bin ------
       uint32_t n_above = 0;
       if (solo && threadIdx.x == 0) sm.ng = 0;
       if (solo) __syncthreads();
-      for (uint32_t s = s0 + threadIdx.x; s < s1; s += NT) {
-        uint32_t key;
-        int32_t i;
+      // (block-uniform trip count: the in-bin slots are reserved with one
+      // atomic per warp)
+      for (uint32_t sb0 = s0; sb0 < s1; sb0 += NT) {
+        const uint32_t s = sb0 + threadIdx.x;
+        uint32_t key = 0;
+        int32_t i = 0;
         float v;
-        if (!src.get(s, key, i, v)) continue;
-        if ((uint64_t)key >= bhi) {
-          ++n_above;
-        } else if (key >= blo) {
+        const bool valid = s < s1 && src.get(s, key, i, v);
+        n_above += valid && (uint64_t)key >= bhi;
+        const bool inb = valid && (uint64_t)key < bhi && key >= blo;
+        const unsigned bal = __ballot_sync(kFull, inb);
+        if (bal == 0u) continue;
+        uint32_t p0 = 0;
+        if (lane_id() == (unsigned)(__ffs(bal) - 1))
+          p0 = atomicAdd(solo ? &sm.ng : &ws->gather_n[r], (uint32_t)__popc(bal));
+        p0 = __shfl_sync(kFull, p0, __ffs(bal) - 1);
+        if (inb) {
+          const uint32_t p = p0 + __popc(bal & lanemask_lt());
           if (solo) {
-            const uint32_t p = atomicAdd(&sm.ng, 1u);
             sm.keys[p] = key;
             sm.gidx[p] = i;
             sm.gblk[p] = (blk << kSlotBits) | (s - s0);
           } else {
-            const uint32_t p = atomicAdd(&ws->gather_n[r], 1u);
             ws->gather_key[p] = key;
             ws->gather_idx[p] = i;
             ws->gather_blk[p] = (blk << kSlotBits) | (s - s0);
@@ -462,20 +518,47 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       above_before = block_sum<NT>(above_before, sm.scan);  // also publishes sm.keys / sm.ng
       sink_stamp(out, 1);
       const uint32_t ng = sm.ng;
-      // tau = t_in-th largest gathered key; gt = # gathered keys > tau
+      // tau = t_in-th largest gathered key; gt = # gathered keys > tau.  A
+      // large gather is first narrowed in shared memory: a 2048-way histogram
+      // of the bin [blo, bhi) over the gathered keys (every block holds the
+      // same gathered set, so no barrier), then the O(n^2) rank runs only over
+      // the sub-bin holding t_in.
+      const uint32_t* rk = sm.keys;  // the keys ranked below
+      uint32_t nr = ng, r_t = t_in, r_above = 0;
+      if (ng > (uint32_t)kRankDirect) {
+        const uint64_t width = bhi - blo;
+        const uint32_t ss = width <= (uint64_t)kBins ? 0u : ceil_log2_u64((width + kBins - 1) / kBins);
+        for (int b = threadIdx.x; b < kHistLen; b += NT) sm.hist[b] = 0;
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < ng; j += NT) atomicAdd(&sm.hist[(sm.keys[j] - (uint32_t)blo) >> ss], 1u);
+        __syncthreads();
+        uint32_t sb, sab, sin;
+        engine_find_bin<NT>(sm.hist, true, t_in, sm, sb, sab, sin);
+        const uint32_t r_lo = (uint32_t)blo + (sb << ss), r_hi = r_lo + ((1u << ss) - 1u);  // inclusive
+        if (threadIdx.x == 0) sm.bcast[7] = 0;
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < ng; j += NT) {  // the sub-bin's keys -> sm.hist[0, sin)
+          const uint32_t x = sm.keys[j];
+          if (x >= r_lo && x <= r_hi) sm.hist[atomicAdd(&sm.bcast[7], 1u)] = x;
+        }
+        rk = sm.hist;
+        nr = sin;
+        r_t = t_in - sab;
+        r_above = sab;
+      }
       if (threadIdx.x == 0) sm.bcast[3] = sm.bcast[4] = 0;
       __syncthreads();
-      for (uint32_t j = threadIdx.x; j < ng; j += NT) {
-        const uint32_t x = sm.keys[j];
+      for (uint32_t j = threadIdx.x; j < nr; j += NT) {
+        const uint32_t x = rk[j];
         uint32_t gt = 0, ge = 0;
-        for (uint32_t q = 0; q < ng; ++q) {
-          const uint32_t y = sm.keys[q];
+        for (uint32_t q = 0; q < nr; ++q) {
+          const uint32_t y = rk[q];
           gt += (y > x);
           ge += (y >= x);
         }
-        if (gt < t_in && ge >= t_in) {
+        if (gt < r_t && ge >= r_t) {
           sm.bcast[3] = x;
-          sm.bcast[4] = gt;
+          sm.bcast[4] = r_above + gt;
         }
       }
       __syncthreads();
@@ -485,8 +568,15 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       // kept flags of the gathered entries: winners of my slice go to a
       // bitmap indexed by slot (O(1) lookup in the write), the ones of
       // earlier blocks shift my output offset
+      // the gathered entries equal to tau (their indices) -> sm.hist[0, n_eq):
+      // the index-order tie ranks run over that short list only
       for (uint32_t w = threadIdx.x; w < kKeptBits / 32; w += NT) sm.kept_bits[w] = 0;
+      if (threadIdx.x == 0) sm.bcast[7] = 0;
       __syncthreads();
+      for (uint32_t j = threadIdx.x; j < ng; j += NT)
+        if (sm.keys[j] == tau) sm.hist[atomicAdd(&sm.bcast[7], 1u)] = (uint32_t)sm.gidx[j];
+      __syncthreads();
+      const uint32_t n_eq = sm.bcast[7];
       uint32_t extra = 0;
       for (uint32_t j = threadIdx.x; j < ng; j += NT) {
         const uint32_t x = sm.keys[j];
@@ -494,7 +584,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
         if (x == tau) {
           uint32_t rank = 0;
           const int32_t ij = sm.gidx[j];
-          for (uint32_t q = 0; q < ng; ++q) rank += (sm.keys[q] == tau && sm.gidx[q] < ij);
+          for (uint32_t q = 0; q < n_eq; ++q) rank += (int32_t)sm.hist[q] < ij;
           kept = rank < need;
         }
         const uint32_t gb = sm.gblk[j] >> kSlotBits, slot = sm.gblk[j] & ((1u << kSlotBits) - 1);

@@ -20,7 +20,7 @@ int coop_launch(const void* func, int grid, int threads, void** args, size_t sme
 // opt a kernel into > 48 KB of dynamic shared memory (once per device); false on error
 bool ensure_dyn_smem(const void* func, size_t bytes);
 // blocks for a cooperative ⊤-merge kernel over lists of <= cap entries
-int merge_grid_for(const void* func, int32_t cap);
+int merge_grid_for(const void* func, int32_t cap, uint32_t* slice_cap);
 
 // Launch with the programmatic-stream-serialization attribute: the kernel may
 // start as soon as the previous kernel in the stream executes

@@ -2,6 +2,8 @@
 // cooperative launch; the algorithm lives in gtk_merge.cuh.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "gtk_internal.h"
 #include "gtk_merge.cuh"
 
@@ -15,29 +17,37 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
   merge_device(a, na, nb, ha, hb, gridDim.x, S);
 }
 
-// blocks for a merge of two lists of <= cap entries: ~2K merged slots per
-// block (slices stay in shared memory), capped at one block per SM
-int merge_grid_for(const void* func, int32_t cap) {
-  if (!ensure_dyn_smem(func, sizeof(MergeSmem))) return 0;
-  // ~512 merged slots per block: the engine's phases are latency-bound, more
-  // blocks shorten each (measured: 2048 -> 512 takes k = 25.6K from 21 to 16.5 us)
-  const int want = (int)((2LL * cap + kMergeSlotsPerBlock - 1) / kMergeSlotsPerBlock);
-  int g = coop_grid(func, kMergeThreads, sizeof(MergeSmem));
-  if (g <= 0) return 0;
+// blocks and shared-memory slice capacity for a merge of two lists of <= cap
+// entries: ~512 merged slots per block (the engine's phases are latency-bound,
+// more blocks shorten each: measured 2048 -> 512 takes k = 25.6K from 21 to
+// 16.5 us), at most one block per SM; the slice capacity covers the expected
+// slice (large k) up to kMergeSliceCapMax
+int merge_grid_for(const void* func, int32_t cap, uint32_t* slice_cap) {
+  if (!ensure_dyn_smem(func, merge_smem_bytes(kMergeSliceCapMax))) return 0;
   const int lim = num_sms();
-  if (g > lim) g = lim;
-  if (want < g) g = want < 1 ? 1 : want;
+  if (lim <= 0) return 0;
+  const int want = (int)((2LL * cap + kMergeSlotsPerBlock - 1) / kMergeSlotsPerBlock);
+  int g = want < lim ? (want < 1 ? 1 : want) : lim;
   if (g > kMaxBlocks) g = kMaxBlocks;
+  const uint64_t per = (2ull * (uint64_t)cap + g - 1) / g;
+  uint32_t sc = kMergeSliceCap;
+  if (per > sc) sc = (uint32_t)std::min<uint64_t>((per + 255) & ~255ull, kMergeSliceCapMax);
+  const int co = coop_grid(func, kMergeThreads, merge_smem_bytes(sc));
+  if (co <= 0) return 0;
+  if (g > co) g = co;
+  *slice_cap = sc;
   return g;
 }
 
 int launch_merge(const MergeArgs& args, int32_t cap, cudaStream_t st) {
-  const int G = merge_grid_for((const void*)merge_kernel, cap);
+  uint32_t sc = 0;
+  const int G = merge_grid_for((const void*)merge_kernel, cap, &sc);
   if (G <= 0) return GTK_ECUDA;
   MergeArgs a = args;
+  a.slice_cap = sc;
   void* p[] = {&a};
   ProfScope prof(kProfMerge, st);
-  return coop_launch((const void*)merge_kernel, G, kMergeThreads, p, sizeof(MergeSmem), st);
+  return coop_launch((const void*)merge_kernel, G, kMergeThreads, p, merge_smem_bytes(sc), st);
 }
 
 }  // namespace gtk

@@ -28,7 +28,8 @@ namespace gtk {
 constexpr int kMergeThreads = 512;
 constexpr int kMergeSub = 2048;        // merged slots staged per sub-chunk
 constexpr int kMergeSlotsPerBlock = 512;  // grid sizing target
-constexpr int kMergeSliceCap = 4096;   // slice slots kept in shared memory
+constexpr int kMergeSliceCap = 4096;   // slice slots kept in shared memory (minimum)
+constexpr int kMergeSliceCapMax = 20480;  // ... up to 160 KB of dynamic smem at large k
 constexpr int kMergeMaxSplits = 65;    // sub-chunk boundaries per block (slice <= 128K)
 
 struct MergeCtl {
@@ -82,6 +83,7 @@ struct MergeArgs {
   int upd_scaling;
   uint32_t* tag;
   uint32_t tag_val;
+  uint32_t slice_cap;  // slice slots staged in shared memory (behind MergeSmem)
 };
 
 __device__ __forceinline__ void merge_stamp(const MergeArgs& a, int i) {
@@ -92,15 +94,18 @@ __device__ __forceinline__ void merge_stamp(const MergeArgs& a, int i) {
   }
 }
 
+// dynamic shared memory: MergeSmem, then the slice (slice_cap idx, slice_cap val)
 struct MergeSmem {
   EngineSmem<kMergeThreads> esm;
-  int32_t slice_idx[kMergeSliceCap];
-  float slice_val[kMergeSliceCap];
   int32_t sAi[kMergeSub], sBi[kMergeSub];
   float sAv[kMergeSub], sBv[kMergeSub];
   uint32_t split[kMergeMaxSplits];
   uint32_t s_valid;
 };
+constexpr size_t kMergeSmemFixed = (sizeof(MergeSmem) + 15) & ~size_t(15);
+static inline size_t merge_smem_bytes(uint32_t slice_cap) {
+  return kMergeSmemFixed + (size_t)slice_cap * (sizeof(int32_t) + sizeof(float));
+}
 
 // number of A elements among the first d merged elements (A before B on ties);
 // executed by one full warp, result returned to every lane.
@@ -228,7 +233,9 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   uint32_t d0, d1;
   slice_of(N, G, blk, d0, d1);
   const uint32_t L = d1 - d0;
-  const bool in_smem = L <= (uint32_t)kMergeSliceCap;
+  const bool in_smem = L <= a.slice_cap;
+  int32_t* const slice_idx = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(&S) + kMergeSmemFixed);
+  float* const slice_val = reinterpret_cast<float*>(slice_idx + a.slice_cap);
   const uint32_t nsub = (L + kMergeSub - 1) / kMergeSub;
   // all sub-chunk boundaries of the slice, one warp each, in parallel
   merge_stamp(a, 0);
@@ -288,8 +295,8 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
       const uint32_t slot = sub + t + r;
       const bool valid = v != 0.0f;
       if (in_smem) {
-        S.slice_idx[slot - d0] = valid ? x : -1;
-        S.slice_val[slot - d0] = v;
+        slice_idx[slot - d0] = valid ? x : -1;
+        slice_val[slot - d0] = v;
       } else {
         a.u_idx[slot] = valid ? x : -1;
         a.u_val[slot] = v;
@@ -308,8 +315,8 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
       const uint32_t slot = sub + t + r;
       const bool valid = !dup && v != 0.0f;
       if (in_smem) {
-        S.slice_idx[slot - d0] = valid ? x : -1;
-        S.slice_val[slot - d0] = v;
+        slice_idx[slot - d0] = valid ? x : -1;
+        slice_val[slot - d0] = v;
       } else {
         a.u_idx[slot] = valid ? x : -1;
         a.u_val[slot] = v;
@@ -341,7 +348,7 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   }
   merge_stamp(a, 3);  // after the histogram barrier
   const bool keep_all = n_valid <= a.k;
-  const SliceSrc src{S.slice_idx, S.slice_val, a.u_idx, a.u_val, d0, in_smem, true};
+  const SliceSrc src{slice_idx, slice_val, a.u_idx, a.u_val, d0, in_smem, true};
   const Sink out{a.o_idx, a.o_val, a.d_no, nullptr, true, a.trace ? a.trace + 5 : nullptr,
                  keep_all ? nullptr : rec, rec_level, rec_tau, rec_tau2, 3u,
                  a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling, a.tag, a.tag_val};

@@ -45,7 +45,8 @@ constexpr int kSampleChunk = kSampleThreads;                // 1024 elements per
 constexpr int kSampleTop = 32;                               // top keys kept per sample block
 constexpr int kSampleMaxChunks = 1024;                       // sample blocks (window holds 32K keys)
 constexpr int kFinishThreads = 512;
-constexpr int kSliceCap = 3072;                              // candidates staged per finish block
+constexpr int kSliceCap = 3072;                              // candidates staged per finish block (minimum)
+constexpr int kSliceCapMax = 20480;                          // ... up to 160 KB of dynamic smem at large k
 constexpr uint32_t kOvfBit = 0x80000000u;
 constexpr uint32_t kMinWindowLevel = 2;  // carried-window margin: from k (1 + 2^2 / 2) = 3k candidates
 constexpr uint32_t kMaxWindowLevel = 4;  // ... up to k (1 + 2^4 / 2) = 9k
@@ -433,7 +434,7 @@ __device__ __forceinline__ float pick(const float (&v)[kMainVec][4], int b) {
 // compaction into the tile's slot row (or the overflow region for a dense
 // tile) and the window histogram.  One block barrier (three for a dense tile);
 // the shared scratch alternates with `par` between a block's tiles.
-__device__ __forceinline__ void main_tile(const MainArgs& a, uint32_t tile, const float (&v)[kMainVec][4], bool full,
+__device__ __forceinline__ bool main_tile(const MainArgs& a, uint32_t tile, const float (&v)[kMainVec][4], bool full,
                                           uint32_t lo, uint32_t shift, int par, uint32_t (&s_wt)[2][16],
                                           int32_t* (&s_didx)[2], float* (&s_dval)[2], uint32_t* s_hist) {
   const uint64_t tbase = (uint64_t)tile * kTile;
@@ -494,7 +495,7 @@ __device__ __forceinline__ void main_tile(const MainArgs& a, uint32_t tile, cons
                                    T0 + T1 + T2 + (before23 >> 16) + (e23 >> 16)};
   if (total == 0) {
     if (threadIdx.x == 0) a.tile_info[tile] = 0u;
-    return;
+    return false;
   }
   if (threadIdx.x == 0) atomicAdd(a.group_cnt + tile / a.tiles_per_group, total);
   int32_t* didx = a.slot_idx + (size_t)tile * a.slots;
@@ -533,20 +534,16 @@ __device__ __forceinline__ void main_tile(const MainArgs& a, uint32_t tile, cons
     if (hist_direct) atomicAdd(a.whist + min((uint32_t)kBins, (key_of(x) - lo) >> shift), 1u);
   }
   if (!hist_direct) {
-    // dense tile (a wide window, e.g. while a residual builds up): a shared
-    // histogram first, so a hot bin costs one global atomic per tile
-    for (int b = threadIdx.x; b < kHistLen; b += kMainThreads) s_hist[b] = 0u;
-    __syncthreads();
+    // dense tile (large k, or a wide window while a residual builds up): the
+    // block's shared histogram (cleared at block start, flushed once at block
+    // end), so a hot bin costs one global atomic per block
     for (uint32_t f = flags; f; f &= f - 1) {
       const int b = __ffs(f) - 1;
       atomicAdd(&s_hist[min((uint32_t)kBins, (key_of(pick(v, b)) - lo) >> shift)], 1u);
     }
-    __syncthreads();
-    for (int b = threadIdx.x; b < kHistLen; b += kMainThreads) {
-      const uint32_t c = s_hist[b];
-      if (c) atomicAdd(a.whist + b, c);
-    }
+    return true;
   }
+  return false;
 }
 
 
@@ -573,12 +570,16 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
       }
     }
   }
+  // the dense-tile histogram, cleared while the loads are in flight (the
+  // first tile's barrier orders it before any use)
+  for (int b = threadIdx.x; b < kHistLen; b += kMainThreads) s_hist[b] = 0u;
   // everything below consumes the sample kernel's window (and may write
   // res_out = res in place, which the sample kernel reads): wait for it --
   // the loads above are already in flight (programmatic dependent launch)
   pdl_wait();
   const uint32_t lo = __ldcg(&a.ctl->lo);
   const uint32_t shift = __ldcg(&a.ctl->shift);
+  bool any_dense = false;
 #pragma unroll
   for (int u = 0; u < kMainTilesPerBlock; ++u) {
     const uint32_t tile = t0 + u;
@@ -617,7 +618,14 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
           v[q][j] = x;
         }
     }
-    main_tile(a, tile, v, full, lo, shift, u & 1, s_wt, s_didx, s_dval, s_hist);
+    any_dense |= main_tile(a, tile, v, full, lo, shift, u & 1, s_wt, s_didx, s_dval, s_hist);
+  }
+  if (any_dense) {  // block-uniform
+    __syncthreads();
+    for (int b = threadIdx.x; b < kHistLen; b += kMainThreads) {
+      const uint32_t c = s_hist[b];
+      if (c) atomicAdd(a.whist + b, c);
+    }
   }
 }
 
@@ -639,7 +647,7 @@ struct FinishArgs {
   const float* slot_val;
   const int32_t* ovf_idx;
   const float* ovf_val;
-  int32_t* ord_idx;  // global staging for a block whose slice exceeds kSliceCap
+  int32_t* ord_idx;  // global staging for a block whose slice exceeds slice_cap
   float* ord_val;
   int32_t* sel_idx;
   float* sel_val;
@@ -653,6 +661,7 @@ struct FinishArgs {
   float upd_lr;
   float upd_Pf;
   int upd_scaling;
+  uint32_t slice_cap;  // candidates per block staged in (dynamic) shared memory
 };
 
 __device__ __forceinline__ void finish_stamp(const FinishArgs& a, int i) {
@@ -663,10 +672,11 @@ __device__ __forceinline__ void finish_stamp(const FinishArgs& a, int i) {
   }
 }
 
-__global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArgs a) {
+__global__ void __launch_bounds__(kFinishThreads, 1) select_finish_kernel(FinishArgs a) {
   __shared__ EngineSmem<kFinishThreads> sm;
-  __shared__ int32_t s_idx[kSliceCap];
-  __shared__ float s_val[kSliceCap];
+  extern __shared__ __align__(16) unsigned char s_dyn[];  // the candidate slice: slice_cap (idx, val)
+  int32_t* s_idx = reinterpret_cast<int32_t*>(s_dyn);
+  float* s_val = reinterpret_cast<float*>(s_dyn + sizeof(int32_t) * a.slice_cap);
   const unsigned G = gridDim.x, blk = blockIdx.x;
   pdl_wait();  // launched programmatically behind the main pass
   pdl_launch_dependents();
@@ -715,7 +725,7 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
   finish_stamp(a, 1);
   if (!overflow && C >= a.k && C <= a.ord_cap) {
     // copy my tiles' candidates into my slice (smem if it fits)
-    const bool in_smem = own <= (uint32_t)kSliceCap;
+    const bool in_smem = own <= a.slice_cap;
     int32_t* di = in_smem ? s_idx : a.ord_idx + before;
     float* dv = in_smem ? s_val : a.ord_val + before;
     static_assert(kGatherCap >= kFinishThreads, "copy scratch");
@@ -733,10 +743,30 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
       s_ovf[threadIdx.x] = (info & kOvfBit) ? __ldcg(a.tile_ovf + t) : 0u;
       __syncthreads();
       const uint32_t nt = min((uint32_t)kFinishThreads, t1 - tb);
-      // entry-indexed gather: entry j of this chunk lives in tile q with
-      // s_dst[q] - run <= j < s_dst[q+1] - run (binary search in smem)
+      // many candidates per tile (large k): one warp per tile, lanes over its
+      // contiguous slot row (coalesced, no search); otherwise entry-indexed:
+      // entry j of this chunk lives in tile q with s_dst[q] - run <= j <
+      // s_dst[q+1] - run (binary search in smem)
+      const bool per_tile = tot >= 8u * nt;
+      if (per_tile) {
+        for (uint32_t q = warp_id(); q < nt; q += kFinishThreads / 32) {
+          const uint32_t inf = s_cnt[q];
+          if (inf & kOvfBit) continue;  // dense tiles are copied below
+          const uint32_t cnt = inf, dst = s_dst[q];
+          const size_t sb = (size_t)(tb + q) * a.slots;
+          for (uint32_t e = lane_id(); e < cnt; e += 32) {
+            if (in_smem) {
+              cp_async4(di + dst + e, a.slot_idx + sb + e);
+              cp_async4(dv + dst + e, a.slot_val + sb + e);
+            } else {
+              di[dst + e] = __ldcg(a.slot_idx + sb + e);
+              dv[dst + e] = __ldcg(a.slot_val + sb + e);
+            }
+          }
+        }
+      }
 #pragma unroll 4
-      for (uint32_t j = threadIdx.x; j < tot; j += kFinishThreads) {
+      for (uint32_t j = per_tile ? tot : threadIdx.x; j < tot; j += kFinishThreads) {
         const uint32_t jj = run + j;
         uint32_t lo = 0, hi = nt;  // last q with s_dst[q] <= jj
         while (hi - lo > 1) {
@@ -773,6 +803,12 @@ __global__ void __launch_bounds__(kFinishThreads) select_finish_kernel(FinishArg
       __syncthreads();
     }
     finish_stamp(a, 2);
+    if (a.trace && blk == 0 && threadIdx.x == 0) {  // diagnostics: slice sizes
+      a.trace[10] = own;
+      a.trace[11] = a.slice_cap;
+      a.trace[12] = C;
+      a.trace[13] = G;
+    }
     cp_async_commit();    // group: the slice
     cp_async_wait<1>();   // the histogram has landed; the slice may still be in flight
     __syncthreads();
@@ -897,15 +933,26 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
   }
   // the finish grid (cooperative): fixed before the main pass, which counts
   // the candidates of each finish block's tile range
-  int G = coop_grid((const void*)select_finish_kernel, kFinishThreads, 0);
+  // slice capacity: a carried window admits ~3k candidates (9k at the widest
+  // margin); stage ~4k / G per block in shared memory, at least kSliceCap
+  const int nsm = num_sms();
+  if (nsm <= 0) return GTK_ECUDA;
+  uint32_t slice_cap = kSliceCap;
+  {
+    const uint64_t per = ((uint64_t)k * 4 + nsm - 1) / nsm;
+    if (per > slice_cap) slice_cap = (uint32_t)std::min<uint64_t>((per + 1023) & ~1023ull, kSliceCapMax);
+  }
+  const size_t fin_smem = (size_t)slice_cap * (sizeof(int32_t) + sizeof(float));
+  if (!ensure_dyn_smem((const void*)select_finish_kernel, (size_t)kSliceCapMax * 8)) return GTK_ECUDA;
+  int G = coop_grid((const void*)select_finish_kernel, kFinishThreads, fin_smem);
   if (G <= 0) return GTK_ECUDA;
   {
     int want = (int)((L.ntiles + 39) / 40);  // ~40 tiles per block (measured best of 22..150)
-    if ((int64_t)want * kSliceCap < (int64_t)k * 2) want = (int)(((int64_t)k * 2 + kSliceCap - 1) / kSliceCap);
+    if ((int64_t)want * slice_cap < (int64_t)k * 2) want = (int)(((int64_t)k * 2 + slice_cap - 1) / slice_cap);
     if (want < 8) want = 8;
     if ((uint32_t)want > L.ntiles) want = (int)L.ntiles;
     if (G > want) G = want;
-    if (G > num_sms()) G = num_sms();
+    if (G > nsm) G = nsm;
     if (G > kMaxBlocks) G = kMaxBlocks;
   }
   const uint32_t tiles_per_group = (L.ntiles + G - 1) / G;
@@ -968,9 +1015,10 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
                 upd.w,
                 upd.lr,
                 upd.Pf,
-                upd.scaling};
+                upd.scaling,
+                slice_cap};
 
 
   void* args[] = {&fa};
-  return coop_launch((const void*)select_finish_kernel, G, kFinishThreads, args, 0, st, true);
+  return coop_launch((const void*)select_finish_kernel, G, kFinishThreads, args, fin_smem, st, true);
 }

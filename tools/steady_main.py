@@ -7,8 +7,9 @@ import paper_1901_04359_b200 as gk
 from paper_1901_04359_b200 import optimizer as opt
 from paper_1901_04359_b200.pipeline import GTopKPipeline
 d = torch.device("cuda", 0)
-m, k = 25_600_000, 25_600
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1500
+m = int(sys.argv[2]) if len(sys.argv) > 2 else 25_600_000
+k = int(sys.argv[3]) if len(sys.argv) > 3 else 25_600
 gen = torch.Generator(device=d).manual_seed(5)
 grads = [torch.randn(m, device=d, generator=gen) for _ in range(2)]
 ep = gk.create_local_cluster(1)[0]

@@ -8,14 +8,16 @@ from paper_1901_04359_b200 import optimizer as opt, _lib
 from paper_1901_04359_b200.pipeline import GTopKPipeline
 lib = _lib.load()
 d = torch.device("cuda", 0)
-m, k = 25_600_000, 25_600
+m = int(sys.argv[1]) if len(sys.argv) > 1 else 25_600_000
+k = int(sys.argv[2]) if len(sys.argv) > 2 else 25_600
+npre = int(sys.argv[3]) if len(sys.argv) > 3 else 1500
 gen = torch.Generator(device=d).manual_seed(5)
 grads = [torch.randn(m, device=d, generator=gen) for _ in range(2)]
 ep = gk.create_local_cluster(1)[0]
 st = opt.make_state(torch.zeros(m, device=d), lr=0.01)
 pipe = GTopKPipeline(ep, st, k, grads)
 pipe.capture()
-pipe.run(1500)
+pipe.run(npre)
 torch.cuda.synchronize()
 tr = torch.zeros(128, dtype=torch.int64, device=d)
 lib.gtk_exchange_set_trace(ctypes.c_void_p(tr.data_ptr()))
@@ -26,5 +28,5 @@ for rep in range(4):
     t = tr.cpu().tolist()
     f = t[48:55]
     print(f"finish rep{rep}: " + " ".join(f"{n}={(v - f[0]) / 1e3:.1f}" for n, v in zip(names, f) if v)
-          + f" | round-0 in_bin={t[55]}", flush=True)
+          + f" | round-0 in_bin={t[55]} w_scanned={(t[56]-f[0])/1e3:.1f} w_put={(t[57]-f[0])/1e3:.1f} own={t[58]} cap={t[59]} C={t[60]} G={t[61]}", flush=True)
 lib.gtk_exchange_set_trace(None)
