@@ -109,6 +109,15 @@ int gtk_select_update(const float* res_in, const float* grad, float* res_out, in
                       size_t ws_bytes, int32_t flags, uint32_t* d_window, float* w, float lr, int32_t P,
                       int32_t scaling, void* stream);
 
+/* Measurement only (bench.py's roofline): `reps` back-to-back launches of
+ * K1's HBM pass alone (res_out = res_in + grad, candidate compaction and the
+ * window histogram) against the key window the last select on this
+ * workspace published, then the workspace's histogram and counters are
+ * cleared (cudaMemsetAsync), so the next select starts clean.  Must follow a
+ * completed select of the same (m, k) on `ws`; sel lists are not written. */
+int gtk_select_main_pass(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
+                         void* ws, size_t ws_bytes, int32_t reps, void* stream);
+
 /* ------------------------------------------------------------------------
  * K2: the sparse top-k merge operator ⊤.
  * Replaces sparse.py:157-195 (top_op(a, b, k)); a = received, b = own

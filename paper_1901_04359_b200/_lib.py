@@ -42,6 +42,7 @@ EXPORTS = (
     "gtk_select",
     "gtk_select_windowed",
     "gtk_select_update",
+    "gtk_select_main_pass",
     "gtk_merge_workspace_bytes",
     "gtk_top_op",
     "gtk_update_workspace_bytes",
@@ -83,6 +84,7 @@ _SIGS = {
     "gtk_select": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _I32, _P], _I32),
     "gtk_select_windowed": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _I32, _P, _P], _I32),
     "gtk_select_update": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _I32, _P, _P, _F, _I32, _I32, _P], _I32),
+    "gtk_select_main_pass": ([_P, _P, _P, _I64, _I32, _P, _SZ, _I32, _P], _I32),
     "gtk_merge_workspace_bytes": ([_I32, _I32, ctypes.POINTER(_SZ)], _I32),
     "gtk_top_op": ([_P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _SZ, _P], _I32),
     "gtk_update_workspace_bytes": ([_I64, ctypes.POINTER(_SZ)], _I32),

@@ -270,16 +270,42 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
       const uint32_t ln = min((uint32_t)__ldcg(a.d_in_n), (uint32_t)a.k);
       const uint32_t ep32 = (uint32_t)epoch;
       const float Pf = (float)a.P;
+      // kK3Batch entries per thread per round: every list load, then every
+      // dependent w / tag / residual load, then the stores -- one memory round
+      // trip per phase instead of three per entry (large k)
+      constexpr int kK3Batch = 4;
       const uint32_t stride = G * kMergeThreads;
-      for (uint32_t e = blk * kMergeThreads + threadIdx.x; e < max(gn, ln); e += stride) {
-        if (e < gn) {
-          const int32_t i = __ldcg(a.acc_idx + e);
-          const float u = scale_u(__ldcg(a.acc_val + e), Pf, a.upd_scaling);
-          a.upd_w[i] = __fsub_rn(a.upd_w[i], __fmul_rn(a.upd_lr, u));
+      const uint32_t nmax = max(gn, ln);
+      for (uint32_t base = blk * kMergeThreads + threadIdx.x; base < nmax; base += kK3Batch * stride) {
+        int32_t gi[kK3Batch], li[kK3Batch];
+        float gv[kK3Batch], lv[kK3Batch], wv[kK3Batch], rv[kK3Batch];
+        uint32_t tg[kK3Batch];
+#pragma unroll
+        for (int u = 0; u < kK3Batch; ++u) {
+          const uint32_t e = base + u * stride;
+          if (e < gn) {
+            gi[u] = __ldcg(a.acc_idx + e);
+            gv[u] = __ldcg(a.acc_val + e);
+          }
+          if (e < ln) {
+            li[u] = __ldcg(a.in_idx + e);
+            lv[u] = __ldcg(a.in_val + e);
+          }
         }
-        if (e < ln) {
-          const int32_t i = __ldcg(a.in_idx + e);
-          if (__ldcg(a.upd_tags + i) != ep32) a.upd_res[i] = __fadd_rn(a.upd_res[i], __ldcg(a.in_val + e));
+#pragma unroll
+        for (int u = 0; u < kK3Batch; ++u) {
+          const uint32_t e = base + u * stride;
+          if (e < gn) wv[u] = a.upd_w[gi[u]];
+          if (e < ln) {
+            tg[u] = __ldcg(a.upd_tags + li[u]);
+            rv[u] = a.upd_res[li[u]];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kK3Batch; ++u) {
+          const uint32_t e = base + u * stride;
+          if (e < gn) a.upd_w[gi[u]] = __fsub_rn(wv[u], __fmul_rn(a.upd_lr, scale_u(gv[u], Pf, a.upd_scaling)));
+          if (e < ln && tg[u] != ep32) a.upd_res[li[u]] = __fadd_rn(rv[u], lv[u]);
         }
       }
     }

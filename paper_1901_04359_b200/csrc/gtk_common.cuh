@@ -111,7 +111,8 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // ---- grid-wide barrier for cooperative launches ---------------------------
 // Generation barrier; count returns to 0 after every use so the workspace
 // needs a single zero-initialisation.
-struct GridBarrier {
+// one 64-bit word: arrival count (low half) and generation (high half)
+struct __align__(8) GridBarrier {
   uint32_t count;
   uint32_t gen;
 };
@@ -129,22 +130,36 @@ __device__ __forceinline__ uint32_t atom_inc_acq_rel_gpu(uint32_t* p, uint32_t l
   return old;
 }
 
-// Thread 0 arrives with an acq_rel atomic (cumulative over the block's writes
-// through the preceding bar.sync), the last arriver resets the count and
-// releases the generation, the others acquire it; bar.sync then extends the
-// ordering to the whole block.  Cross-block data is read with ld.global.cg.
+__device__ __forceinline__ uint64_t atom_add_acq_rel_gpu_u64(uint64_t* p, uint64_t v) {
+  uint64_t old;
+  asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ uint64_t ld_acquire_gpu_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Thread 0 arrives with one acq_rel atomic on the {count, gen} word
+// (cumulative over the block's writes through the preceding bar.sync): the
+// returned word carries both the generation and the arrival rank, so arrival
+// is a single round trip.  The last arriver resets the count and advances the
+// generation with one more release add; the others acquire the new
+// generation; bar.sync then extends the ordering to the whole block.
+// Cross-block data is read with ld.global.cg.
 __device__ __forceinline__ void grid_sync(GridBarrier* b, unsigned nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t g = ld_acquire_gpu(&b->gen);
-    const uint32_t prev = atom_add_acq_rel_gpu(&b->count, 1u);
-    if (prev == nblocks - 1) {
-      b->count = 0;  // ordered before the release below
-      st_release_gpu(&b->gen, g + 1);
+    uint64_t* word = reinterpret_cast<uint64_t*>(b);
+    const uint64_t old = atom_add_acq_rel_gpu_u64(word, 1ull);
+    const uint32_t g = (uint32_t)(old >> 32);
+    if ((uint32_t)old == nblocks - 1) {
+      atom_add_acq_rel_gpu_u64(word, (1ull << 32) - nblocks);  // count -> 0, gen -> g + 1
     } else {
       uint32_t spins = 0;
-      while (ld_acquire_gpu(&b->gen) == g)
-        if (++spins > 32) __nanosleep(20);
+      while ((uint32_t)(ld_acquire_gpu_u64(word) >> 32) == g)
+        if (++spins > 64) __nanosleep(20);
     }
   }
   __syncthreads();

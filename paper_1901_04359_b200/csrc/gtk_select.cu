@@ -1022,3 +1022,35 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
   void* args[] = {&fa};
   return coop_launch((const void*)select_finish_kernel, G, kFinishThreads, args, fin_smem, st, true);
 }
+
+extern "C" int gtk_select_main_pass(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
+                                    void* ws, size_t ws_bytes, int32_t reps, void* stream) {
+  if (!grad || !res_out || !ws || reps < 1) return GTK_EINVAL;
+  if (m < 1 || m >= (int64_t(1) << 31) || k < 1 || k > m) return GTK_EINVAL;
+  const SelectLayout L = select_layout(m, k);
+  if (ws_bytes < L.total) return GTK_ENOMEM;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* base = (char*)ws;
+  SelectCtl* ctl = (SelectCtl*)(base + L.ctl);
+  EngineWS* ews = (EngineWS*)(base + L.engine);
+  uint32_t* group_cnt = (uint32_t*)(base + L.group_cnt);
+  const int nsm = num_sms();
+  if (nsm <= 0) return GTK_ECUDA;
+  // the finish grouping of select_impl (only the per-group counts depend on it)
+  const uint32_t tiles_per_group = (L.ntiles + nsm - 1) / nsm;
+  MainArgs ma{res_in, grad, res_out, (uint32_t)m, L.slots, L.ovf_cap, ctl,
+              (uint32_t*)(base + L.tile_info), (uint32_t*)(base + L.tile_ovf), (int32_t*)(base + L.slot_idx),
+              (float*)(base + L.slot_val), (int32_t*)(base + L.ovf_idx), (float*)(base + L.ovf_val),
+              ews->hist[0], group_cnt, tiles_per_group};
+  const uint32_t gmain = (L.ntiles + kMainTilesPerBlock - 1) / kMainTilesPerBlock;
+  for (int r = 0; r < reps; ++r) {
+    select_main_kernel<<<gmain, kMainThreads, 0, st>>>(ma);
+    GTK_CHECK_LAUNCH();
+  }
+  // the repeated passes accumulated histogram / counter state: clear it
+  GTK_CUDA(cudaMemsetAsync(ews->hist[0], 0, sizeof(uint32_t) * kHistStride, st));
+  GTK_CUDA(cudaMemsetAsync(group_cnt, 0, sizeof(uint32_t) * kMaxBlocks, st));
+  GTK_CUDA(cudaMemsetAsync(&ctl->ovf_cursor, 0, sizeof(ctl->ovf_cursor), st));
+  GTK_CUDA(cudaMemsetAsync(&ctl->overflow, 0, sizeof(ctl->overflow), st));
+  return GTK_OK;
+}

@@ -166,6 +166,30 @@ def select(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, out: Devic
     )
 
 
+def time_main_pass(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, reps: int) -> float:
+    """Measurement only: ms per launch of K1's HBM pass against the window the
+    last select of this (m, k) published (gtk_select_main_pass): CUDA events
+    on the library's stream around `reps` and `2 reps` back-to-back launches;
+    the difference is exactly `reps` launches (the call's trailing workspace
+    clear cancels).  res_out is overwritten with res_in + grad."""
+    m = grad.numel()
+    dev = grad.device
+    ws = select_workspace(m, k, dev)
+    st = torch.cuda.current_stream(dev)
+
+    def timed(n):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        _lib.call("gtk_select_main_pass", P(res_in), P(grad), P(res_out), m, k, P(ws),
+                  ctypes.c_size_t(ws.numel()), n, stream_of(dev))
+        e1.record(st)
+        e1.synchronize()
+        return e0.elapsed_time(e1)
+
+    timed(2)  # warm
+    return (timed(2 * reps) - timed(reps)) / reps
+
+
 def sparse_update_fusable(lr: float, momentum: float) -> bool:
     """K3's sparse-exact form applies (finite lr with the sign bit clear, no
     momentum): the update can ride on the select at P = 1."""

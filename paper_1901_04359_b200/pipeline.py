@@ -137,6 +137,14 @@ class GTopKPipeline:
             print("profile (ms per launch):", out, flush=True)
         return out
 
+    def time_main_pass(self, reps: int = 20) -> float:
+        """ms per launch of K1's HBM pass on this pipeline's current residual
+        and gradient, steady-state window (device.time_main_pass); the scratch
+        residual buffer (the next step's output) is overwritten."""
+        torch.cuda.synchronize(self.dev)
+        p = self.t % 2
+        return _dev.time_main_pass(self.res[p], self.grads[p % len(self.grads)], self.res[1 - p], self.k, reps)
+
     def profile_graph(self, steps: int = 20) -> dict:
         """Per-stage device time (ms) from CUDA event nodes captured around
         each launch inside a step graph, replayed `steps` times and read back

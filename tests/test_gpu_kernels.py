@@ -352,3 +352,37 @@ def test_select_update_matches_select_then_k3(dev, scaling):
     dev.select_update(r, g2, rb, k, lb, st, win, wc, float(np.float32(lr)), 1, scaling)
     assert int(st.item()) & 0x1
     assert torch.equal(wc.view(torch.int32), w0.view(torch.int32))
+
+
+def test_main_pass_measurement_leaves_workspace_clean(dev):
+    """gtk_select_main_pass (bench.py's roofline timing) between two windowed
+    selects: res_out = res + g, and the next select is still bit-exact with no
+    fallback (the accumulated histogram / counters were cleared)."""
+    import torch
+
+    from oracle import gtopk_oracle as orc
+
+    d = torch.device("cuda", 0)
+    rng = np.random.default_rng(8)
+    m, k = 2_000_000, 2000
+    win = dev.new_window(d)
+    lst = dev.DeviceList(m, k, d)
+    st = torch.zeros(1, dtype=torch.int32, device=d)
+    res = np.zeros(m, F32)
+    for step in range(4):
+        g = rng.standard_normal(m).astype(F32)
+        gd, rd = torch.from_numpy(g).to(d), torch.from_numpy(res).to(d)
+        out = torch.empty_like(gd)
+        if step >= 2:
+            ms = dev.time_main_pass(rd, gd, out, k, reps=3)
+            assert ms > 0
+            assert np.array_equal(out.cpu().numpy().view(np.uint32), (res + g).view(np.uint32))
+        st.zero_()
+        dev.select(rd, gd, out, k, lst, st, window=win)
+        wi, wv, wres = orc.top_k_select(res + g, k)
+        i, v = lst.to_host()
+        assert np.array_equal(i, wi) and np.array_equal(v.view(np.uint32), wv.view(np.uint32)), step
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), wres.view(np.uint32)), step
+        if step >= 1:
+            assert int(st.item()) & 0x2 == 0, step
+        res = wres
