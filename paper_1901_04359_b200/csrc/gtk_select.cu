@@ -419,6 +419,7 @@ struct MainArgs {
   uint32_t* whist;      // engine round-0 histogram [kHistLen]
   uint32_t* group_cnt;  // candidates per finish block (tiles_per_group tiles each)
   uint32_t tiles_per_group;
+  uint32_t n2;  // blocks [0, n2) take two tiles, the rest one (the last wave is short)
 };
 
 // v[b >> 2][b & 3] without a dynamically indexed (local-memory) array
@@ -440,18 +441,28 @@ __device__ __forceinline__ bool main_tile(const MainArgs& a, uint32_t tile, cons
   const uint64_t tbase = (uint64_t)tile * kTile;
   const unsigned lane = lane_id(), w = warp_id();
   // candidate flags (bit q*4+j) and the non-finite check
-  uint32_t flags = 0;
-  bool nonfinite = false;
+  // fast path: the largest of my 16 keys decides whether any element can be
+  // a candidate or non-finite (NaN/inf keys are the largest); elements past m
+  // hold +0 (key 0) and are screened by the slow path whenever lo == 0
+  uint32_t kmax = 0;
 #pragma unroll
   for (int q = 0; q < kMainVec; ++q)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint64_t e = tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4 + j;
-      const uint32_t key = key_of(v[q][j]);
-      const bool in = full || e < a.m;
-      nonfinite |= in && key >= kInfKey;
-      if (in && key >= lo) flags |= 1u << (q * 4 + j);
-    }
+    for (int j = 0; j < 4; ++j) kmax = max(kmax, key_of(v[q][j]));
+  uint32_t flags = 0;
+  bool nonfinite = false;
+  if (kmax >= lo || kmax >= kInfKey) {
+#pragma unroll
+    for (int q = 0; q < kMainVec; ++q)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t e = tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4 + j;
+        const uint32_t key = key_of(v[q][j]);
+        const bool in = full || e < a.m;
+        nonfinite |= in && key >= kInfKey;
+        if (in && key >= lo) flags |= 1u << (q * 4 + j);
+      }
+  }
   if (__any_sync(kFull, nonfinite) && lane == 0) a.ctl->nonfinite = 1u;
 
   // index-ordered in-tile offsets, order (q, warp, lane, j): per-lane counts of
@@ -556,12 +567,17 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
 
   // all of this block's tiles are loaded before any is processed: more bytes
   // in flight per resident block
-  const uint32_t t0 = blockIdx.x * kMainTilesPerBlock;
+  // blocks [0, n2) take two tiles; the last ~one wave of blocks takes one
+  // tile each, so the grid's drain (blocks running alone on a few SMs) is short
+  static_assert(kMainTilesPerBlock == 2, "two-tile / one-tile schedule");
+  const uint32_t blk = blockIdx.x;
+  const uint32_t t0 = blk < a.n2 ? 2 * blk : a.n2 + blk;
+  const uint32_t ntile = blk < a.n2 ? 2u : 1u;
   float4 gv[kMainTilesPerBlock][kMainVec], rv[kMainTilesPerBlock][kMainVec];
 #pragma unroll
   for (int u = 0; u < kMainTilesPerBlock; ++u) {
     const uint64_t tbase = (uint64_t)(t0 + u) * kTile;
-    if (tbase + kTile <= a.m) {
+    if ((uint32_t)u < ntile && tbase + kTile <= a.m) {
 #pragma unroll
       for (int q = 0; q < kMainVec; ++q) {
         const uint64_t e = tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4;
@@ -584,7 +600,7 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
   for (int u = 0; u < kMainTilesPerBlock; ++u) {
     const uint32_t tile = t0 + u;
     const uint64_t tbase = (uint64_t)tile * kTile;
-    if (tbase >= a.m) break;
+    if ((uint32_t)u >= ntile || tbase >= a.m) break;
     float v[kMainVec][4];
     const bool full = tbase + kTile <= a.m;
     if (full) {
@@ -849,6 +865,18 @@ __global__ void __launch_bounds__(kFinishThreads, 1) select_finish_kernel(Finish
 
 using namespace gtk;
 
+// main-pass grid: two tiles per block, except that about one wave of resident
+// blocks at the end of the grid takes one tile each (a shorter drain)
+static uint32_t main_grid(uint32_t ntiles, uint32_t* n2) {
+  const int slots = coop_grid((const void*)select_main_kernel, kMainThreads, 0);  // resident blocks, all SMs
+  if (slots <= 0) return 0;
+  uint32_t n1 = std::min<uint32_t>(ntiles, (uint32_t)slots);
+  uint32_t two = (ntiles - n1) / 2;
+  n1 = ntiles - 2 * two;
+  *n2 = two;
+  return two + n1;
+}
+
 extern "C" int gtk_select_workspace_bytes(int64_t m, int32_t k, size_t* bytes) {
   if (!bytes || m < 1 || m >= (int64_t(1) << 31) || k < 1 || k > m) return GTK_EINVAL;
   *bytes = select_layout(m, k).total;
@@ -983,7 +1011,8 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
               tiles_per_group};
   {
     ProfScope prof_main(kProfSelectMain, st);
-    const uint32_t gmain = (L.ntiles + kMainTilesPerBlock - 1) / kMainTilesPerBlock;
+    const uint32_t gmain = main_grid(L.ntiles, &ma.n2);
+    if (gmain == 0) return GTK_ECUDA;
     GTK_CUDA(launch_pdl(select_main_kernel, dim3(gmain), dim3(kMainThreads), 0, st, ma));
     GTK_CHECK_LAUNCH();
   }
@@ -1042,7 +1071,8 @@ extern "C" int gtk_select_main_pass(const float* res_in, const float* grad, floa
               (uint32_t*)(base + L.tile_info), (uint32_t*)(base + L.tile_ovf), (int32_t*)(base + L.slot_idx),
               (float*)(base + L.slot_val), (int32_t*)(base + L.ovf_idx), (float*)(base + L.ovf_val),
               ews->hist[0], group_cnt, tiles_per_group};
-  const uint32_t gmain = (L.ntiles + kMainTilesPerBlock - 1) / kMainTilesPerBlock;
+  const uint32_t gmain = main_grid(L.ntiles, &ma.n2);
+  if (gmain == 0) return GTK_ECUDA;
   for (int r = 0; r < reps; ++r) {
     select_main_kernel<<<gmain, kMainThreads, 0, st>>>(ma);
     GTK_CHECK_LAUNCH();
