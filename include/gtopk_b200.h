@@ -179,8 +179,13 @@ int gtk_dense_sum(const float* const* srcs, int32_t P, int64_t m, float* out, vo
  *  merge, tag}); send_to/recv_from = -1 for none; merge=1 -> acc = ⊤(recv, acc),
  *  merge=0 -> acc = recv (broadcast).
  *  peer_inbox: host array of P device pointers (IPC-mapped) to each rank's
- *  inbox region of gtk_exchange_inbox_bytes(k, nsteps) bytes.
- *  peer_flags: host array of P device pointers to each rank's uint64 flags[nsteps*2].
+ *  inbox region of gtk_exchange_inbox_bytes(k, nsteps) bytes (zeroed once).
+ *  Lists travel as low-latency records: per entry one 16-byte store of two
+ *  64-bit words {idx | tag << 32, val bits | tag << 32}, the slot header
+ *  {count | tag, hint | tag}, tag = the call's epoch; the receiver polls the
+ *  words until they carry its tag (no separate flag or fence).
+ *  peer_flags: host array of P device pointers to each rank's uint64
+ *  flags[nsteps*2] -- unused by the record protocol, kept in the ABI.
  * ------------------------------------------------------------------------ */
 int gtk_exchange_inbox_bytes(int32_t k, int32_t nsteps, size_t* bytes);
 int gtk_exchange_flags_bytes(int32_t nsteps, size_t* bytes);

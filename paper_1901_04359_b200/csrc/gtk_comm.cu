@@ -2,25 +2,31 @@
 // collectives.py:188-219 + binomial_bcast :168-185), fused with the ⊤ merge.
 //
 // One persistent cooperative kernel per rank executes the rank's whole
-// schedule (butterfly for P = 2^n, reduce-tree + binomial broadcast otherwise):
+// schedule (butterfly for P = 2^n, reduce-tree + binomial broadcast otherwise).
+// Lists travel as low-latency (LL) records: every entry is one 16-byte store
+// of two self-validating 64-bit words {idx | tag, val bits | tag} into the
+// partner's IPC-mapped inbox slot (s, epoch & 1), the slot header likewise
+// {count | tag, hint | tag}; tag = the call's epoch.  The receiver polls the
+// words it reads (header, then the entries as the merge reads them) until
+// they carry the call's tag -- no flag, no fence, no release round trip.
 //
-//   step s:  [send]  every block copies its share of the current accumulator
-//                    (count, idx[], val[]) into the partner's inbox slot
-//                    (s, epoch & 1) with plain stores to the IPC-mapped peer
-//                    pointer -- posted writes over NVLink -- then fences at
-//                    system scope and bumps the partner's step flag with a
-//                    red.release.sys.add;
-//            [recv]  thread 0 of every block spins (ld.acquire.sys) on its own
-//                    step flag until it reaches epoch * G (one arrival per
-//                    sender block per call; the counters are monotonic so they
-//                    never need resetting), with a %globaltimer timeout;
+//   step s:  [send]  the list to send was pushed by the previous step's merge
+//                    as it wrote it (fused: the merge's output goes to acc and
+//                    to the next partner at once); otherwise (first step,
+//                    poisoned, broadcast forwarding after a copy) every block
+//                    pushes its share of the current list;
+//            [recv]  every block polls the header (count, k-th key hint;
+//                    count = -1: the sender is poisoned) with a %globaltimer
+//                    timeout, then
 //            [merge] acc = ⊤(inbox, acc) with the same device merge as K2
-//                    (received-then-own, collectives.py:214), or acc = inbox
-//                    for a broadcast step.
+//                    (received-then-own, collectives.py:214), reading the
+//                    inbox records as they arrive, or acc = inbox for a
+//                    broadcast step.
 //
-// Inbox slots are double-buffered by call parity; every rank receives the
-// final list causally after all merges of the call, so a slot is never
-// overwritten while its reader is still merging.
+// Inbox slots are double-buffered by call parity; a rank can only overwrite a
+// slot of its partner after that partner finished the previous call that used
+// it (every call exchanges in both directions), so records are never
+// overwritten while read, and a stale record carries another call's tag.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -68,30 +74,18 @@ struct ExchangeArgs {
 };
 
 
-// inbox slot: 16 B header {count, hint} | idx[k4] | val[k4], k4 = k rounded up
-// to 4 so both arrays are 16-byte aligned for 128-bit peer stores
-__host__ __device__ inline size_t slot_k4(int32_t k) { return ((size_t)k + 3) & ~size_t(3); }
-__host__ __device__ inline size_t slot_bytes(int32_t k) {
-  return (16 + slot_k4(k) * 8 + 255) & ~size_t(255);
+// inbox slot: 16 B LL header {count | tag, hint | tag} | k LL entries of 16 B
+// {idx | tag, val bits | tag}
+__host__ __device__ inline size_t slot_bytes(int32_t k) { return (16 + (size_t)k * 16 + 255) & ~size_t(255); }
+__device__ __forceinline__ uint64_t* slot_of(char* inbox, int s, uint32_t par, int32_t k) {
+  return reinterpret_cast<uint64_t*>(inbox + ((size_t)s * 2 + par) * slot_bytes(k));
 }
 
-// copy entries [e0, e1) of (src_idx, src_val) to (dst_idx, dst_val) -- 128-bit
-// accesses on the 4-aligned body (all list buffers start 16-byte aligned)
-__device__ __forceinline__ void copy_entries(int32_t* dst_idx, float* dst_val, const int32_t* src_idx,
-                                             const float* src_val, uint32_t e0, uint32_t e1) {
-  const uint32_t a0 = (e0 + 3) & ~3u, a1 = max(a0, e1 & ~3u);
-  for (uint32_t e = e0 + threadIdx.x; e < min(a0, e1); e += blockDim.x) {
-    dst_idx[e] = __ldcg(src_idx + e);
-    dst_val[e] = __ldcg(src_val + e);
-  }
-  for (uint32_t q = a0 / 4 + threadIdx.x; q < a1 / 4; q += blockDim.x) {
-    reinterpret_cast<int4*>(dst_idx)[q] = __ldcg(reinterpret_cast<const int4*>(src_idx) + q);
-    reinterpret_cast<float4*>(dst_val)[q] = __ldcg(reinterpret_cast<const float4*>(src_val) + q);
-  }
-  for (uint32_t e = max(a1, e0) + threadIdx.x; e < e1; e += blockDim.x) {
-    dst_idx[e] = __ldcg(src_idx + e);
-    dst_val[e] = __ldcg(src_val + e);
-  }
+// push entries [e0, e1) of (idx, val) as LL records to body (peer memory)
+__device__ __forceinline__ void push_ll(uint64_t* body, const int32_t* idx, const float* val, uint32_t e0,
+                                        uint32_t e1, uint32_t tag) {
+  for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x)
+    st_ll_pair(body + 2 * (size_t)e, (uint32_t)__ldcg(idx + e), __float_as_uint(__ldcg(val + e)), tag);
 }
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -104,6 +98,7 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   extern __shared__ __align__(16) unsigned char dsm[];
   MergeSmem& S = *reinterpret_cast<MergeSmem*>(dsm);
   __shared__ uint32_t s_n, s_hint;
+  __shared__ bool s_poison;
   const unsigned G = gridDim.x, blk = blockIdx.x;
   pdl_wait();               // launched programmatically behind the select
   pdl_launch_dependents();  // K3 may become resident; it waits for our completion
@@ -129,36 +124,32 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   const float* cur_val = a.in_idx ? a.in_val : a.acc_val;
   const int32_t* cur_n = a.in_idx ? a.d_in_n : a.d_acc_n;
 
+  const uint32_t tag = (uint32_t)epoch;
+  const LLPoll poll{a.timeout_ns > 0 ? globaltimer() + (uint64_t)a.timeout_ns : 0ull, a.d_status, a.d_abort};
+  bool poisoned = self_poison;  // per block, but every block decides it from the same words
+  bool pushed = false;          // this step's send already went out with the previous step's output
   for (int s = 0; s < a.nsteps; ++s) {
     const Step st = a.steps[s];
-    if (st.send_to >= 0) {
-      char* slot = a.inbox[st.send_to] + ((size_t)s * 2 + par) * slot_bytes(a.k);
-      int32_t* r_n = (int32_t*)slot;
-      int32_t* r_idx = (int32_t*)(slot + 16);
-      float* r_val = (float*)(slot + 16 + slot_k4(a.k) * 4);
-      const bool poisoned = self_poison || (__ldcg(a.d_status) & GTK_DEV_PEER_FAILED);
+    // the next step sends the list this step's merge / copy produces: fuse
+    const bool fuse_next = s + 1 < a.nsteps && a.steps[s + 1].send_to >= 0;
+    if (st.send_to >= 0 && !pushed) {
+      uint64_t* slot = slot_of(a.inbox[st.send_to], s, par, a.k);
       uint32_t n = poisoned ? 0u : (uint32_t)__ldcg(cur_n);
       if (n > (uint32_t)a.k) n = a.k;
-      const uint32_t per = ((n + G - 1) / G + 3) & ~3u;  // 4-aligned shares: 128-bit peer stores
+      const uint32_t per = (n + G - 1) / G;
       const uint32_t e0 = min(n, blk * per), e1 = min(n, e0 + per);
-      copy_entries(r_idx, r_val, cur_idx, cur_val, e0, e1);
+      push_ll(slot + 2, cur_idx, cur_val, e0, e1, tag);
       if (blk == 0 && threadIdx.x == 0) {
-        r_n[0] = poisoned ? -1 : (int32_t)n;
-        r_n[1] = poisoned ? 0 : __ldcg(cur_n + 1);  // k-th key hint travels with the list
+        // the k-th key hint travels with the list; count -1 = poisoned
+        st_ll_pair(slot, poisoned ? 0xFFFFFFFFu : n, poisoned ? 0u : (uint32_t)__ldcg(cur_n + 1), tag);
         if (a.step_counts) a.step_counts[2 * s] = (int32_t)n;
       }
-      // bar.sync orders every thread's peer stores before thread 0's
-      // system-scope release, which publishes them all (cumulativity)
-      __syncthreads();
-      if (tr) a.trace[96 + s] = (int64_t)globaltimer();
-      if (threadIdx.x == 0) {
-        // (no separate fence.sc.sys: the release add orders the block's peer
-        // stores before the flag by itself -- measured 3-4 us cheaper)
-        red_release_sys_add_u64(a.flags[st.send_to] + s, 1ull);
-        if (tr) a.trace[100 + s] = (int64_t)globaltimer();
-      }
-      if (tr) a.trace[2 + 4 * s] = (int64_t)globaltimer();
+      if (tr) a.trace[100 + s] = (int64_t)globaltimer();
     }
+    if (st.send_to >= 0 && pushed && blk == 0 && threadIdx.x == 0 && a.step_counts)
+      a.step_counts[2 * s] = min(__ldcg(cur_n), a.k);  // the previous merge's output (final after the barrier)
+    pushed = false;
+    if (tr) a.trace[2 + 4 * s] = (int64_t)globaltimer();
     if (st.recv_from >= 0) {
       // everything local the merge needs is loaded before the wait
       uint32_t* wrec = (st.merge && s < kMergeWindowSlots) ? a.windows + 8 * s : nullptr;
@@ -171,42 +162,33 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
         if (n_own > (uint32_t)a.k) n_own = a.k;
         hint_own = self_poison ? 0u : (uint32_t)__ldcg(cur_n + 1);
       }
+      const uint64_t* slot = slot_of(a.inbox[a.rank], s, par, a.k);
       if (threadIdx.x == 0) {
-        const uint64_t t0 = globaltimer();
-        uint32_t spins = 0;
-        while (ld_acquire_sys_u64(a.flags[a.rank] + s) < target) {
-          if (((++spins) & 1023u) == 0) {
-            if (a.d_abort && *a.d_abort) {
-              atomicOr(a.d_status, GTK_DEV_ABORTED);
-              break;
-            }
-            if (a.timeout_ns > 0 && (int64_t)(globaltimer() - t0) > a.timeout_ns) {
-              atomicOr(a.d_status, GTK_DEV_TIMEOUT);
-              break;
-            }
-          }
-          if (spins > 64) __nanosleep(32);
-        }
-        __threadfence();
-      }
-      __syncthreads();
-      if (tr) a.trace[3 + 4 * s] = (int64_t)globaltimer();
-      char* slot = a.inbox[a.rank] + ((size_t)s * 2 + par) * slot_bytes(a.k);
-      const int32_t* in_idx = (const int32_t*)(slot + 16);
-      const float* in_val = (const float*)(slot + 16 + slot_k4(a.k) * 4);
-      if (threadIdx.x == 0) {
-        int32_t n = __ldcg((const int32_t*)slot);
-        if (n < 0 && blk == 0) atomicOr(a.d_status, GTK_DEV_PEER_FAILED);
-        s_n = (uint32_t)(n < 0 ? 0 : (n > a.k ? a.k : n));  // clamp (garbage after a timeout)
-        s_hint = (uint32_t)__ldcg((const int32_t*)slot + 1);
+        uint32_t n, hint;
+        const bool ok = ld_ll_pair(slot, tag, poll, n, hint);
+        const bool peer_poison = ok && n == 0xFFFFFFFFu;
+        if (peer_poison && blk == 0) atomicOr(a.d_status, GTK_DEV_PEER_FAILED);
+        s_n = (!ok || peer_poison) ? 0u : (n > (uint32_t)a.k ? (uint32_t)a.k : n);
+        s_hint = hint;
+        s_poison = !ok || peer_poison;
       }
       __syncthreads();
       const uint32_t n_in = s_n, hint_in = s_hint;
+      poisoned = poisoned || s_poison;
+      if (tr) a.trace[3 + 4 * s] = (int64_t)globaltimer();
       if (blk == 0 && threadIdx.x == 0 && a.step_counts) a.step_counts[2 * s + 1] = (int32_t)n_in;
+      // fused send of this step's output (never for a poisoned rank: the next
+      // push must carry count -1)
+      uint64_t* out_slot = nullptr;
+      if (fuse_next && !poisoned) {
+        out_slot = slot_of(a.inbox[a.steps[s + 1].send_to], s + 1, par, a.k);
+        pushed = true;
+      }
       if (st.merge) {
         MergeArgs m = a.merge;
-        m.a_idx = in_idx;
-        m.a_val = in_val;
+        m.a_ll = slot + 2;
+        m.a_tag = tag;
+        m.poll = poll;
         m.b_idx = cur_idx;
         m.b_val = cur_val;
         m.o_idx = a.acc_idx;
@@ -215,7 +197,12 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
         m.trace = a.trace ? a.trace + 32 + 16 * s : nullptr;
         if (a.upd_w && s == last_recv) {  // the final global list: K3's membership tags
           m.tag = a.upd_tags;
-          m.tag_val = (uint32_t)epoch;
+          m.tag_val = tag;
+        }
+        if (out_slot) {
+          m.ll_body = out_slot + 2;
+          m.ll_head = out_slot;
+          m.ll_tag = tag;
         }
         merge_device(m, n_in, n_own, hint_in, hint_own, G, S, wrec, wv);
       } else {
@@ -223,14 +210,17 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
         const uint32_t e0 = min(n_in, blk * per), e1 = min(n_in, e0 + per);
         const bool k3 = a.upd_w && s == last_recv;  // the broadcast's copy is the final global list
         for (uint32_t e = e0 + threadIdx.x; e < e1; e += kMergeThreads) {
-          const int32_t i = __ldcg(in_idx + e);
-          a.acc_idx[e] = i;
-          a.acc_val[e] = __ldcg(in_val + e);
-          if (k3) a.upd_tags[i] = (uint32_t)epoch;
+          uint32_t i, vb;
+          ld_ll_pair(slot + 2 + 2 * (size_t)e, tag, poll, i, vb);
+          a.acc_idx[e] = (int32_t)i;
+          a.acc_val[e] = __uint_as_float(vb);
+          if (k3) a.upd_tags[i] = tag;
+          if (out_slot) st_ll_pair(out_slot + 2 + 2 * (size_t)e, i, vb, tag);
         }
         if (blk == 0 && threadIdx.x == 0) {
           a.d_acc_n[0] = (int32_t)n_in;
           a.d_acc_n[1] = (int32_t)hint_in;
+          if (out_slot) st_ll_pair(out_slot, n_in, hint_in, tag);
         }
       }
       cur_idx = a.acc_idx;
@@ -238,8 +228,8 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
       cur_n = a.d_acc_n;
       if (tr) a.trace[4 + 4 * s] = (int64_t)globaltimer();
     }
-    // the next push reads acc written by every block; no barrier after the
-    // last step (the next call starts on a kernel boundary)
+    // the next step's merge reads acc written by every block; no barrier after
+    // the last step (the next call starts on a kernel boundary)
     if (s + 1 < a.nsteps) grid_sync(&a.merge.ews->bar, G);
     if (tr) a.trace[5 + 4 * s] = (int64_t)globaltimer();
   }

@@ -111,6 +111,60 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // ---- grid-wide barrier for cooperative launches ---------------------------
 // Generation barrier; count returns to 0 after every use so the workspace
 // needs a single zero-initialisation.
+// ---- low-latency (LL) peer records ------------------------------------------
+// A 64-bit word {payload (low 32), tag (high 32)}, stored and loaded with
+// single-copy-atomic 64-bit accesses at system scope: a receiver polls the
+// word itself until the tag is the call's, so no separate flag, fence or
+// release round trip is needed (NCCL's LL idea).  Pairs go out as one
+// 16-byte store; each 8-byte half validates itself.
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void st_ll_pair(uint64_t* p, uint32_t a, uint32_t b, uint32_t tag) {
+  const uint64_t x = ((uint64_t)tag << 32) | a, y = ((uint64_t)tag << 32) | b;
+  asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(x), "l"(y) : "memory");
+}
+__device__ __forceinline__ void ld_ll_pair_raw(const uint64_t* p, uint64_t& x, uint64_t& y) {
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(p) : "memory");
+}
+// Polling context: give up (status |= TIMEOUT / ABORTED, payload 0) once the
+// deadline passes or the host raises the abort flag.
+struct LLPoll {
+  uint64_t deadline;  // %globaltimer ns; 0 = none
+  uint32_t* status;
+  const volatile uint32_t* abort;
+};
+static __device__ __noinline__ bool ll_wait_failed(const LLPoll& c) {
+  if (c.abort && *c.abort) {
+    atomicOr(c.status, 0x8u);  // GTK_DEV_ABORTED
+    return true;
+  }
+  if (c.deadline && globaltimer_ns() > c.deadline) {
+    atomicOr(c.status, 0x4u);  // GTK_DEV_TIMEOUT
+    return true;
+  }
+  return false;
+}
+// the pair at p once both halves carry `tag`
+__device__ __forceinline__ bool ld_ll_pair(const uint64_t* p, uint32_t tag, const LLPoll& c, uint32_t& a,
+                                           uint32_t& b) {
+  uint64_t x, y;
+  ld_ll_pair_raw(p, x, y);
+  uint32_t spins = 0;
+  while ((uint32_t)(x >> 32) != tag || (uint32_t)(y >> 32) != tag) {
+    if ((++spins & 255u) == 0 && ll_wait_failed(c)) {
+      a = b = 0;
+      return false;
+    }
+    ld_ll_pair_raw(p, x, y);
+  }
+  a = (uint32_t)x;
+  b = (uint32_t)y;
+  return true;
+}
+
 // one 64-bit word: arrival count (low half) and generation (high half)
 struct __align__(8) GridBarrier {
   uint32_t count;

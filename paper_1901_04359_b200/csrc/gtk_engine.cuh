@@ -116,7 +116,19 @@ struct Sink {
   int upd_scaling;
   uint32_t* tag;      // exchange + K3: tag[idx] = tag_val marks membership of the final global list (nullable)
   uint32_t tag_val;
+  // exchange: the output also goes straight to the next step's partner as LL
+  // records (body[2p] = {idx, val bits}, head = {count, hint}), nullable
+  uint64_t* ll_body = nullptr;
+  uint64_t* ll_head = nullptr;
+  uint32_t ll_tag = 0;
 };
+
+// block 0 publishes the output count (and the k-th-key hint)
+__device__ __forceinline__ void sink_count(const Sink& out, uint32_t n, uint32_t hint) {
+  out.d_count[0] = (int32_t)n;
+  if (out.write_hint) out.d_count[1] = (int32_t)hint;
+  if (out.ll_head) st_ll_pair(out.ll_head, n, out.write_hint ? hint : 0u, out.ll_tag);
+}
 
 // one kept entry to the output list (+ the select's side effects)
 __device__ __forceinline__ void sink_put(const Sink& out, uint32_t p, int32_t i, float v) {
@@ -125,6 +137,7 @@ __device__ __forceinline__ void sink_put(const Sink& out, uint32_t p, int32_t i,
   if (out.zero_at) out.zero_at[i] = 0.0f;
   if (out.upd_w) out.upd_w[i] = __fsub_rn(out.upd_w[i], __fmul_rn(out.upd_lr, scale_u(v, out.upd_Pf, out.upd_scaling)));
   if (out.tag) out.tag[i] = out.tag_val;
+  if (out.ll_body) st_ll_pair(out.ll_body + 2 * (size_t)p, (uint32_t)i, __float_as_uint(v), out.ll_tag);
 }
 
 __device__ __forceinline__ void sink_stamp(const Sink& out, int i) {
@@ -254,6 +267,7 @@ __device__ __forceinline__ void sink_put_batch(const Sink& out, const uint32_t (
     if (out.zero_at) out.zero_at[i] = 0.0f;
     if (out.upd_w) out.upd_w[i] = __fsub_rn(wv[j], __fmul_rn(out.upd_lr, scale_u(v, out.upd_Pf, out.upd_scaling)));
     if (out.tag) out.tag[i] = out.tag_val;
+    if (out.ll_body) st_ll_pair(out.ll_body + 2 * (size_t)bp[j], (uint32_t)i, __float_as_uint(v), out.ll_tag);
   }
 }
 
@@ -358,10 +372,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
     if (blk == 0) {
       for (int r = 0; r < kRounds; ++r)
         for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[r][b] = 0;
-      if (threadIdx.x == 0) {
-        out.d_count[0] = (int32_t)kt;
-        if (out.write_hint) out.d_count[1] = 0;
-      }
+      if (threadIdx.x == 0) sink_count(out, kt, 0u);
     }
     return true;
   }
@@ -613,10 +624,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       if (blk == 0) {  // every block is past its last histogram read
         for (int rr = 0; rr < kRounds; ++rr)
           for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[rr][b] = 0;
-        if (threadIdx.x == 0) {
-          out.d_count[0] = (int32_t)kt;
-          if (out.write_hint) out.d_count[1] = (int32_t)tau;
-        }
+        if (threadIdx.x == 0) sink_count(out, kt, tau);
       }
       return true;
     }
@@ -672,10 +680,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       if (blk == 0) {
         for (int rr = 0; rr < kRounds; ++rr)
           for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[rr][b] = 0;
-        if (threadIdx.x == 0) {
-          out.d_count[0] = (int32_t)kt;
-          if (out.write_hint) out.d_count[1] = (int32_t)tau;
-        }
+        if (threadIdx.x == 0) sink_count(out, kt, tau);
       }
       return true;
     }

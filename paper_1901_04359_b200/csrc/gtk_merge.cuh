@@ -84,7 +84,38 @@ struct MergeArgs {
   uint32_t* tag;
   uint32_t tag_val;
   uint32_t slice_cap;  // slice slots staged in shared memory (behind MergeSmem)
+  // exchange: A arrives as LL records in the inbox (a_ll[2i] = {idx, val bits}
+  // tagged a_tag; a_idx / a_val unused), polled as they are read
+  const uint64_t* a_ll = nullptr;
+  uint32_t a_tag = 0;
+  LLPoll poll = {};
+  // exchange: the output also goes to the next step's partner (see Sink)
+  uint64_t* ll_body = nullptr;
+  uint64_t* ll_head = nullptr;
+  uint32_t ll_tag = 0;
 };
+
+// entry i of A (plain list or polled LL records)
+__device__ __forceinline__ void a_entry(const MergeArgs& a, uint32_t i, int32_t& idx, float& val) {
+  if (a.a_ll) {
+    uint32_t x, y;
+    ld_ll_pair(a.a_ll + 2 * (size_t)i, a.a_tag, a.poll, x, y);
+    idx = (int32_t)x;
+    val = __uint_as_float(y);
+  } else {
+    idx = __ldcg(a.a_idx + i);
+    val = __ldcg(a.a_val + i);
+  }
+}
+__device__ __forceinline__ int32_t a_index(const MergeArgs& a, uint32_t i) {
+  if (a.a_ll) {
+    int32_t idx;
+    float v;
+    a_entry(a, i, idx, v);
+    return idx;
+  }
+  return __ldcg(a.a_idx + i);
+}
 
 __device__ __forceinline__ void merge_stamp(const MergeArgs& a, int i) {
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -109,7 +140,7 @@ static inline size_t merge_smem_bytes(uint32_t slice_cap) {
 
 // number of A elements among the first d merged elements (A before B on ties);
 // executed by one full warp, result returned to every lane.
-static __device__ __forceinline__ uint32_t merge_path_warp(const int32_t* A, uint32_t na, const int32_t* B,
+static __device__ __forceinline__ uint32_t merge_path_warp(const MergeArgs& a, uint32_t na, const int32_t* B,
                                                            uint32_t nb, uint32_t d) {
   uint32_t L = d > nb ? d - nb : 0u;
   uint32_t H = d < na ? d : na;
@@ -120,13 +151,13 @@ static __device__ __forceinline__ uint32_t merge_path_warp(const int32_t* A, uin
       bool q = false;
       if (lane < n) {
         const uint32_t i = L + lane;
-        q = __ldcg(A + i) <= __ldcg(B + (d - 1 - i));
+        q = a_index(a, i) <= __ldcg(B + (d - 1 - i));
       }
       L += __popc(__ballot_sync(kFull, q));
       break;
     }
     const uint32_t p = L + (uint32_t)(((uint64_t)n * (lane + 1)) / 33);
-    const bool q = __ldcg(A + p) <= __ldcg(B + (d - 1 - p));
+    const bool q = a_index(a, p) <= __ldcg(B + (d - 1 - p));
     const unsigned bal = __ballot_sync(kFull, q);
     const int t = __popc(bal);
     const uint32_t p_prev = __shfl_sync(kFull, p, t > 0 ? t - 1 : 0);
@@ -199,6 +230,7 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
     if (blk == 0 && threadIdx.x == 0) {
       a.d_no[0] = 0;
       a.d_no[1] = 0;
+      if (a.ll_head) st_ll_pair(a.ll_head, 0u, 0u, a.ll_tag);
     }
     grid_sync(&a.ews->bar, G);  // callers may reuse the inputs right after
     return;
@@ -241,7 +273,7 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   merge_stamp(a, 0);
   for (uint32_t j = warp_id(); j <= nsub; j += kMergeThreads / 32) {
     const uint32_t d = min(d1, d0 + j * kMergeSub);
-    const uint32_t i = merge_path_warp(a.a_idx, na, a.b_idx, nb, d);
+    const uint32_t i = merge_path_warp(a, na, a.b_idx, nb, d);
     if (lane_id() == 0) S.split[j] = i;
   }
   __syncthreads();
@@ -260,8 +292,7 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
       for (int u = 0; u < 4; ++u) {
         const uint32_t t = base + u * kMergeThreads + threadIdx.x;
         if (t < la) {
-          ri[u] = __ldcg(a.a_idx + ia + t);
-          rv[u] = __ldcg(a.a_val + ia + t);
+          a_entry(a, ia + t, ri[u], rv[u]);
         } else if (t < la + lb) {
           ri[u] = __ldcg(a.b_idx + ja + (t - la));
           rv[u] = __ldcg(a.b_val + ja + (t - la));
@@ -279,7 +310,7 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
         }
       }
     }
-    const int32_t prevA = ia > 0 ? __ldcg(a.a_idx + ia - 1) : -1;
+    const int32_t prevA = ia > 0 ? a_index(a, ia - 1) : -1;
     const int32_t nextB = jb < nb ? __ldcg(a.b_idx + jb) : -1;
     const float nextBv = jb < nb ? __ldcg(a.b_val + jb) : 0.0f;
     __syncthreads();
@@ -351,7 +382,8 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   const SliceSrc src{slice_idx, slice_val, a.u_idx, a.u_val, d0, in_smem, true};
   const Sink out{a.o_idx, a.o_val, a.d_no, nullptr, true, a.trace ? a.trace + 5 : nullptr,
                  keep_all ? nullptr : rec, rec_level, rec_tau, rec_tau2, 3u,
-                 a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling, a.tag, a.tag_val};
+                 a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling, a.tag, a.tag_val,
+                 a.ll_body, a.ll_head, a.ll_tag};
   const uint32_t* h0 = solo ? esm.hist : a.ews->hist[0];
   bool ok = engine_run<kMergeThreads>(src, d0, d1, keep_all ? n_valid : a.k, keep_all, win_lo, win_shift, h0, solo,
                                       a.ews, esm, out, G);

@@ -441,28 +441,18 @@ __device__ __forceinline__ bool main_tile(const MainArgs& a, uint32_t tile, cons
   const uint64_t tbase = (uint64_t)tile * kTile;
   const unsigned lane = lane_id(), w = warp_id();
   // candidate flags (bit q*4+j) and the non-finite check
-  // fast path: the largest of my 16 keys decides whether any element can be
-  // a candidate or non-finite (NaN/inf keys are the largest); elements past m
-  // hold +0 (key 0) and are screened by the slow path whenever lo == 0
-  uint32_t kmax = 0;
+  uint32_t flags = 0;
+  bool nonfinite = false;
 #pragma unroll
   for (int q = 0; q < kMainVec; ++q)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) kmax = max(kmax, key_of(v[q][j]));
-  uint32_t flags = 0;
-  bool nonfinite = false;
-  if (kmax >= lo || kmax >= kInfKey) {
-#pragma unroll
-    for (int q = 0; q < kMainVec; ++q)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint64_t e = tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4 + j;
-        const uint32_t key = key_of(v[q][j]);
-        const bool in = full || e < a.m;
-        nonfinite |= in && key >= kInfKey;
-        if (in && key >= lo) flags |= 1u << (q * 4 + j);
-      }
-  }
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t e = tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4 + j;
+      const uint32_t key = key_of(v[q][j]);
+      const bool in = full || e < a.m;
+      nonfinite |= in && key >= kInfKey;
+      if (in && key >= lo) flags |= 1u << (q * 4 + j);
+    }
   if (__any_sync(kFull, nonfinite) && lane == 0) a.ctl->nonfinite = 1u;
 
   // index-ordered in-tile offsets, order (q, warp, lane, j): per-lane counts of

@@ -13,8 +13,8 @@ def val(key, scale):
     return float(row[i].replace(",", "")) * scale[units[i]]
 
 
-B = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-T = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+B = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+T = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
 rd, wr = val("dram__bytes_read.sum", B), val("dram__bytes_write.sum", B)
 rec = {"kernel": row[head.index("Kernel Name")].split("(")[0], "dram_bytes_read": int(rd),
        "dram_bytes_write": int(wr), "dram_bytes_per_launch": int(rd + wr),
