@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(kSampleThreads) select_sample_kernel(SampleArg
   // reading, and only then let the main pass launch (its early loads read res)
   pdl_wait();
   pdl_launch_dependents();
+  sample_stamp(a, 0, blockIdx.x == 0);
   if (a.window && !a.force_exact && (__ldcg(a.window) & 1u) && __ldcg(a.window + 3) == a.k) {
     // the previous call of this parameter measured the window: no sampling
     if (blockIdx.x == 0) {
@@ -420,6 +421,7 @@ struct MainArgs {
   uint32_t* group_cnt;  // candidates per finish block (tiles_per_group tiles each)
   uint32_t tiles_per_group;
   uint32_t n2;  // blocks [0, n2) take two tiles, the rest one (the last wave is short)
+  int64_t* trace = nullptr;  // optional timeline stamps: [0] block 0 start, [1] last block end (max)
 };
 
 // v[b >> 2][b & 3] without a dynamically indexed (local-memory) array
@@ -561,6 +563,7 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
   // tile each, so the grid's drain (blocks running alone on a few SMs) is short
   static_assert(kMainTilesPerBlock == 2, "two-tile / one-tile schedule");
   const uint32_t blk = blockIdx.x;
+  if (a.trace && blk == 0 && threadIdx.x == 0) a.trace[0] = (int64_t)globaltimer_ns();
   const uint32_t t0 = blk < a.n2 ? 2 * blk : a.n2 + blk;
   const uint32_t ntile = blk < a.n2 ? 2u : 1u;
   float4 gv[kMainTilesPerBlock][kMainVec], rv[kMainTilesPerBlock][kMainVec];
@@ -633,6 +636,10 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
       if (c) atomicAdd(a.whist + b, c);
     }
   }
+  if (a.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax((unsigned long long*)a.trace + 1, (unsigned long long)globaltimer_ns());
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -678,7 +685,7 @@ __device__ __forceinline__ void finish_stamp(const FinishArgs& a, int i) {
   }
 }
 
-__global__ void __launch_bounds__(kFinishThreads, 1) select_finish_kernel(FinishArgs a) {
+__global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(FinishArgs a) {
   __shared__ EngineSmem<kFinishThreads> sm;
   extern __shared__ __align__(16) unsigned char s_dyn[];  // the candidate slice: slice_cap (idx, val)
   int32_t* s_idx = reinterpret_cast<int32_t*>(s_dyn);
@@ -821,8 +828,11 @@ __global__ void __launch_bounds__(kFinishThreads, 1) select_finish_kernel(Finish
     SliceSrc src{s_idx, s_val, a.ord_idx, a.ord_val, before, in_smem, false};
     if (engine_run<kFinishThreads>(src, before, before + own, a.k, false, __ldcg(&a.ctl->lo),
                                    __ldcg(&a.ctl->shift), sm.hist, true, a.ews, sm, out, G,
-                                   /*slice_async=*/true))
+                                   /*slice_async=*/true)) {
+      if (a.trace && threadIdx.x == 0)  // timeline: last block end (trace_buffer()[114])
+        atomicMax((unsigned long long*)a.trace + 66, (unsigned long long)globaltimer_ns());
       return;
+    }
   }
   // exact dense fallback over acc (= res_out, untouched so far)
   cp_async_wait_all();  // the histogram prefetch must land before sm.hist is reused
@@ -1003,6 +1013,7 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
     ProfScope prof_main(kProfSelectMain, st);
     const uint32_t gmain = main_grid(L.ntiles, &ma.n2);
     if (gmain == 0) return GTK_ECUDA;
+    ma.trace = trace_buffer() ? trace_buffer() + 112 : nullptr;
     GTK_CUDA(launch_pdl(select_main_kernel, dim3(gmain), dim3(kMainThreads), 0, st, ma));
     GTK_CHECK_LAUNCH();
   }

@@ -234,8 +234,10 @@ def test_top_op_known_answers(gk):
         gk.top_op(sv(3, [(0, 1.0)]), sv(4, [(0, 1.0)]), 1)
 
 
-@pytest.mark.parametrize("k", [1, 7, 1000, 25_600, 100_000])
+@pytest.mark.parametrize("k", [1, 7, 1000, 25_600, 100_000, 660_000])
 def test_top_op_large_vs_oracle(gk, k):
+    """(660K: the density sweep's largest k -- union slices in dynamic shared
+    memory, in-bin gathers ranked through the sub-histogram)"""
     from oracle import gtopk_oracle as orc
 
     rng = np.random.default_rng(k)
@@ -385,4 +387,44 @@ def test_main_pass_measurement_leaves_workspace_clean(dev):
         assert np.array_equal(out.cpu().numpy().view(np.uint32), wres.view(np.uint32)), step
         if step >= 1:
             assert int(st.item()) & 0x2 == 0, step
+        res = wres
+
+
+@pytest.mark.parametrize("kind", ["normal", "int"])
+def test_windowed_select_large_k_vs_oracle(dev, kind):
+    """rho = 0.01 at m = 13.2M (k = 132K): finish slices beyond the minimum
+    shared-memory capacity, per-tile candidate copies, sub-histogram ranking of
+    large in-bin gathers, batched w updates (gtk_select_update) -- bit-exact
+    over carried-window steps with a building residual."""
+    import torch
+
+    from oracle import gtopk_oracle as orc
+
+    d = torch.device("cuda", 0)
+    rng = np.random.default_rng(31)
+    m, k = 13_200_000, 132_000
+    win = dev.new_window(d)
+    lst = dev.DeviceList(m, k, d)
+    st = torch.zeros(1, dtype=torch.int32, device=d)
+    res = np.zeros(m, F32)
+    w = rng.standard_normal(m).astype(F32)
+    wd = torch.from_numpy(w).to(d)
+    lr = float(np.float32(0.05))
+    for step in range(3):
+        if kind == "normal":
+            g = rng.standard_normal(m).astype(F32)
+        else:
+            g = rng.integers(-3, 4, m).astype(F32)
+        gd, rd = torch.from_numpy(g).to(d), torch.from_numpy(res).to(d)
+        out = torch.empty_like(gd)
+        st.zero_()
+        dev.select_update(rd, gd, out, k, lst, st, win, wd, lr, 1, 0)
+        wi, wv, wres = orc.top_k_select(res + g, k)
+        i, v = lst.to_host()
+        assert np.array_equal(i, wi) and np.array_equal(v.view(np.uint32), wv.view(np.uint32)), (kind, step)
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), wres.view(np.uint32)), (kind, step)
+        upd = np.zeros(m, F32)
+        upd[wi] = wv / np.float32(1)
+        w = (w - np.float32(lr) * upd).astype(F32)
+        assert np.array_equal(wd.cpu().numpy().view(np.uint32), w.view(np.uint32)), (kind, step)
         res = wres

@@ -26,6 +26,9 @@ for rep in range(4):
     tr.zero_(); torch.cuda.synchronize()
     pipe.step_eager(); torch.cuda.synchronize()
     t = tr.cpu().tolist()
+    s0 = t[64]  # sample kernel, block 0 after its pdl_wait
+    print(f"timeline rep{rep} (us from sample start): main start={(t[112]-s0)/1e3:.1f} main end={(t[113]-s0)/1e3:.1f} "
+          f"finish start={(t[48]-s0)/1e3:.1f} finish end={(t[114]-s0)/1e3:.1f}", flush=True)
     f = t[48:55]
     print(f"finish rep{rep}: " + " ".join(f"{n}={(v - f[0]) / 1e3:.1f}" for n, v in zip(names, f) if v)
           + f" | round-0 in_bin={t[55]} w_scanned={(t[56]-f[0])/1e3:.1f} w_put={(t[57]-f[0])/1e3:.1f} own={t[58]} cap={t[59]} C={t[60]} G={t[61]}", flush=True)
