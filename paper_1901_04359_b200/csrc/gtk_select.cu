@@ -584,7 +584,10 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
   for (int b = threadIdx.x; b < kHistLen; b += kMainThreads) s_hist[b] = 0u;
   // everything below consumes the sample kernel's window (and may write
   // res_out = res in place, which the sample kernel reads): wait for it --
-  // the loads above are already in flight (programmatic dependent launch)
+  // the loads above are already in flight (programmatic dependent launch;
+  // griddepcontrol.wait itself costs ~1 us per block, hidden behind them:
+  // a variant without the sample kernel that had to wait before loading res
+  // measured 6 us slower per step)
   pdl_wait();
   const uint32_t lo = __ldcg(&a.ctl->lo);
   const uint32_t shift = __ldcg(&a.ctl->shift);
@@ -843,8 +846,8 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
     if (threadIdx.x < kRounds) a.ews->gather_n[threadIdx.x] = 0;
     if (threadIdx.x == 0) {
       atomicOr(a.d_status, GTK_DEV_FALLBACK);
-      // the next call samples again; a window that admitted too few keys
-      // widens its margin from then on
+      // the record is invalid until the exact pass below rewrites it; a
+      // window that admitted too few keys widens its margin from then on
       const bool low_miss = !overflow && C < a.k;
       if (a.window) {
         a.window[0] = (low_miss ? min(kMaxWindowLevel, wlevel + 1) : wlevel) << 8;
@@ -856,8 +859,12 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
   DenseSrc dsrc{a.res_out};
   uint32_t s0, s1;
   slice_of(a.m, G, blk, s0, s1);
+  // the exact pass's own round-0 histogram (full key range, 2^20-key bins)
+  // records a fresh window for the next call (block 0), at the raised margin
+  // after a low miss and with no growth estimate across the gap
   Sink dout = out;
-  dout.next_window = nullptr;
+  dout.window_level = (!overflow && C < a.k) ? min(kMaxWindowLevel, wlevel + 1) : wlevel;
+  dout.prev_tau = dout.prev_tau2 = 0u;
   engine_run<kFinishThreads>(dsrc, s0, s1, a.k, false, 0u, 20u, nullptr, false, a.ews, sm, dout, G);
 }
 
