@@ -26,6 +26,8 @@ from .device import DeviceList
 
 
 class GTopKPipeline:
+    kBlockSteps = 20  # steps per block graph (even: the residual parity returns)
+
     """gtopk_step for fixed (state, k, P, gradient buffers), graph-replayed.
 
     grads: list of device gradient tensors; step t reads grads[t % len(grads)].
@@ -66,6 +68,7 @@ class GTopKPipeline:
             self.plan = self.group.plan(self.k, self.m)
         self.t = 0
         self.graphs = None
+        self.block_graph = None
         self.kernels_per_step = None
         self.use_graph = use_graph
 
@@ -107,7 +110,14 @@ class GTopKPipeline:
                 self._enqueue(parity)
             graphs.append(g)
         self.kernels_per_step = (_lib.load().gtk_launch_count() - n0) // 2
+        # kBlockSteps steps (both parities, in order) in one graph: one graph
+        # launch per block of steps instead of per step
+        blk = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(blk, stream=stream):
+            for j in range(self.kBlockSteps):
+                self._enqueue(j % 2)
         self.graphs = graphs
+        self.block_graph = blk
         torch.cuda.synchronize(self.dev)
 
     def profile(self, steps: int = 20) -> dict:
@@ -183,6 +193,11 @@ class GTopKPipeline:
 
     def run(self, n: int) -> None:
         """Enqueue n steps (graph replays when captured)."""
+        if self.graphs is not None:
+            while n >= self.kBlockSteps and self.t % 2 == 0:
+                self.block_graph.replay()
+                self.t += self.kBlockSteps
+                n -= self.kBlockSteps
         for _ in range(n):
             if self.graphs is not None:
                 self.graphs[self.t % 2].replay()
