@@ -54,6 +54,7 @@ extern "C" {
 
 /* gtk_select flags */
 #define GTK_SELECT_FORCE_EXACT 0x1 /* skip the sampled-threshold fast path (testing) */
+#define GTK_STEP_PREPUSHED 0x10000  /* exchange schedule flag, see gtk_gtopk_exchange */
 
 int gtk_version(void);
 const char* gtk_strerror(int code);
@@ -96,6 +97,19 @@ int gtk_select(const float* res_in, const float* grad, float* res_out, int64_t m
 int gtk_select_windowed(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
                         int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
                         size_t ws_bytes, int32_t flags, uint32_t* d_window, void* stream);
+
+/* gtk_select_windowed whose selection also goes out, as it is written, to
+ * the gTopKAllReduce exchange's first partner: LL records (see
+ * gtk_gtopk_exchange) into that partner's inbox step-0 slot of the upcoming
+ * exchange call (tag = *d_epoch + 1, slot parity = tag & 1); a non-finite
+ * input sends count -1.  The following exchange call must carry
+ * GTK_STEP_PREPUSHED on step 0 of its schedule.
+ *   peer_slot0: the partner's IPC-mapped inbox base (its step-0 slots);
+ *   d_epoch: the exchange plan's device epoch counter. */
+int gtk_select_push(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
+                    int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
+                    size_t ws_bytes, int32_t flags, uint32_t* d_window, void* peer_slot0,
+                    const uint64_t* d_epoch, void* stream);
 
 /* gtk_select_windowed + K3 in the same launches, for P = 1 where the global
  * top-k IS the local selection (gtopk_allreduce over one rank is the
@@ -172,12 +186,14 @@ int gtk_dense_sum(const float* const* srcs, int32_t P, int64_t m, float* out, vo
 /* ------------------------------------------------------------------------
  * gTopKAllReduce exchange (collectives.py:188-219) over NVLink peer memory.
  * One persistent cooperative kernel per rank runs every round of the
- * schedule: push the current list into the partner's inbox (peer stores),
- * signal with a system-scope release, wait on its own inbox flag, merge (⊤).
+ * schedule: push the current list into the partner's inbox (self-validating
+ * LL records, below), poll its own inbox for the partner's list, merge (⊤).
  *
  *  schedule (host array, nsteps entries of 4 int32: {send_to, recv_from,
- *  merge, tag}); send_to/recv_from = -1 for none; merge=1 -> acc = ⊤(recv, acc),
- *  merge=0 -> acc = recv (broadcast).
+ *  merge, flags}); send_to/recv_from = -1 for none; merge=1 -> acc = ⊤(recv, acc),
+ *  merge=0 -> acc = recv (broadcast); flags: low 16 bits informational (the
+ *  step index), GTK_STEP_PREPUSHED on step 0 = its send was done by
+ *  gtk_select_push.
  *  peer_inbox: host array of P device pointers (IPC-mapped) to each rank's
  *  inbox region of gtk_exchange_inbox_bytes(k, nsteps) bytes (zeroed once).
  *  Lists travel as low-latency records: per entry one 16-byte store of two

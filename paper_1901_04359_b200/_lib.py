@@ -31,6 +31,7 @@ DEV_PEER_FAILED = 0x10
 DEV_ERROR_MASK = 0x1D
 
 SELECT_FORCE_EXACT = 0x1
+STEP_PREPUSHED = 0x10000
 
 # every symbol include/gtopk_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = (
@@ -42,6 +43,7 @@ EXPORTS = (
     "gtk_select",
     "gtk_select_windowed",
     "gtk_select_update",
+    "gtk_select_push",
     "gtk_select_main_pass",
     "gtk_merge_workspace_bytes",
     "gtk_top_op",
@@ -84,6 +86,7 @@ _SIGS = {
     "gtk_select": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _I32, _P], _I32),
     "gtk_select_windowed": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _I32, _P, _P], _I32),
     "gtk_select_update": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _I32, _P, _P, _F, _I32, _I32, _P], _I32),
+    "gtk_select_push": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _I32, _P, _P, _P, _P], _I32),
     "gtk_select_main_pass": ([_P, _P, _P, _I64, _I32, _P, _SZ, _I32, _P], _I32),
     "gtk_merge_workspace_bytes": ([_I32, _I32, ctypes.POINTER(_SZ)], _I32),
     "gtk_top_op": ([_P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _SZ, _P], _I32),

@@ -74,9 +74,7 @@ struct ExchangeArgs {
 };
 
 
-// inbox slot: 16 B LL header {count | tag, hint | tag} | k LL entries of 16 B
-// {idx | tag, val bits | tag}
-__host__ __device__ inline size_t slot_bytes(int32_t k) { return (16 + (size_t)k * 16 + 255) & ~size_t(255); }
+__host__ __device__ inline size_t slot_bytes(int32_t k) { return ll_slot_bytes(k); }
 __device__ __forceinline__ uint64_t* slot_of(char* inbox, int s, uint32_t par, int32_t k) {
   return reinterpret_cast<uint64_t*>(inbox + ((size_t)s * 2 + par) * slot_bytes(k));
 }
@@ -127,7 +125,9 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   const uint32_t tag = (uint32_t)epoch;
   const LLPoll poll{a.timeout_ns > 0 ? globaltimer() + (uint64_t)a.timeout_ns : 0ull, a.d_status, a.d_abort};
   bool poisoned = self_poison;  // per block, but every block decides it from the same words
-  bool pushed = false;          // this step's send already went out with the previous step's output
+  // this step's send already went out: with the previous step's output, or
+  // (step 0) with the select's output (gtk_select_push)
+  bool pushed = (a.steps[0].tag & kStepPrepushed) != 0;
   for (int s = 0; s < a.nsteps; ++s) {
     const Step st = a.steps[s];
     // the next step sends the list this step's merge / copy produces: fuse
@@ -417,6 +417,7 @@ static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32
   a.d_epoch = d_epoch;
   for (int s = 0; s < nsteps; ++s) {
     a.steps[s] = Step{schedule[4 * s], schedule[4 * s + 1], schedule[4 * s + 2], schedule[4 * s + 3]};
+    if ((a.steps[s].tag & kStepPrepushed) && (s != 0 || a.steps[s].send_to < 0)) return GTK_EINVAL;
     if (a.steps[s].send_to >= P || a.steps[s].recv_from >= P) return GTK_EINVAL;
   }
   for (int r = 0; r < P; ++r) {

@@ -129,6 +129,11 @@ __device__ __forceinline__ void st_ll_pair(uint64_t* p, uint32_t a, uint32_t b, 
 __device__ __forceinline__ void ld_ll_pair_raw(const uint64_t* p, uint64_t& x, uint64_t& y) {
   asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(p) : "memory");
 }
+// inbox slot of the exchange (one per step and call parity): 16 B LL header
+// {count | tag, hint | tag} | k LL entries of 16 B {idx | tag, val bits | tag}
+__host__ __device__ inline size_t ll_slot_bytes(int32_t k) { return (16 + (size_t)k * 16 + 255) & ~size_t(255); }
+constexpr int32_t kStepPrepushed = 0x10000;  // schedule flag: step 0's send was done by gtk_select_push
+
 // Polling context: give up (status |= TIMEOUT / ABORTED, payload 0) once the
 // deadline passes or the host raises the abort flag.
 struct LLPoll {

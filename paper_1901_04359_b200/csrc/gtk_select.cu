@@ -678,6 +678,12 @@ struct FinishArgs {
   float upd_Pf;
   int upd_scaling;
   uint32_t slice_cap;  // candidates per block staged in (dynamic) shared memory
+  // gtk_select_push: the selection also goes out as LL records to the
+  // exchange's first partner (inbox step-0 slots at ll_base, slot parity and
+  // tag from the upcoming exchange call's epoch = *ll_epoch + 1), nullable
+  uint64_t* ll_base = nullptr;
+  const uint64_t* ll_epoch = nullptr;
+  uint32_t ll_slot_words = 0;
 };
 
 __device__ __forceinline__ void finish_stamp(const FinishArgs& a, int i) {
@@ -705,6 +711,10 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
       for (int b = threadIdx.x; b < kHistLen; b += kFinishThreads) a.ews->hist[0][b] = 0;
       if (threadIdx.x == 0) {
         atomicOr(a.d_status, GTK_DEV_NONFINITE);
+        if (a.ll_base) {  // the exchange's first partner learns it at once: count -1 (poisoned)
+          const uint32_t tag = (uint32_t)(__ldcg((const unsigned long long*)a.ll_epoch) + 1ull);
+          st_ll_pair(a.ll_base + (size_t)(tag & 1u) * a.ll_slot_words, 0xFFFFFFFFu, 0u, tag);
+        }
         if (a.window) {
           a.window[0] = wlevel << 8;
           a.window[4] = a.window[5] = 0u;
@@ -713,8 +723,15 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
     }
     return;
   }
-  const Sink out{a.sel_idx, a.sel_val, a.d_count, a.res_out, true, a.trace ? a.trace + 3 : nullptr,
-                 a.window, wlevel, wtau, wtau2, 1u, a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling};
+  Sink out{a.sel_idx, a.sel_val, a.d_count, a.res_out, true, a.trace ? a.trace + 3 : nullptr,
+           a.window, wlevel, wtau, wtau2, 1u, a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling};
+  if (a.ll_base) {  // the exchange's step 0 send, straight from the write phase
+    const uint32_t tag = (uint32_t)(__ldcg((const unsigned long long*)a.ll_epoch) + 1ull);
+    uint64_t* slot = a.ll_base + (size_t)(tag & 1u) * a.ll_slot_words;
+    out.ll_body = slot + 2;
+    out.ll_head = slot;
+    out.ll_tag = tag;
+  }
   finish_stamp(a, 0);
 
   // the round-0 window histogram (main pass) -> sm.hist by async copies
@@ -906,15 +923,30 @@ struct FusedUpdate {
 };
 }  // namespace
 
+struct PeerPush {
+  uint64_t* slot0;
+  const uint64_t* epoch;
+};
 static int select_impl(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
                        int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
-                       size_t ws_bytes, int32_t flags, uint32_t* d_window, FusedUpdate upd, void* stream);
+                       size_t ws_bytes, int32_t flags, uint32_t* d_window, FusedUpdate upd, void* stream,
+                       PeerPush push = {nullptr, nullptr});
 
 extern "C" int gtk_select_windowed(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
                                    int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status,
                                    void* ws, size_t ws_bytes, int32_t flags, uint32_t* d_window, void* stream) {
   return select_impl(res_in, grad, res_out, m, k, sel_idx, sel_val, d_count, d_status, ws, ws_bytes, flags,
                      d_window, FusedUpdate{nullptr, 0.0f, 1.0f, 0}, stream);
+}
+
+extern "C" int gtk_select_push(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
+                               int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
+                               size_t ws_bytes, int32_t flags, uint32_t* d_window, void* peer_slot0,
+                               const uint64_t* d_epoch, void* stream) {
+  if (!peer_slot0 || !d_epoch) return GTK_EINVAL;
+  return select_impl(res_in, grad, res_out, m, k, sel_idx, sel_val, d_count, d_status, ws, ws_bytes, flags,
+                     d_window, FusedUpdate{nullptr, 0.0f, 1.0f, 0}, stream,
+                     PeerPush{(uint64_t*)peer_slot0, d_epoch});
 }
 
 extern "C" int gtk_select_update(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
@@ -930,7 +962,8 @@ extern "C" int gtk_select_update(const float* res_in, const float* grad, float* 
 
 static int select_impl(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
                        int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
-                       size_t ws_bytes, int32_t flags, uint32_t* d_window, FusedUpdate upd, void* stream) {
+                       size_t ws_bytes, int32_t flags, uint32_t* d_window, FusedUpdate upd, void* stream,
+                       PeerPush push) {
   if (!grad || !res_out || !sel_idx || !sel_val || !d_count || !d_status || !ws) return GTK_EINVAL;
   if (m < 1 || m >= (int64_t(1) << 31) || k < 1 || k > m) return GTK_EINVAL;
   const SelectLayout L = select_layout(m, k);
@@ -1054,6 +1087,11 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
                 upd.Pf,
                 upd.scaling,
                 slice_cap};
+  if (push.slot0) {
+    fa.ll_base = push.slot0;
+    fa.ll_epoch = push.epoch;
+    fa.ll_slot_words = (uint32_t)(ll_slot_bytes(k) / sizeof(uint64_t));
+  }
 
 
   void* args[] = {&fa};

@@ -166,6 +166,21 @@ def select(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, out: Devic
     )
 
 
+def select_push(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, out: DeviceList,
+                status: torch.Tensor, window: torch.Tensor | None, peer_slot0: int, epoch: torch.Tensor) -> None:
+    """K1 whose selection also goes straight to the exchange's first partner
+    (gtk_select_push): peer_slot0 = that partner's mapped inbox, epoch = the
+    exchange plan's device epoch.  The next exchange runs prepushed."""
+    m = grad.numel()
+    dev = grad.device
+    ws = select_workspace(m, k, dev)
+    _lib.call(
+        "gtk_select_push", P(res_in), P(grad), P(res_out), m, k, P(out.idx), P(out.val), P(out.count),
+        P(status), P(ws), ctypes.c_size_t(ws.numel()), 0, P(window), ctypes.c_void_p(peer_slot0), P(epoch),
+        stream_of(dev),
+    )
+
+
 def time_main_pass(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, reps: int) -> float:
     """Measurement only: ms per launch of K1's HBM pass against the window the
     last select of this (m, k) published (gtk_select_main_pass): CUDA events

@@ -84,6 +84,16 @@ class _ExchangePlan:
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.epoch = torch.zeros(1, dtype=torch.int64, device=dev)  # advanced by the kernel
         self.tags = None  # u32[m] K3 membership tags (gtk_gtopk_exchange_update), allocated on first use
+        # gtk_select_push: the first step's partner inbox (its step-0 slots),
+        # and the schedule variant whose step 0 is marked as already pushed
+        s0 = steps[0][0] if steps else -1
+        self.push_slot0 = self.peer_inbox[s0] if s0 >= 0 else None
+        if s0 >= 0:
+            pre = sched.copy()
+            pre[3] |= _lib.STEP_PREPUSHED
+            self.schedule_prepushed = (ctypes.c_int32 * len(pre))(*pre.tolist())
+        else:
+            self.schedule_prepushed = None
         dist.barrier(group=group.gloo)  # every rank mapped every peer before first use
 
     def close(self):
@@ -154,14 +164,17 @@ class DistDeviceGroup:
         return plan.acc
 
     def enqueue_exchange(self, plan: _ExchangePlan, lst: DeviceList, status: torch.Tensor,
-                         update=None) -> None:
+                         update=None, prepushed: bool = False) -> None:
         """Launch the fused exchange kernel on the current stream: plan.acc
         becomes the global top-k of every rank's `lst`.  No host sync; the
         launch is CUDA-graph capturable (device-side epoch).  update = (w,
         res, lr, scaling): K3's sparse form runs in the same kernel
         (gtk_gtopk_exchange_update; `lst` must not be plan.acc)."""
         src = None if lst is plan.acc else lst
-        args = [self.rank, self.world, plan.schedule, plan.nsteps, plan.peer_inbox,
+        if prepushed and plan.schedule_prepushed is None:
+            raise ValueError("no first-step partner to have pushed to")
+        sched = plan.schedule_prepushed if prepushed else plan.schedule
+        args = [self.rank, self.world, sched, plan.nsteps, plan.peer_inbox,
                 plan.peer_flags, P(plan.epoch), P(plan.acc.idx), P(plan.acc.val), P(plan.acc.count),
                 plan.k, P(status), None, ctypes.c_int64(int(self.timeout * 1e9)), P(plan.step_counts),
                 P(src.idx if src else None), P(src.val if src else None), P(src.count if src else None),

@@ -81,6 +81,14 @@ class GTopKPipeline:
             _dev.select_update(res_in, grad, res_out, self.k, self.sel, self.status, self.window,
                                self.state._w, self.lr, 1, self.scaling)
             return
+        if self.P > 1 and _dev.sparse_update_fusable(self.lr, self.mom) and self.plan.push_slot0 is not None:
+            # the selection goes to the first partner as it is written
+            # (gtk_select_push), K3 rides on the exchange kernel
+            _dev.select_push(res_in, grad, res_out, self.k, self.sel, self.status, self.window,
+                             self.plan.push_slot0, self.plan.epoch)
+            self.group.enqueue_exchange(self.plan, self.sel, self.status,
+                                        update=(self.state._w, res_out, self.lr, self.scaling), prepushed=True)
+            return
         _dev.select(res_in, grad, res_out, self.k, self.sel, self.status, window=self.window)
         if self.P > 1 and _dev.sparse_update_fusable(self.lr, self.mom):
             # K3 rides on the exchange kernel (one launch fewer, no membership pass)

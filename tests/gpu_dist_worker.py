@@ -108,6 +108,24 @@ def main():
     except TransportError:
         check(r != P - 1, "poison: TransportError on the failing rank")
     check(np.array_equal(st3.weights, w_before) and st3.iteration == 0, "poison: state changed")
+    # 5. poison through the graph pipeline (the selection goes to the first
+    #    partner straight from K1's finish: a non-finite input sends count -1
+    #    from there): every rank's sticky status fails, K3 never ran after it
+    m5, k5 = 50_000, 50
+    gp = [np.random.default_rng(100 + r).standard_normal(m5).astype(F32) for _ in range(2)]
+    if r == P - 1:
+        gp[1][77] = np.inf
+    st5 = opt.make_state(torch.zeros(m5, device=dev), lr=0.1)
+    pipe5 = GTopKPipeline(ep, st5, k5, [torch.from_numpy(x).to(dev) for x in gp])
+    try:
+        pipe5.capture()  # step 1 (the second gradient) is poisoned
+        pipe5.run(3)
+        pipe5.check()
+        check(False, "pipeline poison: no exception")
+    except FloatingPointError:
+        check(r == P - 1, "pipeline poison: FloatingPointError on a healthy rank")
+    except TransportError:
+        check(r != P - 1, "pipeline poison: TransportError on the failing rank")
     # the cluster is still usable afterwards
     res = coll.gtopk_allreduce(ep, SparseVector(100, [r], [1.0 + r]), 1, P)
     check(res.global_topk.indices.tolist() == [P - 1], "after poison")
