@@ -375,7 +375,14 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
     }
     if (threadIdx.x == 0 && S.s_valid) atomicAdd(&a.ctl->n_valid, S.s_valid);
     grid_sync(&a.ews->bar, G);
+    // the global histogram -> shared memory by async copies, landing while
+    // the valid count is read: the engine's bin search then needs no second
+    // L2 round trip
+    for (int b = threadIdx.x; b < kHistLen; b += kMergeThreads) cp_async4(&esm.hist[b], a.ews->hist[0] + b);
+    cp_async_commit();
     n_valid = __ldcg(&a.ctl->n_valid);
+    cp_async_wait_all();
+    __syncthreads();
   }
   merge_stamp(a, 3);  // after the histogram barrier
   const bool keep_all = n_valid <= a.k;
@@ -384,9 +391,8 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
                  keep_all ? nullptr : rec, rec_level, rec_tau, rec_tau2, 3u,
                  a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling, a.tag, a.tag_val,
                  a.ll_body, a.ll_head, a.ll_tag};
-  const uint32_t* h0 = solo ? esm.hist : a.ews->hist[0];
-  bool ok = engine_run<kMergeThreads>(src, d0, d1, keep_all ? n_valid : a.k, keep_all, win_lo, win_shift, h0, solo,
-                                      a.ews, esm, out, G);
+  bool ok = engine_run<kMergeThreads>(src, d0, d1, keep_all ? n_valid : a.k, keep_all, win_lo, win_shift, esm.hist,
+                                      true, a.ews, esm, out, G);
   merge_stamp(a, 4);  // engine done
   if (a.trace && rec && blk == 0 && threadIdx.x == 0) a.trace[13] = __ldcg(rec + 1);
   if (!ok) {  // the window missed (hint: cancellation; carried: a shift): full key range
