@@ -30,6 +30,10 @@ constexpr int kGatherCap = 1024;  // gather buffer size
 constexpr int kGatherMax = 384;   // gathered entries loaded speculatively with the count after the barrier
 constexpr int kRankDirect = 96;   // gathers up to this size are ranked O(n^2) directly; larger via a sub-histogram
 constexpr int kMaxBlocks = 1024;
+#ifndef GTK_MERGE_BIN_TARGET
+#define GTK_MERGE_BIN_TARGET 64
+#endif
+constexpr uint32_t kMergeBinTarget = GTK_MERGE_BIN_TARGET;  // merge windows: entries in the k-th key's bin
 
 struct EngineWS {
   GridBarrier bar;
@@ -433,7 +437,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
           // for resolution instead -- bins narrow enough that the k-th key's
           // bin holds ~64 entries at the measured density, the k-th key in
           // the middle of the 2048 bins (>= 1024 bins of room to move down)
-          const uint64_t dens_w = ((uint64_t)64 << shift) / in_bin;  // key units per ~64 entries
+          const uint64_t dens_w = ((uint64_t)kMergeBinTarget << shift) / in_bin;  // key units per ~target entries
           uint32_t sd = 0;
           while (sd < 31 && (2ull << sd) <= dens_w) ++sd;
           sd += out.window_level - 2;  // a miss widens
