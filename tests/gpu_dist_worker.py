@@ -64,6 +64,17 @@ def main():
         check(np.array_equal(bits(res.global_topk.values), bits(want_v)), f"val trial {trial}")
         check(d.msgs_sent >= 1, f"stats trial {trial}")
 
+    # 1b. large k (the density sweep's regime): union slices of the exchange
+    #     kernel's merges beyond the minimum shared-memory capacity, LL
+    #     records of 400K entries per step
+    m, k = 4_000_000, 400_000
+    lr_rng = np.random.default_rng(9)
+    lists = [orc.top_k_select(lr_rng.standard_normal(m).astype(F32), k)[:2] for _ in range(P)]
+    want_i, want_v = orc.tree_fold(lists, k)
+    res = coll.gtopk_allreduce(ep, SparseVector(m, *lists[r]), k, P)
+    check(np.array_equal(res.global_topk.indices, want_i), "large-k idx")
+    check(np.array_equal(bits(res.global_topk.values), bits(want_v)), "large-k val")
+
     # 2. full gtopk_step trajectories vs the oracle (m=270K ResNet-20 size)
     m, k, steps = 270_000, 270, 4
     g_rng = np.random.default_rng(5)
