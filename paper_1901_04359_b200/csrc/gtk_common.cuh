@@ -111,6 +111,10 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // ---- grid-wide barrier for cooperative launches ---------------------------
 // Generation barrier; count returns to 0 after every use so the workspace
 // needs a single zero-initialisation.
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // ---- low-latency (LL) peer records ------------------------------------------
 // A 64-bit word {payload (low 32), tag (high 32)}, stored and loaded with
 // single-copy-atomic 64-bit accesses at system scope: a receiver polls the

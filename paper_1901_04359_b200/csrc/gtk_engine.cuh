@@ -490,6 +490,9 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
         const bool valid = s < s1 && src.get(s, key, i, v);
         n_above += valid && (uint64_t)key >= bhi;
         const bool inb = valid && (uint64_t)key < bhi && key >= blo;
+        // a potential winner: its w line (fused update) heads for L2 now, so
+        // the write phase's read-modify-write after the barrier hits there
+        if (out.upd_w && valid && key >= blo) prefetch_l2(out.upd_w + i);
         const unsigned bal = __ballot_sync(kFull, inb);
         if (bal == 0u) continue;
         uint32_t p0 = 0;
