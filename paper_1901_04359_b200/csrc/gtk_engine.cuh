@@ -308,7 +308,7 @@ __device__ void engine_write(const Src& src, uint32_t s0, uint32_t s1, uint32_t 
     const uint32_t ex = block_excl_scan<NT>(cnt, sm.scan, &k_tot);
     sm.wcnt[threadIdx.x] = ex;
     __syncthreads();
-    if (c0 == s0) sink_stamp(out, 5);
+    if (c0 == s0 && out.zero_at) sink_stamp(out, 5);  // (select only: a merge keeps diagnostics there)
     const unsigned lt = lanemask_lt();
     while (kbits) {
       uint32_t bp[kSinkBatch];
@@ -330,7 +330,7 @@ __device__ void engine_write(const Src& src, uint32_t s0, uint32_t s1, uint32_t 
     }
     out_pos += k_tot;
     __syncthreads();  // sm.wcnt is reused by the next chunk
-    if (c0 == s0) sink_stamp(out, 6);
+    if (c0 == s0 && out.zero_at) sink_stamp(out, 6);
   }
 }
 
