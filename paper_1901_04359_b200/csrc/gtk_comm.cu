@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
       }
       if (tr) a.trace[100 + s] = (int64_t)globaltimer();
     }
-    if (st.send_to >= 0 && pushed && blk == 0 && threadIdx.x == 0 && a.step_counts)
+    if (st.send_to >= 0 && pushed && blk == 0 && threadIdx.x == 32 && a.step_counts)  // (not the polling thread)
       a.step_counts[2 * s] = min(__ldcg(cur_n), a.k);  // the previous merge's output (final after the barrier)
     pushed = false;
     if (tr) a.trace[2 + 4 * s] = (int64_t)globaltimer();
