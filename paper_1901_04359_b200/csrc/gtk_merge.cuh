@@ -284,6 +284,16 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
     const uint32_t ia = S.split[j], ib = S.split[j + 1];
     const uint32_t ja = sub - ia, jb = sub_end - ib;
     const uint32_t la = ib - ia, lb = jb - ja;
+    // the neighbours across the sub-chunk edges go out first (an LL record of
+    // A is only checked after the staging loads: no extra round trip)
+    uint64_t pax = 0, pay = 0;
+    int32_t prevA = -1;
+    if (ia > 0) {
+      if (a.a_ll) ld_ll_pair_raw(a.a_ll + 2 * (size_t)(ia - 1), pax, pay);
+      else prevA = __ldcg(a.a_idx + ia - 1);
+    }
+    const int32_t nextB = jb < nb ? __ldcg(a.b_idx + jb) : -1;
+    const float nextBv = jb < nb ? __ldcg(a.b_val + jb) : 0.0f;
     // stage A[ia, ib) and B[ja, jb): every load of the sub-chunk in flight at once
     for (uint32_t base = 0; base < la + lb; base += 4 * kMergeThreads) {
       int32_t ri[4];
@@ -310,9 +320,9 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
         }
       }
     }
-    const int32_t prevA = ia > 0 ? a_index(a, ia - 1) : -1;
-    const int32_t nextB = jb < nb ? __ldcg(a.b_idx + jb) : -1;
-    const float nextBv = jb < nb ? __ldcg(a.b_val + jb) : 0.0f;
+    if (ia > 0 && a.a_ll)
+      prevA = ((uint32_t)(pax >> 32) == a.a_tag && (uint32_t)(pay >> 32) == a.a_tag) ? (int32_t)(uint32_t)pax
+                                                                                      : a_index(a, ia - 1);
     __syncthreads();
     for (uint32_t t = threadIdx.x; t < la; t += kMergeThreads) {
       const int32_t x = S.sAi[t];
