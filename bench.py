@@ -32,7 +32,6 @@ from __future__ import annotations
 import argparse
 import ctypes
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -46,6 +45,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "gTopKAllReduce+select ms/iter at m=25.6M ρ=0.001 @1/2/4/8 B200; select HBM GB/s"
+DATA = "synthetic: cli.run_bench draws (seed 0, rank r = draw r; next batch = draw P + r)"
 M_DEFAULT = 25_600_000
 RHO_DEFAULT = 0.001
 
@@ -136,37 +136,15 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
-def oracle_step_time(m, rho, P, step_budget_s, total_budget_s, seed_base=0, max_steps=10**9):
-    """Time oracle gtopk steps (thread per rank, like the reference's
-    run_workers) on a sample of the workload.  Returns (ms_per_step_scaled,
-    sample_description, steps_run).  If one full-size step would exceed
-    step_budget_s, each step runs on a contiguous sample of m_s elements and
-    the time is scaled by m log m / (m_s log m_s) (argsort dominates the
-    reference step)."""
-    from oracle import gtopk_oracle as orc
-
-    waves = math.ceil(P / max(1, host_cores()))
-    est_full = 0.28e-6 * m * waves  # ~7 s per rank at 25.6M on one core (survey probe)
-    frac = min(1.0, step_budget_s / max(est_full, 1e-9))
-    budget_s = total_budget_s
-    ms_ = max(1024, int(m * frac))
-    ks = k_from_density(rho, ms_)
-    rng = np.random.default_rng(seed_base)
-    grads = [rng.standard_normal(ms_).astype(np.float32) for _ in range(P)]
-    states = [orc.State(np.zeros(ms_, np.float32), 0.01) for _ in range(P)]
-    times = []
-    t_end = time.perf_counter() + budget_s
-    while len(times) < max_steps:
-        t0 = time.perf_counter()
-        orc.threaded_gtopk_step(states, grads, ks)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() > t_end:
-            break
-    scale = (m * math.log2(m)) / (ms_ * math.log2(ms_))
-    ms = statistics.mean(times) * 1e3 * scale
-    sample = (f"{len(times)} oracle gtopk step(s) on {P} host thread(s), m_s={ms_} "
-              f"({ms_ / m:.3f} of m), k_s={ks}; time x m*log2(m)/(m_s*log2(m_s)) = x{scale:.3f}")
-    return ms, sample, len(times)
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def host_cores():
@@ -176,15 +154,55 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def workload_config(m, rho, P):
+    """The `config` both arms report, key for key (the driver compares them)."""
+    k = k_from_density(rho, m)
+    return {"workload": f"resnet50-size gradient m={m} rho={rho} (k={k}), P={P} ranks, one per GPU",
+            "m": m, "k": k, "rho": rho, "P": P}
+
+
+def oracle_steps(m, rho, P, steps, warmup):
+    """The reference's CPU path (the oracle port: numpy, one host thread per
+    rank like run_workers) on the FULL workload: `warmup` untimed and `steps`
+    timed gtopk steps (residual-add + select + tree fold + update) on the same
+    gradients as the GPU arm (cli.run_bench draws: seed 0, rank r = draw r;
+    next batch = draw P + r).  Returns (ms per step, description)."""
+    from oracle import gtopk_oracle as orc
+
+    k = k_from_density(rho, m)
+    rng = np.random.default_rng(0)
+    draws = [rng.standard_normal(m).astype(np.float32) for _ in range(2 * P)]
+    batches = [draws[:P], draws[P:]]
+    states = [orc.State(np.zeros(m, np.float32), 0.01) for _ in range(P)]
+    for i in range(warmup):
+        orc.threaded_gtopk_step(states, batches[i % 2], k)
+    times = []
+    for i in range(steps):
+        t0 = time.perf_counter()
+        orc.threaded_gtopk_step(states, batches[(warmup + i) % 2], k)
+        times.append(time.perf_counter() - t0)
+    ms = statistics.mean(times) * 1e3
+    sd = statistics.pstdev(times) * 1e3 if len(times) > 1 else 0.0
+    desc = (f"{steps} timed (+{warmup} untimed) full-size oracle gtopk steps (m={m}, k={k}) on {P} host "
+            f"thread(s), one per rank; mean {ms:.1f} ms, std {sd:.1f} ms; {host_cores()} cores available "
+            f"({cpu_model()})")
+    return ms, desc
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's CPU path (oracle port) on the host cores
+# ---------------------------------------------------------------------------
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
     P = max(1, world)
     m, rho = args.m, args.rho
-    k = k_from_density(rho, m)
-    budget = float(os.environ.get("GTK_REF_BUDGET_S", "150"))
-    per_step = min(10.0, max(1.0, budget / max(1, args.steps + args.warmup)))
-    ms, sample, n = oracle_step_time(m, rho, P, per_step, budget, max_steps=args.steps)
+    # full size, no extrapolation: ~3.6 s per step at the headline, so the
+    # driver's --steps 20 --warmup 5 run takes ~1.5 min; the warm-up is capped
+    # at 3 steps (the CPU path has no caches to warm beyond the first call)
+    ms, sample = oracle_steps(m, rho, P, args.steps, min(args.warmup, 3))
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -198,9 +216,8 @@ def run_reference(args, rank, world):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": f"resnet50-size gradient m={m} rho={rho} (k={k}), P={P} ranks",
-                   "m": m, "k": k, "rho": rho, "P": P},
+        "data": DATA,
+        "config": workload_config(m, rho, P),
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": min(P, host_cores()), "kind": "port",
                          "sample": sample},
         "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -360,8 +377,7 @@ def run_b200(args, rank, world):
     # ---- CPU baseline (rank 0, N = 1 only) -----------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cms, sample, _ = oracle_step_time(m, rho, 1, 10.0, float(os.environ.get("GTK_CPU_BUDGET_S", "20")),
-                                          max_steps=3)
+        cms, sample = oracle_steps(m, rho, 1, 3, 0)  # ~11 s of CPU work
         cpu = {"value": round(cms, 3), "unit": "ms", "cores": 1, "kind": "port", "sample": sample}
 
     if rank == 0:
@@ -378,10 +394,10 @@ def run_b200(args, rank, world):
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "f32",
-            "data": "synthetic: cli.run_bench draws (seed 0, rank r = draw r; next batch = draw P + r)",
-            "config": {
-                "workload": f"resnet50-size gradient m={m} rho={rho} (k={k}), P={P} ranks, one per GPU",
-                "m": m, "k": k, "rho": rho, "P": P, "exchange": exch,
+            "data": DATA,
+            "config": workload_config(m, rho, P),
+            "run": {
+                "exchange": exch,
                 "step": "K1 select + gTopKAllReduce + K3 update, CUDA-graph replay",
                 "l2": "inputs larger than L2: 307 MB streamed by K1 per step vs 126 MB L2",
                 "residual": f"steady state: {args.precondition} untimed preconditioning steps before warmup",
@@ -398,8 +414,8 @@ def run_b200(args, rank, world):
                 "rounds": pipe.plan.nsteps,
                 "us_per_round": (round(stage["exchange"] * 1e3 / pipe.plan.nsteps, 2)
                                  if stage.get("exchange") else None),
-                # k (i32 idx + f32 val) per round over 900 GB/s NVLink 5
-                "nvlink_floor_us_per_round": round(8 * k / 900e3, 3),
+                # k LL records of 16 B (idx|tag, value|tag) per round over 900 GB/s NVLink 5
+                "nvlink_floor_us_per_round": round(16 * k / 900e3, 3),
                 "note": "per round: push + partner flag + merge (+ K3 after the last round); latency-bound"},
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": 4 * m,
                     "d2h_bytes_per_step": 8},

@@ -54,6 +54,7 @@ extern "C" {
 
 /* gtk_select flags */
 #define GTK_SELECT_FORCE_EXACT 0x1 /* skip the sampled-threshold fast path (testing) */
+#define GTK_SELECT_CHAIN 0x2       /* chained windowed select, see gtk_select_settle */
 #define GTK_STEP_PREPUSHED 0x10000  /* exchange schedule flag, see gtk_gtopk_exchange */
 
 int gtk_version(void);
@@ -123,6 +124,25 @@ int gtk_select_update(const float* res_in, const float* grad, float* res_out, in
                       size_t ws_bytes, int32_t flags, uint32_t* d_window, float* w, float lr, int32_t P,
                       int32_t scaling, void* stream);
 
+/* Chained selects (flags |= GTK_SELECT_CHAIN on gtk_select_windowed /
+ * gtk_select_update; d_window required): a training loop's successive
+ * selections of one residual, two launches per call instead of three.
+ *  - no sampling kernel: the window comes from the record (a record that
+ *    holds none -- the first call, or after a miss -- costs one exact dense
+ *    pass, which records a window for the next call);
+ *  - the k winners' residual slots are left PENDING in res_out (holding acc)
+ *    and the exact winner predicate goes to the record {tau = the k-th key,
+ *    cut = the largest kept index with key == tau}: the next chained call
+ *    zeroes them on the fly while it streams res_in = this call's res_out, so
+ *    its loads never wait for this call's finish;
+ *  - gtk_select_settle(res_out, sel_idx, d_count, d_window) materialises the
+ *    residual the reference keeps (optimizer.py:230: +0.0 at the winners) --
+ *    call it before the residual is read by anything but the next chained
+ *    select.  Selections, values and the settled residual are bitwise those
+ *    of gtk_select_windowed.  res_out must not alias res_in or grad. */
+int gtk_select_settle(float* res, const int32_t* sel_idx, const int32_t* d_count, uint32_t* d_window,
+                      void* stream);
+
 /* Measurement only (bench.py's roofline): `reps` back-to-back launches of
  * K1's HBM pass alone (res_out = res_in + grad, candidate compaction and the
  * window histogram) against the key window the last select on this
@@ -153,15 +173,13 @@ int gtk_top_op(const int32_t* a_idx, const float* a_val, const int32_t* d_na, co
  *   vel may be NULL when momentum == 0.  l_idx may be NULL (no extra residual).
  *   Bitwise identical to the reference's dense update.
  * ------------------------------------------------------------------------ */
-int gtk_update_workspace_bytes(int64_t m, size_t* bytes);
 /*   d_skip: optional device status word; if any GTK_DEV_* error bit is set
  *           the kernels leave w/res/vel untouched (a failed step must not
  *           change the state, optimizer.py:219-230). */
 int gtk_scatter_update(float* w, float* res, float* vel, const int32_t* g_idx, const float* g_val,
                        const int32_t* d_gn, const int32_t* l_idx, const float* l_val,
                        const int32_t* d_ln, int64_t m, float lr, float momentum, int32_t P,
-                       int32_t scaling, const uint32_t* d_skip, void* ws, size_t ws_bytes,
-                       void* stream);
+                       int32_t scaling, const uint32_t* d_skip, void* stream);
 
 /* optimizer.py:92-99 with a dense update: u = divide_by > 0 ? upd / FLOAT(divide_by) : upd;
  * if vel: vel = FLOAT(mom)*vel + u, u = vel;  w -= FLOAT(lr) * u.  (dense/topk baselines) */
@@ -200,17 +218,24 @@ int gtk_dense_sum(const float* const* srcs, int32_t P, int64_t m, float* out, vo
  *  64-bit words {idx | tag << 32, val bits | tag << 32}, the slot header
  *  {count | tag, hint | tag}, tag = the call's epoch; the receiver polls the
  *  words until they carry its tag (no separate flag or fence).
- *  peer_flags: host array of P device pointers to each rank's uint64
- *  flags[nsteps*2] -- unused by the record protocol, kept in the ABI.
  * ------------------------------------------------------------------------ */
 int gtk_exchange_inbox_bytes(int32_t k, int32_t nsteps, size_t* bytes);
-int gtk_exchange_flags_bytes(int32_t nsteps, size_t* bytes);
 /* cudaMalloc'd + zeroed region (IPC handles need whole allocations) */
 int gtk_dev_alloc(size_t bytes, void** dptr);
 int gtk_dev_free(void* dptr);
 int gtk_ipc_get_handle(void* dptr, void* handle_out /* 64 bytes */);
 int gtk_ipc_open_handle(const void* handle /* 64 bytes */, void** dptr_out);
 int gtk_ipc_close_handle(void* dptr);
+/* Abort word of a device group (replaces the reference's cluster abort,
+ * transport.py:210-214, :246-248): pinned host memory mapped into the device
+ * address space.  gtk_abort_word_set(host, 1) while an exchange kernel waits
+ * makes it stop polling within microseconds, OR GTK_DEV_ABORTED into its
+ * status word and skip K3 -- the step then raises TransportError("cluster
+ * aborted") instead of waiting out its timeout.  dev_ptr is the d_abort
+ * argument of the exchange calls. */
+int gtk_abort_word_create(uint32_t** host_ptr, uint32_t** dev_ptr);
+int gtk_abort_word_set(uint32_t* host_ptr, uint32_t value);
+int gtk_abort_word_destroy(uint32_t* host_ptr);
 /*  d_epoch: device uint64 call counter, zero-initialised, advanced by the
  *         kernel itself (so the launch can be captured in a CUDA graph and
  *         replayed); it stays identical on every rank.
@@ -221,9 +246,9 @@ int gtk_ipc_close_handle(void* dptr);
  *  in_*: optional input list; when given the kernel first copies it into acc
  *         (so the caller's local selection stays intact for K3).
  *  ws: a merge workspace of gtk_merge_workspace_bytes(k, k) bytes.
- *  d_abort: optional (host-mapped) flag polled while waiting. */
+ *  d_abort: optional abort word (gtk_abort_word_create's dev_ptr) polled while waiting. */
 int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
-                       void* const* peer_inbox, uint64_t* const* peer_flags, uint64_t* d_epoch,
+                       void* const* peer_inbox, uint64_t* d_epoch,
                        int32_t* acc_idx, float* acc_val, int32_t* d_acc_n, int32_t k,
                        uint32_t* d_status, const uint32_t* d_abort, int64_t timeout_ns,
                        int32_t* step_counts, const int32_t* in_idx, const float* in_val,
@@ -239,7 +264,7 @@ int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedule, int32_t
  * required; nsteps > 0 (one rank: gtk_select_update).
  *   d_tags: device uint32[m], zeroed once, owned per exchange plan. */
 int gtk_gtopk_exchange_update(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
-                              void* const* peer_inbox, uint64_t* const* peer_flags, uint64_t* d_epoch,
+                              void* const* peer_inbox, uint64_t* d_epoch,
                               int32_t* acc_idx, float* acc_val, int32_t* d_acc_n, int32_t k,
                               uint32_t* d_status, const uint32_t* d_abort, int64_t timeout_ns,
                               int32_t* step_counts, const int32_t* in_idx, const float* in_val,

@@ -31,6 +31,7 @@ DEV_PEER_FAILED = 0x10
 DEV_ERROR_MASK = 0x1D
 
 SELECT_FORCE_EXACT = 0x1
+SELECT_CHAIN = 0x2
 STEP_PREPUSHED = 0x10000
 
 # every symbol include/gtopk_b200.h declares (checked by tests/test_capi.py)
@@ -45,21 +46,23 @@ EXPORTS = (
     "gtk_select_update",
     "gtk_select_push",
     "gtk_select_main_pass",
+    "gtk_select_settle",
     "gtk_merge_workspace_bytes",
     "gtk_top_op",
-    "gtk_update_workspace_bytes",
     "gtk_scatter_update",
     "gtk_dense_apply",
     "gtk_densify",
     "gtk_topk_accumulate",
     "gtk_dense_sum",
     "gtk_exchange_inbox_bytes",
-    "gtk_exchange_flags_bytes",
     "gtk_dev_alloc",
     "gtk_dev_free",
     "gtk_ipc_get_handle",
     "gtk_ipc_open_handle",
     "gtk_ipc_close_handle",
+    "gtk_abort_word_create",
+    "gtk_abort_word_set",
+    "gtk_abort_word_destroy",
     "gtk_gtopk_exchange",
     "gtk_gtopk_exchange_update",
     "gtk_prof_enable",
@@ -88,11 +91,11 @@ _SIGS = {
     "gtk_select_update": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _I32, _P, _P, _F, _I32, _I32, _P], _I32),
     "gtk_select_push": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _I32, _P, _P, _P, _P], _I32),
     "gtk_select_main_pass": ([_P, _P, _P, _I64, _I32, _P, _SZ, _I32, _P], _I32),
+    "gtk_select_settle": ([_P, _P, _P, _P, _P], _I32),
     "gtk_merge_workspace_bytes": ([_I32, _I32, ctypes.POINTER(_SZ)], _I32),
     "gtk_top_op": ([_P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _SZ, _P], _I32),
-    "gtk_update_workspace_bytes": ([_I64, ctypes.POINTER(_SZ)], _I32),
     "gtk_scatter_update": (
-        [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _F, _F, _I32, _I32, _P, _P, _SZ, _P],
+        [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _F, _F, _I32, _I32, _P, _P],
         _I32,
     ),
     "gtk_dense_apply": ([_P, _P, _P, _I64, _F, _F, _I32, _P], _I32),
@@ -100,18 +103,21 @@ _SIGS = {
     "gtk_topk_accumulate": ([_P, _P, _P, _I32, _I64, _I64, _P, _I32, _P], _I32),
     "gtk_dense_sum": ([_P, _I32, _I64, _P, _P], _I32),
     "gtk_exchange_inbox_bytes": ([_I32, _I32, ctypes.POINTER(_SZ)], _I32),
-    "gtk_exchange_flags_bytes": ([_I32, ctypes.POINTER(_SZ)], _I32),
     "gtk_dev_alloc": ([_SZ, ctypes.POINTER(_P)], _I32),
     "gtk_dev_free": ([_P], _I32),
     "gtk_ipc_get_handle": ([_P, _P], _I32),
     "gtk_ipc_open_handle": ([_P, ctypes.POINTER(_P)], _I32),
     "gtk_ipc_close_handle": ([_P], _I32),
+    "gtk_abort_word_create": ([ctypes.POINTER(ctypes.POINTER(ctypes.c_uint32)),
+                               ctypes.POINTER(ctypes.POINTER(ctypes.c_uint32))], _I32),
+    "gtk_abort_word_set": ([ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint32], _I32),
+    "gtk_abort_word_destroy": ([ctypes.POINTER(ctypes.c_uint32)], _I32),
     "gtk_gtopk_exchange": (
-        [_I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P],
+        [_I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P],
         _I32,
     ),
     "gtk_gtopk_exchange_update": (
-        [_I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P, _P, _F,
+        [_I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P, _P, _F,
          _I32, _P, _P],
         _I32,
     ),

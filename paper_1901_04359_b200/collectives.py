@@ -14,8 +14,9 @@ The three aggregation paths keep their reference semantics and accounting:
 * dense_ring_allreduce -- elementwise sum (:88-128); within rtol 1e-4 of the
                        sequential sum, bitwise identical on all ranks.
 
-Byte-level helpers (allgather, binomial_bcast) keep the reference's host
-algorithms over Endpoint.send/recv.
+Byte-level helpers (allgather, binomial_bcast) run the reference's ring and
+binomial message patterns over Endpoint.send/recv (the accounting depends on
+them).
 """
 
 from __future__ import annotations
@@ -227,7 +228,10 @@ def gtopk_allreduce(ep: Endpoint, local, k: int, P: int | None = None) -> GTopKR
         i, v = out.to_host()
         g = SparseVector(local.dim, i, v)
         return GTopKResult(g, IndexMask.from_indices(local.dim, g.indices))
-    dsv = DeviceSparseVector(out)
+    # a fresh list per rank and call, like the reference's decode
+    # (collectives.py:216-219): the exchange plan's accumulator (and the
+    # in-process leader's list, shared by every rank) is reused by later calls
+    dsv = DeviceSparseVector(out.clone(cap=k))
     return GTopKResult(dsv, _LazyDeviceMask(dsv))
 
 
@@ -329,7 +333,10 @@ def rank_order_sparse_sum(ep: Endpoint, local):
 # ---------------------------------------------------------------------------
 
 
-def _local_dense_leader(ops):
+def _local_dense_leader(ops, ring_stats=True):
+    """Rank-ordered sum of every rank's dense vector (one kernel).  Accounting:
+    the ring allreduce's 2(P-1) chunk messages (collectives.py:101-126), or
+    with ring_stats=False the allgather of whole vectors (optimizer.py:108-115)."""
     P = len(ops)
     m = ops[0][1].numel()
     for _ep, g in ops:
@@ -339,12 +346,12 @@ def _local_dense_leader(ops):
             )
     out = torch.empty(m, dtype=torch.float32, device=ops[0][1].device)
     _dev.dense_sum([g for _ep, g in ops], m, out)
-    chunk = -(-m // P)
+    msgs, nbytes = (2 * (P - 1), 4 * -(-m // P)) if ring_stats else (P - 1, 4 * m)
     for ep_r, _g in ops:
-        ep_r.stats.msgs_sent += 2 * (P - 1)
-        ep_r.stats.msgs_recv += 2 * (P - 1)
-        ep_r.stats.bytes_sent += 2 * (P - 1) * chunk * 4
-        ep_r.stats.bytes_recv += 2 * (P - 1) * chunk * 4
+        ep_r.stats.msgs_sent += msgs
+        ep_r.stats.msgs_recv += msgs
+        ep_r.stats.bytes_sent += msgs * nbytes
+        ep_r.stats.bytes_recv += msgs * nbytes
     return out
 
 
@@ -376,39 +383,74 @@ def dense_ring_allreduce(ep: Endpoint, g):
     return out if on_device else out.cpu().numpy()
 
 
+def rank_order_dense_sum(ep: Endpoint, g):
+    """optimizer.py:105-115 (_rank_order_dense_sum): every rank's dense vector
+    gathered and accumulated from +0 in rank order 0..P-1 -- the summation
+    order of topk_allreduce, so k = m trajectories compare bitwise.  Host
+    input -> numpy; device input -> CUDA tensor (identical on every rank)."""
+    on_device = isinstance(g, torch.Tensor) and g.is_cuda
+    group = ep.group
+    gh = None if on_device else as_dense(g)
+    if hasattr(group, "dense_rank_order"):
+        dev = group.device
+        gd = g.contiguous().to(torch.float32) if on_device else torch.from_numpy(np.ascontiguousarray(gh)).to(dev)
+        out = group.dense_rank_order(ep, gd)
+    else:
+        dev = _group_device(ep)
+        gd = g.contiguous().to(torch.float32) if on_device else torch.from_numpy(np.ascontiguousarray(gh)).to(dev)
+        out = group.run(ep.rank, (ep, gd), lambda ops: _local_dense_leader(ops, ring_stats=False))
+    return out if on_device else out.cpu().numpy()
+
+
 # ---------------------------------------------------------------------------
-# byte-level helpers (host; the reference's own algorithms)
+# byte-level helpers (host; the reference's message patterns)
 # ---------------------------------------------------------------------------
+
+
+def _ring_allgather_plan(rank: int, P: int):
+    """Step s of the ring: forward block (rank - s) to the right neighbour,
+    receive block (rank - s - 1) from the left one (collectives.py:138-144)."""
+    return [(s, (rank - s) % P, (rank - s - 1) % P) for s in range(P - 1)]
 
 
 def allgather(ep: Endpoint, payload: bytes) -> list[bytes]:
-    """collectives.py:131-145 -- ring pass; payloads indexed by source rank."""
-    P = ep.world_size
-    blocks: list = [None] * P
-    blocks[ep.rank] = bytes(payload)
-    if P == 1:
-        return [blocks[ep.rank]]
-    right, left = (ep.rank + 1) % P, (ep.rank - 1) % P
-    for step in range(P - 1):
-        ep.send(right, _TAG_GATHER + step, blocks[(ep.rank - step) % P])
-        blocks[(ep.rank - step - 1) % P] = ep.recv(left, _TAG_GATHER + step)
-    return blocks
+    """collectives.py:131-145 -- every rank's payload, indexed by source rank,
+    in P - 1 ring steps (P - 1 messages sent and received per rank)."""
+    P, me = ep.world_size, ep.rank
+    right, left = (me + 1) % P, (me - 1) % P
+    have = {me: bytes(payload)}
+    for step, fwd, want in _ring_allgather_plan(me, P):
+        ep.send(right, _TAG_GATHER + step, have[fwd])
+        have[want] = ep.recv(left, _TAG_GATHER + step)
+    return [have[r] for r in range(P)]
+
+
+def _binomial_plan(rel: int, P: int):
+    """(round j, peer offset, sends?) of a binomial broadcast for the rank at
+    distance `rel` from the root: in round j the ranks that already hold the
+    payload (rel < 2^(j-1)) forward it 2^(j-1) further (collectives.py:176-184)."""
+    plan = []
+    for j in range(1, ceil_log2(P) + 1):
+        half = 1 << (j - 1)
+        if rel < half and rel + half < P:
+            plan.append((j, half, True))
+        elif half <= rel < 2 * half:
+            plan.append((j, -half, False))
+    return plan
 
 
 def binomial_bcast(ep: Endpoint, root: int, payload: bytes | None) -> bytes:
-    """collectives.py:168-185 -- root's payload to all in ⌈log2 P⌉ rounds."""
+    """collectives.py:168-185 -- the root's payload on every rank after
+    ceil(log2 P) rounds."""
     P = ep.world_size
     rel = (ep.rank - root) % P
     if rel == 0 and payload is None:
         raise ValueError("root must supply the payload")
-    if P == 1:
-        return bytes(payload)
-    buf = bytes(payload) if rel == 0 else b""
-    for j in range(1, ceil_log2(P) + 1):
-        half = 1 << (j - 1)
-        if rel < half:
-            if rel + half < P:
-                ep.send((rel + half + root) % P, _TAG_BCAST + j, buf)
-        elif rel < 2 * half:
-            buf = ep.recv((rel - half + root) % P, _TAG_BCAST + j)
-    return buf
+    data = bytes(payload) if rel == 0 else b""
+    for j, off, sends in _binomial_plan(rel, P):
+        peer = (root + rel + off) % P
+        if sends:
+            ep.send(peer, _TAG_BCAST + j, data)
+        else:
+            data = ep.recv(peer, _TAG_BCAST + j)
+    return data

@@ -50,12 +50,11 @@ struct ExchangeArgs {
   uint64_t* d_epoch;  // device call counter (identical on every rank): graph-replay safe
   Step steps[kMaxSteps];
   char* inbox[kMaxRanks];     // peer-mapped inbox bases (index = rank)
-  uint64_t* flags[kMaxRanks]; // peer-mapped flag arrays
   int32_t* acc_idx;
   float* acc_val;
   int32_t* d_acc_n;
   uint32_t* d_status;
-  const volatile uint32_t* d_abort;
+  const uint32_t* d_abort;  // host-mapped abort word (nullable)
   int64_t timeout_ns;
   int32_t* step_counts;  // [nsteps][2] (sent, received) entry counts, for stats
   int64_t* trace;        // optional %globaltimer phase stamps (block 0), see gtk_exchange_set_trace
@@ -104,7 +103,6 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   // after the final grid barrier)
   const uint64_t epoch = __ldcg((const unsigned long long*)a.d_epoch) + 1;
   const uint32_t par = (uint32_t)(epoch & 1u);
-  const uint64_t target = epoch * (uint64_t)G;
   // poison: a rank whose select failed (non-finite input) still runs every
   // step so no peer hangs, but sends count = -1; receivers flag PEER_FAILED
   // and forward the poison, so every rank fails the step and K3 is skipped.
@@ -321,9 +319,33 @@ extern "C" int gtk_exchange_inbox_bytes(int32_t k, int32_t nsteps, size_t* bytes
   return GTK_OK;
 }
 
-extern "C" int gtk_exchange_flags_bytes(int32_t nsteps, size_t* bytes) {
-  if (!bytes || nsteps < 0 || nsteps > kMaxSteps) return GTK_EINVAL;
-  *bytes = sizeof(uint64_t) * (size_t)(nsteps > 0 ? nsteps : 1);
+// abort word of a device group: pinned host memory mapped into the device's
+// address space, so the host sets it while an exchange kernel polls it
+extern "C" int gtk_abort_word_create(uint32_t** host_ptr, uint32_t** dev_ptr) {
+  if (!host_ptr || !dev_ptr) return GTK_EINVAL;
+  void* h = nullptr;
+  GTK_CUDA(cudaHostAlloc(&h, sizeof(uint32_t), cudaHostAllocMapped | cudaHostAllocPortable));
+  *(volatile uint32_t*)h = 0u;
+  void* d = nullptr;
+  const cudaError_t e = cudaHostGetDevicePointer(&d, h, 0);
+  if (e != cudaSuccess) {
+    cudaFreeHost(h);
+    set_last_cuda_error(e);
+    return GTK_ECUDA;
+  }
+  *host_ptr = (uint32_t*)h;
+  *dev_ptr = (uint32_t*)d;
+  return GTK_OK;
+}
+
+extern "C" int gtk_abort_word_set(uint32_t* host_ptr, uint32_t value) {
+  if (!host_ptr) return GTK_EINVAL;
+  __atomic_store_n(host_ptr, value, __ATOMIC_SEQ_CST);
+  return GTK_OK;
+}
+
+extern "C" int gtk_abort_word_destroy(uint32_t* host_ptr) {
+  if (host_ptr) GTK_CUDA(cudaFreeHost(host_ptr));
   return GTK_OK;
 }
 
@@ -363,25 +385,25 @@ extern "C" int gtk_ipc_close_handle(void* dptr) {
 }
 
 static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps, void* const* peer_inbox,
-                         uint64_t* const* peer_flags, uint64_t* d_epoch, int32_t* acc_idx, float* acc_val,
+                         uint64_t* d_epoch, int32_t* acc_idx, float* acc_val,
                          int32_t* d_acc_n, int32_t k, uint32_t* d_status, const uint32_t* d_abort,
                          int64_t timeout_ns, int32_t* step_counts, const int32_t* in_idx, const float* in_val,
                          const int32_t* d_in_n, void* ws, size_t ws_bytes, float* upd_w, float* upd_res,
                          float upd_lr, int32_t upd_scaling, uint32_t* upd_tags, void* stream);
 
 extern "C" int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
-                                  void* const* peer_inbox, uint64_t* const* peer_flags, uint64_t* d_epoch,
+                                  void* const* peer_inbox, uint64_t* d_epoch,
                                   int32_t* acc_idx, float* acc_val, int32_t* d_acc_n, int32_t k,
                                   uint32_t* d_status, const uint32_t* d_abort, int64_t timeout_ns,
                                   int32_t* step_counts, const int32_t* in_idx, const float* in_val,
                                   const int32_t* d_in_n, void* ws, size_t ws_bytes, void* stream) {
-  return exchange_impl(rank, P, schedule, nsteps, peer_inbox, peer_flags, d_epoch, acc_idx, acc_val, d_acc_n, k,
+  return exchange_impl(rank, P, schedule, nsteps, peer_inbox, d_epoch, acc_idx, acc_val, d_acc_n, k,
                        d_status, d_abort, timeout_ns, step_counts, in_idx, in_val, d_in_n, ws, ws_bytes, nullptr,
                        nullptr, 0.0f, 0, nullptr, stream);
 }
 
 extern "C" int gtk_gtopk_exchange_update(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
-                                         void* const* peer_inbox, uint64_t* const* peer_flags, uint64_t* d_epoch,
+                                         void* const* peer_inbox, uint64_t* d_epoch,
                                          int32_t* acc_idx, float* acc_val, int32_t* d_acc_n, int32_t k,
                                          uint32_t* d_status, const uint32_t* d_abort, int64_t timeout_ns,
                                          int32_t* step_counts, const int32_t* in_idx, const float* in_val,
@@ -390,13 +412,13 @@ extern "C" int gtk_gtopk_exchange_update(int32_t rank, int32_t P, const int32_t*
   if (!w || !res || !in_idx || !d_tags || scaling < 0 || scaling > 2 || !std::isfinite(lr) || std::signbit(lr))
     return GTK_EINVAL;
   if (nsteps == 0) return GTK_EINVAL;  // one rank: gtk_select_update
-  return exchange_impl(rank, P, schedule, nsteps, peer_inbox, peer_flags, d_epoch, acc_idx, acc_val, d_acc_n, k,
+  return exchange_impl(rank, P, schedule, nsteps, peer_inbox, d_epoch, acc_idx, acc_val, d_acc_n, k,
                        d_status, d_abort, timeout_ns, step_counts, in_idx, in_val, d_in_n, ws, ws_bytes, w, res, lr,
                        scaling, d_tags, stream);
 }
 
 static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps, void* const* peer_inbox,
-                         uint64_t* const* peer_flags, uint64_t* d_epoch, int32_t* acc_idx, float* acc_val,
+                         uint64_t* d_epoch, int32_t* acc_idx, float* acc_val,
                          int32_t* d_acc_n, int32_t k, uint32_t* d_status, const uint32_t* d_abort,
                          int64_t timeout_ns, int32_t* step_counts, const int32_t* in_idx, const float* in_val,
                          const int32_t* d_in_n, void* ws, size_t ws_bytes, float* upd_w, float* upd_res,
@@ -404,7 +426,7 @@ static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32
   if (P < 1 || P > kMaxRanks || rank < 0 || rank >= P || nsteps < 0 || nsteps > kMaxSteps || k < 1)
     return GTK_EINVAL;
   if (!acc_idx || !acc_val || !d_acc_n || !d_status || !ws || !d_epoch) return GTK_EINVAL;
-  if (nsteps > 0 && (!schedule || !peer_inbox || !peer_flags)) return GTK_EINVAL;
+  if (nsteps > 0 && (!schedule || !peer_inbox)) return GTK_EINVAL;
   const MergeLayout L = merge_layout(k);
   if (ws_bytes < L.total) return GTK_ENOMEM;
   if (nsteps == 0) return GTK_OK;
@@ -420,15 +442,12 @@ static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32
     if ((a.steps[s].tag & kStepPrepushed) && (s != 0 || a.steps[s].send_to < 0)) return GTK_EINVAL;
     if (a.steps[s].send_to >= P || a.steps[s].recv_from >= P) return GTK_EINVAL;
   }
-  for (int r = 0; r < P; ++r) {
-    a.inbox[r] = (char*)peer_inbox[r];
-    a.flags[r] = peer_flags[r];
-  }
+  for (int r = 0; r < P; ++r) a.inbox[r] = (char*)peer_inbox[r];
   a.acc_idx = acc_idx;
   a.acc_val = acc_val;
   a.d_acc_n = d_acc_n;
   a.d_status = d_status;
-  a.d_abort = (const volatile uint32_t*)d_abort;
+  a.d_abort = d_abort;
   a.timeout_ns = timeout_ns;
   a.step_counts = step_counts;
   a.trace = trace_buffer();

@@ -143,10 +143,15 @@ constexpr int32_t kStepPrepushed = 0x10000;  // schedule flag: step 0's send was
 struct LLPoll {
   uint64_t deadline;  // %globaltimer ns; 0 = none
   uint32_t* status;
-  const volatile uint32_t* abort;
+  const uint32_t* abort;  // host-mapped abort word (gtk_abort_word_create), nullable
 };
-static __device__ __noinline__ bool ll_wait_failed(const LLPoll& c) {
-  if (c.abort && *c.abort) {
+__device__ __forceinline__ uint32_t ld_relaxed_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+static __device__ __noinline__ bool ll_wait_failed(const LLPoll c) {
+  if (c.abort && ld_relaxed_sys_u32(c.abort)) {
     atomicOr(c.status, 0x8u);  // GTK_DEV_ABORTED
     return true;
   }

@@ -49,6 +49,12 @@ struct EngineWS {
 
 constexpr uint32_t kKeptBits = 32768;  // slice slots covered by the kept bitmap (a finish slice is <= 20480)
 constexpr uint32_t kSlotBits = 22;    // gather record: (block << 22) | slot within the block's slice
+// slots past kSlotMax (a dense-fallback slice of m > ~600M elements) are
+// recorded as kSlotMax: any slot >= kKeptBits is resolved by index (keep_fn's
+// scan), so only the block field must stay exact; kSlotMax < 2^22 - 1 keeps
+// the record of block 1023 distinct from the "not kept" mark 0xFFFFFFFF
+constexpr uint32_t kSlotMax = (1u << kSlotBits) - 2;
+static_assert(kKeptBits <= kSlotMax, "kept bitmap beyond the slot field");
 
 template <int NT>
 struct EngineSmem {
@@ -125,7 +131,24 @@ struct Sink {
   uint64_t* ll_body = nullptr;
   uint64_t* ll_head = nullptr;
   uint32_t ll_tag = 0;
+  // chained select (GTK_SELECT_CHAIN): the winners' residual slots are left
+  // pending instead of zeroed; the exact winner predicate goes to the key
+  // window record: rec[6] = tau (the k-th key), rec[7] = cut (the largest
+  // index among the kept entries with key == tau), rec[0] |= kRecPending --
+  // i is a winner iff key > tau || (key == tau && i <= cut) (nullable)
+  uint32_t* pend_rec = nullptr;
 };
+
+constexpr uint32_t kRecValid = 0x1u;    // window record word 0: lo/shift/k describe the next call's window
+constexpr uint32_t kRecPending = 0x2u;  // ... the residual still holds the last chained call's winners
+
+// block 0, thread 0, after the write: the pending-winner predicate (chained select)
+__device__ __forceinline__ void sink_pending(const Sink& out, uint32_t tau) {
+  if (out.pend_rec) {
+    out.pend_rec[6] = tau;
+    out.pend_rec[0] = out.pend_rec[0] | kRecPending;
+  }
+}
 
 // block 0 publishes the output count (and the k-th-key hint)
 __device__ __forceinline__ void sink_count(const Sink& out, uint32_t n, uint32_t hint) {
@@ -452,7 +475,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
         out.next_window[3] = kt;
         out.next_window[4] = tau_n;
         out.next_window[5] = p1;
-        out.next_window[0] = 1u | (out.window_level << 8);
+        out.next_window[0] = kRecValid | (out.window_level << 8);
       }
     } else if (!engine_find_bin<NT>(hist, hsm, t, sm, bin, above, in_bin)) {
       return false;
@@ -504,11 +527,11 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
           if (solo) {
             sm.keys[p] = key;
             sm.gidx[p] = i;
-            sm.gblk[p] = (blk << kSlotBits) | (s - s0);
+            sm.gblk[p] = (blk << kSlotBits) | min(s - s0, kSlotMax);
           } else {
             ws->gather_key[p] = key;
             ws->gather_idx[p] = i;
-            ws->gather_blk[p] = (blk << kSlotBits) | (s - s0);
+            ws->gather_blk[p] = (blk << kSlotBits) | min(s - s0, kSlotMax);
           }
         }
       }
@@ -604,6 +627,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
           const int32_t ij = sm.gidx[j];
           for (uint32_t q = 0; q < n_eq; ++q) rank += (int32_t)sm.hist[q] < ij;
           kept = rank < need;
+          if (out.pend_rec && blk == 0 && rank + 1 == need) out.pend_rec[7] = (uint32_t)ij;  // the last kept tie
         }
         const uint32_t gb = sm.gblk[j] >> kSlotBits, slot = sm.gblk[j] & ((1u << kSlotBits) - 1);
         if (kept) {
@@ -631,7 +655,10 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       if (blk == 0) {  // every block is past its last histogram read
         for (int rr = 0; rr < kRounds; ++rr)
           for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[rr][b] = 0;
-        if (threadIdx.x == 0) sink_count(out, kt, tau);
+        if (threadIdx.x == 0) {
+          sink_count(out, kt, tau);
+          sink_pending(out, tau);
+        }
       }
       return true;
     }
@@ -678,6 +705,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
         uint32_t eq_tot;
         const uint32_t eq_rank = block_excl_scan<NT>(is_eq, sm.scan, &eq_tot);
         if (is_eq && eq_seen + eq_rank < need) keep = true;
+        if (is_eq && eq_seen + eq_rank + 1 == need && out.pend_rec) out.pend_rec[7] = (uint32_t)i;  // the last kept tie
         uint32_t k_tot;
         const uint32_t k_rank = block_excl_scan<NT>(keep ? 1u : 0u, sm.scan, &k_tot);
         if (keep) sink_put(out, out_pos + k_rank, i, v);
@@ -687,7 +715,10 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       if (blk == 0) {
         for (int rr = 0; rr < kRounds; ++rr)
           for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[rr][b] = 0;
-        if (threadIdx.x == 0) sink_count(out, kt, tau);
+        if (threadIdx.x == 0) {
+          sink_count(out, kt, tau);
+          sink_pending(out, tau);
+        }
       }
       return true;
     }

@@ -9,7 +9,7 @@
 
 namespace gtk {
 
-__global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs a) {
+__global__ void __launch_bounds__(kMergeThreads, 1) merge_kernel(MergeArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   MergeSmem& S = *reinterpret_cast<MergeSmem*>(dsm);
   const uint32_t na = (uint32_t)__ldcg(a.d_na), nb = (uint32_t)__ldcg(a.d_nb);

@@ -30,7 +30,7 @@ constexpr int kMergeSub = 2048;        // merged slots staged per sub-chunk
 constexpr int kMergeSlotsPerBlock = 512;  // grid sizing target
 constexpr int kMergeSliceCap = 4096;   // slice slots kept in shared memory (minimum)
 constexpr int kMergeSliceCapMax = 20480;  // ... up to 160 KB of dynamic smem at large k
-constexpr int kMergeMaxSplits = 65;    // sub-chunk boundaries per block (slice <= 128K)
+constexpr int kMergeMaxSplits = 65;    // sub-chunk boundaries staged per group (64 sub-chunks = 128K slots)
 
 struct MergeCtl {
   uint32_t n_valid;
@@ -269,106 +269,111 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   int32_t* const slice_idx = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(&S) + kMergeSmemFixed);
   float* const slice_val = reinterpret_cast<float*>(slice_idx + a.slice_cap);
   const uint32_t nsub = (L + kMergeSub - 1) / kMergeSub;
-  // all sub-chunk boundaries of the slice, one warp each, in parallel
   merge_stamp(a, 0);
-  for (uint32_t j = warp_id(); j <= nsub; j += kMergeThreads / 32) {
-    const uint32_t d = min(d1, d0 + j * kMergeSub);
-    const uint32_t i = merge_path_warp(a, na, a.b_idx, nb, d);
-    if (lane_id() == 0) S.split[j] = i;
-  }
-  __syncthreads();
-  merge_stamp(a, 1);  // merge-path splits known
   uint32_t my_valid = 0;
-  for (uint32_t j = 0; j < nsub; ++j) {
-    const uint32_t sub = d0 + j * kMergeSub, sub_end = min(d1, sub + kMergeSub);
-    const uint32_t ia = S.split[j], ib = S.split[j + 1];
-    const uint32_t ja = sub - ia, jb = sub_end - ib;
-    const uint32_t la = ib - ia, lb = jb - ja;
-    // the neighbours across the sub-chunk edges go out first (an LL record of
-    // A is only checked after the staging loads: no extra round trip)
-    uint64_t pax = 0, pay = 0;
-    int32_t prevA = -1;
-    if (ia > 0) {
-      if (a.a_ll) ld_ll_pair_raw(a.a_ll + 2 * (size_t)(ia - 1), pax, pay);
-      else prevA = __ldcg(a.a_idx + ia - 1);
-    }
-    const int32_t nextB = jb < nb ? __ldcg(a.b_idx + jb) : -1;
-    const float nextBv = jb < nb ? __ldcg(a.b_val + jb) : 0.0f;
-    // stage A[ia, ib) and B[ja, jb): every load of the sub-chunk in flight at once
-    for (uint32_t base = 0; base < la + lb; base += 4 * kMergeThreads) {
-      int32_t ri[4];
-      float rv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t t = base + u * kMergeThreads + threadIdx.x;
-        if (t < la) {
-          a_entry(a, ia + t, ri[u], rv[u]);
-        } else if (t < la + lb) {
-          ri[u] = __ldcg(a.b_idx + ja + (t - la));
-          rv[u] = __ldcg(a.b_val + ja + (t - la));
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t t = base + u * kMergeThreads + threadIdx.x;
-        if (t < la) {
-          S.sAi[t] = ri[u];
-          S.sAv[t] = rv[u];
-        } else if (t < la + lb) {
-          S.sBi[t - la] = ri[u];
-          S.sBv[t - la] = rv[u];
-        }
-      }
-    }
-    if (ia > 0 && a.a_ll)
-      prevA = ((uint32_t)(pax >> 32) == a.a_tag && (uint32_t)(pay >> 32) == a.a_tag) ? (int32_t)(uint32_t)pax
-                                                                                      : a_index(a, ia - 1);
-    __syncthreads();
-    for (uint32_t t = threadIdx.x; t < la; t += kMergeThreads) {
-      const int32_t x = S.sAi[t];
-      const uint32_t r = lower_bound_s(S.sBi, lb, x);
-      float v = S.sAv[t];
-      if (r < lb) {
-        if (S.sBi[r] == x) v = add_x86(v, S.sBv[r]);
-      } else if (nextB == x) {
-        v = add_x86(v, nextBv);
-      }
-      const uint32_t slot = sub + t + r;
-      const bool valid = v != 0.0f;
-      if (in_smem) {
-        slice_idx[slot - d0] = valid ? x : -1;
-        slice_val[slot - d0] = v;
-      } else {
-        a.u_idx[slot] = valid ? x : -1;
-        a.u_val[slot] = v;
-      }
-      if (valid) {
-        ++my_valid;
-        const uint32_t key = merge_key_of(v);
-        if (key >= win_lo) atomicAdd(&esm.hist[min((uint32_t)kBins, (key - win_lo) >> win_shift)], 1u);
-      }
-    }
-    for (uint32_t t = threadIdx.x; t < lb; t += kMergeThreads) {
-      const int32_t x = S.sBi[t];
-      const uint32_t r = upper_bound_s(S.sAi, la, x);
-      const bool dup = r > 0 ? (S.sAi[r - 1] == x) : (prevA == x);
-      const float v = S.sBv[t];
-      const uint32_t slot = sub + t + r;
-      const bool valid = !dup && v != 0.0f;
-      if (in_smem) {
-        slice_idx[slot - d0] = valid ? x : -1;
-        slice_val[slot - d0] = v;
-      } else {
-        a.u_idx[slot] = valid ? x : -1;
-        a.u_val[slot] = v;
-      }
-      if (valid) {
-        ++my_valid;
-        const uint32_t key = merge_key_of(v);
-        if (key >= win_lo) atomicAdd(&esm.hist[min((uint32_t)kBins, (key - win_lo) >> win_shift)], 1u);
-      }
+  // sub-chunks in groups of kMergeMaxSplits - 1: all boundaries of a group,
+  // one warp each, in parallel, then the group's union slots (any slice size)
+  for (uint32_t j0 = 0; j0 < nsub; j0 += kMergeMaxSplits - 1) {
+    const uint32_t jn = min(nsub - j0, (uint32_t)kMergeMaxSplits - 1);
+    for (uint32_t j = warp_id(); j <= jn; j += kMergeThreads / 32) {
+      const uint32_t d = min(d1, d0 + (j0 + j) * kMergeSub);
+      const uint32_t i = merge_path_warp(a, na, a.b_idx, nb, d);
+      if (lane_id() == 0) S.split[j] = i;
     }
     __syncthreads();
+    if (j0 == 0) merge_stamp(a, 1);  // merge-path splits known
+    for (uint32_t jj = 0; jj < jn; ++jj) {
+      const uint32_t j = j0 + jj;
+      const uint32_t sub = d0 + j * kMergeSub, sub_end = min(d1, sub + kMergeSub);
+      const uint32_t ia = S.split[jj], ib = S.split[jj + 1];
+      const uint32_t ja = sub - ia, jb = sub_end - ib;
+      const uint32_t la = ib - ia, lb = jb - ja;
+      // the neighbours across the sub-chunk edges go out first (an LL record of
+      // A is only checked after the staging loads: no extra round trip)
+      uint64_t pax = 0, pay = 0;
+      int32_t prevA = -1;
+      if (ia > 0) {
+        if (a.a_ll) ld_ll_pair_raw(a.a_ll + 2 * (size_t)(ia - 1), pax, pay);
+        else prevA = __ldcg(a.a_idx + ia - 1);
+      }
+      const int32_t nextB = jb < nb ? __ldcg(a.b_idx + jb) : -1;
+      const float nextBv = jb < nb ? __ldcg(a.b_val + jb) : 0.0f;
+      // stage A[ia, ib) and B[ja, jb): every load of the sub-chunk in flight at once
+      for (uint32_t base = 0; base < la + lb; base += 4 * kMergeThreads) {
+        int32_t ri[4];
+        float rv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t t = base + u * kMergeThreads + threadIdx.x;
+          if (t < la) {
+            a_entry(a, ia + t, ri[u], rv[u]);
+          } else if (t < la + lb) {
+            ri[u] = __ldcg(a.b_idx + ja + (t - la));
+            rv[u] = __ldcg(a.b_val + ja + (t - la));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t t = base + u * kMergeThreads + threadIdx.x;
+          if (t < la) {
+            S.sAi[t] = ri[u];
+            S.sAv[t] = rv[u];
+          } else if (t < la + lb) {
+            S.sBi[t - la] = ri[u];
+            S.sBv[t - la] = rv[u];
+          }
+        }
+      }
+      if (ia > 0 && a.a_ll)
+        prevA = ((uint32_t)(pax >> 32) == a.a_tag && (uint32_t)(pay >> 32) == a.a_tag) ? (int32_t)(uint32_t)pax
+                                                                                        : a_index(a, ia - 1);
+      __syncthreads();
+      for (uint32_t t = threadIdx.x; t < la; t += kMergeThreads) {
+        const int32_t x = S.sAi[t];
+        const uint32_t r = lower_bound_s(S.sBi, lb, x);
+        float v = S.sAv[t];
+        if (r < lb) {
+          if (S.sBi[r] == x) v = add_x86(v, S.sBv[r]);
+        } else if (nextB == x) {
+          v = add_x86(v, nextBv);
+        }
+        const uint32_t slot = sub + t + r;
+        const bool valid = v != 0.0f;
+        if (in_smem) {
+          slice_idx[slot - d0] = valid ? x : -1;
+          slice_val[slot - d0] = v;
+        } else {
+          a.u_idx[slot] = valid ? x : -1;
+          a.u_val[slot] = v;
+        }
+        if (valid) {
+          ++my_valid;
+          const uint32_t key = merge_key_of(v);
+          if (key >= win_lo) atomicAdd(&esm.hist[min((uint32_t)kBins, (key - win_lo) >> win_shift)], 1u);
+        }
+      }
+      for (uint32_t t = threadIdx.x; t < lb; t += kMergeThreads) {
+        const int32_t x = S.sBi[t];
+        const uint32_t r = upper_bound_s(S.sAi, la, x);
+        const bool dup = r > 0 ? (S.sAi[r - 1] == x) : (prevA == x);
+        const float v = S.sBv[t];
+        const uint32_t slot = sub + t + r;
+        const bool valid = !dup && v != 0.0f;
+        if (in_smem) {
+          slice_idx[slot - d0] = valid ? x : -1;
+          slice_val[slot - d0] = v;
+        } else {
+          a.u_idx[slot] = valid ? x : -1;
+          a.u_val[slot] = v;
+        }
+        if (valid) {
+          ++my_valid;
+          const uint32_t key = merge_key_of(v);
+          if (key >= win_lo) atomicAdd(&esm.hist[min((uint32_t)kBins, (key - win_lo) >> win_shift)], 1u);
+        }
+      }
+      __syncthreads();
+    }
   }
   my_valid = warp_sum(my_valid);
   if (lane_id() == 0 && my_valid) atomicAdd(&S.s_valid, my_valid);

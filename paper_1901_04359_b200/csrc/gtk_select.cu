@@ -422,7 +422,23 @@ struct MainArgs {
   uint32_t tiles_per_group;
   uint32_t n2;  // blocks [0, n2) take two tiles, the rest one (the last wave is short)
   int64_t* trace = nullptr;  // optional timeline stamps: [0] block 0 start, [1] last block end (max)
+  // key-window record (nullable): its pending-winner predicate (a chained
+  // select left the winners of res in place) is applied to res on the fly;
+  // chained calls (chain = 1) also take the window from it -- there is no
+  // sampling kernel -- and reset the engine's gather counters
+  const uint32_t* window = nullptr;
+  uint32_t k = 0;
+  uint32_t chain = 0;
+  uint32_t force_exact = 0;
+  uint32_t* gather_n = nullptr;
 };
+
+// res with a chained select's pending winners zeroed: the winner predicate of
+// the previous call's exact top-k (gtk_engine.cuh, Sink::pend_rec)
+__device__ __forceinline__ float settle_res(float r, uint64_t i, uint32_t ptau, uint32_t pcut) {
+  const uint32_t kr = key_of(r);
+  return (kr > ptau || (kr == ptau && i <= (uint64_t)pcut)) ? 0.0f : r;
+}
 
 // v[b >> 2][b & 3] without a dynamically indexed (local-memory) array
 __device__ __forceinline__ float pick(const float (&v)[kMainVec][4], int b) {
@@ -550,7 +566,7 @@ __device__ __forceinline__ bool main_tile(const MainArgs& a, uint32_t tile, cons
 }
 
 
-__global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
+__global__ void __launch_bounds__(kMainThreads, 3) select_main_kernel(MainArgs a) {
   __shared__ uint32_t s_wt[2][16];  // per warp: packed candidate totals of the q segments
   __shared__ int32_t* s_didx[2];
   __shared__ float* s_dval[2];
@@ -589,8 +605,33 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
   // a variant without the sample kernel that had to wait before loading res
   // measured 6 us slower per step)
   pdl_wait();
-  const uint32_t lo = __ldcg(&a.ctl->lo);
-  const uint32_t shift = __ldcg(&a.ctl->shift);
+  uint32_t lo, shift;
+  bool pend = false;
+  uint32_t ptau = 0, pcut = 0;
+  if (a.window) {
+    const uint32_t w0 = __ldcg(a.window);
+    pend = a.res != nullptr && (w0 & kRecPending) != 0;
+    ptau = __ldcg(a.window + 6);
+    pcut = __ldcg(a.window + 7);
+    if (a.chain) {
+      const bool valid = !a.force_exact && (w0 & kRecValid) && __ldcg(a.window + 3) == a.k;
+      lo = valid ? __ldcg(a.window + 1) : 0x7FFFFFFFu;  // no window: nothing passes, the finish runs exact
+      shift = valid ? __ldcg(a.window + 2) : 0u;
+      if (blk == 0) {  // the finish's engine counters (used only after this kernel)
+        if (threadIdx.x < (unsigned)kRounds) a.gather_n[threadIdx.x] = 0u;
+        if (threadIdx.x == 0) {
+          a.ctl->lo = lo;
+          a.ctl->shift = shift;
+        }
+      }
+    } else {
+      lo = __ldcg(&a.ctl->lo);
+      shift = __ldcg(&a.ctl->shift);
+    }
+  } else {
+    lo = __ldcg(&a.ctl->lo);
+    shift = __ldcg(&a.ctl->shift);
+  }
   bool any_dense = false;
 #pragma unroll
   for (int u = 0; u < kMainTilesPerBlock; ++u) {
@@ -604,10 +645,18 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
       for (int q = 0; q < kMainVec; ++q) {
         float4 x = gv[u][q];
         if (a.res) {
-          x.x = __fadd_rn(rv[u][q].x, x.x);
-          x.y = __fadd_rn(rv[u][q].y, x.y);
-          x.z = __fadd_rn(rv[u][q].z, x.z);
-          x.w = __fadd_rn(rv[u][q].w, x.w);
+          float4 r = rv[u][q];
+          if (pend) {
+            const uint64_t e = tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4;
+            r.x = settle_res(r.x, e, ptau, pcut);
+            r.y = settle_res(r.y, e + 1, ptau, pcut);
+            r.z = settle_res(r.z, e + 2, ptau, pcut);
+            r.w = settle_res(r.w, e + 3, ptau, pcut);
+          }
+          x.x = __fadd_rn(r.x, x.x);
+          x.y = __fadd_rn(r.y, x.y);
+          x.z = __fadd_rn(r.z, x.z);
+          x.w = __fadd_rn(r.w, x.w);
         }
         st_stream4(a.res_out + tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4, x);
         v[q][0] = x.x;
@@ -624,7 +673,7 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
           float x = 0.0f;
           if (e < a.m) {
             x = a.grad[e];
-            if (a.res) x = __fadd_rn(a.res[e], x);
+            if (a.res) x = __fadd_rn(pend ? settle_res(a.res[e], e, ptau, pcut) : a.res[e], x);
             a.res_out[e] = x;
           }
           v[q][j] = x;
@@ -671,7 +720,7 @@ struct FinishArgs {
   uint32_t* d_status;
   int64_t* trace;  // optional phase stamps (block 0): [0] start [1] scanned [2] copied [3..6] engine
   uint32_t* window;  // nullable: {valid | level << 8, lo, shift, k, tau} for the next call (written here)
-  const uint32_t* group_cnt;  // candidates per block, counted by the main pass
+  uint32_t* group_cnt;  // candidates per block, counted by the main pass (reset here for the next call)
   uint32_t tiles_per_group;
   float* upd_w;      // nullable: fused K3 at P = 1 (gtk_select_update)
   float upd_lr;
@@ -684,7 +733,20 @@ struct FinishArgs {
   uint64_t* ll_base = nullptr;
   const uint64_t* ll_epoch = nullptr;
   uint32_t ll_slot_words = 0;
+  uint32_t chain = 0;  // GTK_SELECT_CHAIN: winners stay pending in res_out (Sink::pend_rec)
 };
+
+// block 0 of the finish, once every block has read them: the main pass's
+// counters start the next call at zero (a chained call has no sampling kernel
+// to reset them)
+__device__ __forceinline__ void reset_select_counters(const FinishArgs& a, unsigned G) {
+  for (unsigned i = threadIdx.x; i < G; i += blockDim.x) a.group_cnt[i] = 0u;
+  if (threadIdx.x == 0) {
+    a.ctl->ovf_cursor = 0u;
+    a.ctl->overflow = 0u;
+    a.ctl->nonfinite = 0u;
+  }
+}
 
 __device__ __forceinline__ void finish_stamp(const FinishArgs& a, int i) {
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -707,8 +769,10 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
   const bool wsame = a.window && blk == 0 && __ldcg(a.window + 3) == a.k;
   const uint32_t wtau = wsame ? __ldcg(a.window + 4) : 0u, wtau2 = wsame ? __ldcg(a.window + 5) : 0u;
   if (__ldcg(&a.ctl->nonfinite)) {
+    grid_sync(&a.ews->bar, G);  // every block has read the counters
     if (blk == 0) {
       for (int b = threadIdx.x; b < kHistLen; b += kFinishThreads) a.ews->hist[0][b] = 0;
+      reset_select_counters(a, G);
       if (threadIdx.x == 0) {
         atomicOr(a.d_status, GTK_DEV_NONFINITE);
         if (a.ll_base) {  // the exchange's first partner learns it at once: count -1 (poisoned)
@@ -716,15 +780,18 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
           st_ll_pair(a.ll_base + (size_t)(tag & 1u) * a.ll_slot_words, 0xFFFFFFFFu, 0u, tag);
         }
         if (a.window) {
-          a.window[0] = wlevel << 8;
+          // the step fails and the state keeps res_in: its pending winners
+          // (a chained predecessor's) stay recorded
+          a.window[0] = (wlevel << 8) | (__ldcg(a.window) & kRecPending);
           a.window[4] = a.window[5] = 0u;
         }
       }
     }
     return;
   }
-  Sink out{a.sel_idx, a.sel_val, a.d_count, a.res_out, true, a.trace ? a.trace + 3 : nullptr,
+  Sink out{a.sel_idx, a.sel_val, a.d_count, a.chain ? nullptr : a.res_out, true, a.trace ? a.trace + 3 : nullptr,
            a.window, wlevel, wtau, wtau2, 1u, a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling};
+  if (a.chain) out.pend_rec = a.window;
   if (a.ll_base) {  // the exchange's step 0 send, straight from the write phase
     const uint32_t tag = (uint32_t)(__ldcg((const unsigned long long*)a.ll_epoch) + 1ull);
     uint64_t* slot = a.ll_base + (size_t)(tag & 1u) * a.ll_slot_words;
@@ -851,6 +918,7 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
                                    /*slice_async=*/true)) {
       if (a.trace && threadIdx.x == 0)  // timeline: last block end (trace_buffer()[114])
         atomicMax((unsigned long long*)a.trace + 66, (unsigned long long)globaltimer_ns());
+      if (blk == 0) reset_select_counters(a, G);  // (the engine's grid barrier is behind every read)
       return;
     }
   }
@@ -883,6 +951,7 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
   dout.window_level = (!overflow && C < a.k) ? min(kMaxWindowLevel, wlevel + 1) : wlevel;
   dout.prev_tau = dout.prev_tau2 = 0u;
   engine_run<kFinishThreads>(dsrc, s0, s1, a.k, false, 0u, 20u, nullptr, false, a.ews, sm, dout, G);
+  if (blk == 0) reset_select_counters(a, G);
 }
 
 }  // namespace gtk
@@ -966,6 +1035,10 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
                        PeerPush push) {
   if (!grad || !res_out || !sel_idx || !sel_val || !d_count || !d_status || !ws) return GTK_EINVAL;
   if (m < 1 || m >= (int64_t(1) << 31) || k < 1 || k > m) return GTK_EINVAL;
+  // a chained call needs the record that carries its window and the pending
+  // winners, and its own output buffer (res_in is read early, before the
+  // previous call's kernels have finished)
+  if ((flags & GTK_SELECT_CHAIN) && (!d_window || res_out == res_in || res_out == grad)) return GTK_EINVAL;
   const SelectLayout L = select_layout(m, k);
   if (ws_bytes < L.total) return GTK_ENOMEM;
   const bool aligned = ((uintptr_t)grad % 16 == 0) && ((uintptr_t)res_out % 16 == 0) &&
@@ -1026,12 +1099,15 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
   const uint32_t tiles_per_group = (L.ntiles + G - 1) / G;
   uint32_t* group_cnt = (uint32_t*)(base + L.group_cnt);
 
+  const bool chain = (flags & GTK_SELECT_CHAIN) != 0;
+  const bool force_exact = (flags & GTK_SELECT_FORCE_EXACT) != 0;
   ProfScope prof_all(kProfSelect, st);
-  SampleArgs sa{res_in, grad, (uint32_t)m, stride, nchunks, r_lo, r_hi,
-                (uint32_t)((flags & GTK_SELECT_FORCE_EXACT) ? 1 : 0), stop, d_window, (uint32_t)k, ctl, ews,
-                group_cnt, trace_buffer() ? trace_buffer() + 64 : nullptr};
-  GTK_CUDA(launch_pdl(select_sample_kernel, dim3(nchunks), dim3(kSampleThreads), 0, st, sa));
-  GTK_CHECK_LAUNCH();
+  if (!chain) {  // a chained call takes its window from the record: no sampling pass
+    SampleArgs sa{res_in, grad, (uint32_t)m, stride, nchunks, r_lo, r_hi, (uint32_t)(force_exact ? 1 : 0), stop,
+                  d_window, (uint32_t)k, ctl, ews, group_cnt, trace_buffer() ? trace_buffer() + 64 : nullptr};
+    GTK_CUDA(launch_pdl(select_sample_kernel, dim3(nchunks), dim3(kSampleThreads), 0, st, sa));
+    GTK_CHECK_LAUNCH();
+  }
 
   MainArgs ma{res_in,
               grad,
@@ -1049,6 +1125,11 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
               ews->hist[0],
               group_cnt,
               tiles_per_group};
+  ma.window = d_window;
+  ma.k = (uint32_t)k;
+  ma.chain = chain ? 1u : 0u;
+  ma.force_exact = force_exact ? 1u : 0u;
+  ma.gather_n = ews->gather_n;
   {
     ProfScope prof_main(kProfSelectMain, st);
     const uint32_t gmain = main_grid(L.ntiles, &ma.n2);
@@ -1087,6 +1168,7 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
                 upd.Pf,
                 upd.scaling,
                 slice_cap};
+  fa.chain = chain ? 1u : 0u;
   if (push.slot0) {
     fa.ll_base = push.slot0;
     fa.ll_epoch = push.epoch;
@@ -1128,5 +1210,20 @@ extern "C" int gtk_select_main_pass(const float* res_in, const float* grad, floa
   GTK_CUDA(cudaMemsetAsync(group_cnt, 0, sizeof(uint32_t) * kMaxBlocks, st));
   GTK_CUDA(cudaMemsetAsync(&ctl->ovf_cursor, 0, sizeof(ctl->ovf_cursor), st));
   GTK_CUDA(cudaMemsetAsync(&ctl->overflow, 0, sizeof(ctl->overflow), st));
+  return GTK_OK;
+}
+
+__global__ void settle_kernel(float* res, const int32_t* sel_idx, const int32_t* d_count, uint32_t* window) {
+  const uint32_t n = (uint32_t)__ldg(d_count);
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
+    res[__ldg(sel_idx + e)] = 0.0f;
+  if (blockIdx.x == 0 && threadIdx.x == 0) window[0] &= ~kRecPending;
+}
+
+extern "C" int gtk_select_settle(float* res, const int32_t* sel_idx, const int32_t* d_count, uint32_t* d_window,
+                                 void* stream) {
+  if (!res || !sel_idx || !d_count || !d_window) return GTK_EINVAL;
+  settle_kernel<<<num_sms(), 256, 0, (cudaStream_t)stream>>>(res, sel_idx, d_count, d_window);
+  GTK_CHECK_LAUNCH();
   return GTK_OK;
 }

@@ -154,19 +154,10 @@ static int grid_for(uint64_t n, int threads) {
 
 using namespace gtk;
 
-extern "C" int gtk_update_workspace_bytes(int64_t m, size_t* bytes) {
-  if (!bytes || m < 1) return GTK_EINVAL;
-  *bytes = 0;
-  return GTK_OK;
-}
-
 extern "C" int gtk_scatter_update(float* w, float* res, float* vel, const int32_t* g_idx, const float* g_val,
                                   const int32_t* d_gn, const int32_t* l_idx, const float* l_val,
                                   const int32_t* d_ln, int64_t m, float lr, float momentum, int32_t P,
-                                  int32_t scaling, const uint32_t* d_skip, void* ws, size_t ws_bytes,
-                                  void* stream) {
-  (void)ws;
-  (void)ws_bytes;
+                                  int32_t scaling, const uint32_t* d_skip, void* stream) {
   if (!w || !g_idx || !g_val || !d_gn || m < 1 || m >= (int64_t(1) << 31) || P < 1) return GTK_EINVAL;
   if (scaling < 0 || scaling > 2) return GTK_EINVAL;
   if (l_idx && (!l_val || !d_ln || !res)) return GTK_EINVAL;

@@ -214,18 +214,26 @@ def sparse_update_fusable(lr: float, momentum: float) -> bool:
 
 def select_update(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, out: DeviceList,
                   status: torch.Tensor, window: torch.Tensor | None, w: torch.Tensor, lr: float, P_: int,
-                  scaling: int) -> None:
+                  scaling: int, chain: bool = False) -> None:
     """K1 + K3 for P = 1 (gtk_select_update): the selection is the global
     top-k, and every selected entry also updates w exactly like
-    scatter_update's sparse form."""
+    scatter_update's sparse form.  chain=True (GTK_SELECT_CHAIN): no sampling
+    kernel, res_in's pending winners (the previous chained call's) are zeroed
+    on the fly and this call's stay pending in res_out until `settle`."""
     m = grad.numel()
     dev = grad.device
     ws = select_workspace(m, k, dev)
     _lib.call(
         "gtk_select_update", P(res_in), P(grad), P(res_out), m, k, P(out.idx), P(out.val), P(out.count),
-        P(status), P(ws), ctypes.c_size_t(ws.numel()), 0, P(window), P(w), ctypes.c_float(lr), P_, scaling,
-        stream_of(dev),
+        P(status), P(ws), ctypes.c_size_t(ws.numel()), _lib.SELECT_CHAIN if chain else 0, P(window), P(w),
+        ctypes.c_float(lr), P_, scaling, stream_of(dev),
     )
+
+
+def settle(res: torch.Tensor, sel: DeviceList, window: torch.Tensor) -> None:
+    """gtk_select_settle: +0.0 at the last chained select's winners (the
+    residual the reference keeps), and the record's pending flag cleared."""
+    _lib.call("gtk_select_settle", P(res), P(sel.idx), P(sel.count), P(window), stream_of(res.device))
 
 
 def top_op(a: DeviceList, b: DeviceList, k: int, out: DeviceList) -> None:
@@ -247,7 +255,7 @@ def scatter_update(w, res, vel, glist: DeviceList, llist, m, lr, momentum, P_, s
         "gtk_scatter_update", P(w), P(res), P(vel), P(glist.idx), P(glist.val), P(glist.count),
         P(llist.idx if llist is not None else None), P(llist.val if llist is not None else None),
         P(llist.count if llist is not None else None), m, ctypes.c_float(lr),
-        ctypes.c_float(momentum), P_, scaling, P(skip), None, ctypes.c_size_t(0), stream_of(dev),
+        ctypes.c_float(momentum), P_, scaling, P(skip), stream_of(dev),
     )
 
 

@@ -7,9 +7,9 @@ is the plumbing only:
   * a gloo group carries host bytes (Endpoint.send/recv, the CUDA IPC handle
     exchange, barriers).
 gTopKAllReduce itself is ONE kernel per rank (`gtk_gtopk_exchange`): it
-pushes its accumulator into the partner's IPC-mapped inbox over NVLink,
-signals with a system-scope release, waits on its own flag and merges (⊤),
-for every round of the schedule -- recursive-doubling butterfly for P = 2^n
+stores its accumulator into the partner's IPC-mapped inbox over NVLink as
+self-validating low-latency records, polls its own inbox for the partner's
+and merges (⊤), for every round of the schedule -- recursive-doubling butterfly for P = 2^n
 (bitwise equal to the reference's tree + broadcast), the reference's exact
 tree + binomial broadcast otherwise (collectives.py:206-217).
 """
@@ -39,8 +39,8 @@ def _schedule(rank: int, world: int, mode: str):
 
 
 class _ExchangePlan:
-    """Per-k resources of the fused exchange: own inbox/flags (cudaMalloc,
-    IPC-exported), the peers' mapped pointers, accumulator and workspace."""
+    """Per-k resources of the fused exchange: own inbox (cudaMalloc,
+    IPC-exported), the peers' mapped inboxes, accumulator and workspace."""
 
     def __init__(self, group: "DistDeviceGroup", k: int):
         lib = _lib.load()
@@ -50,33 +50,26 @@ class _ExchangePlan:
         self.steps = steps
         sched = np.array([[s, r, mg, j] for j, (s, r, mg) in enumerate(steps)], dtype=np.int32).reshape(-1)
         self.schedule = (ctypes.c_int32 * max(len(sched), 1))(*sched.tolist())
-        n_in, n_fl = ctypes.c_size_t(), ctypes.c_size_t()
+        n_in = ctypes.c_size_t()
         _lib.check(lib.gtk_exchange_inbox_bytes(k, self.nsteps, ctypes.byref(n_in)))
-        _lib.check(lib.gtk_exchange_flags_bytes(self.nsteps, ctypes.byref(n_fl)))
-        self.inbox, self.flags = ctypes.c_void_p(), ctypes.c_void_p()
+        self.inbox = ctypes.c_void_p()
         _lib.check(lib.gtk_dev_alloc(n_in.value, ctypes.byref(self.inbox)))
-        _lib.check(lib.gtk_dev_alloc(n_fl.value, ctypes.byref(self.flags)))
-        handles = np.zeros(128, dtype=np.uint8)
-        _lib.check(lib.gtk_ipc_get_handle(self.inbox, handles[:64].ctypes.data_as(ctypes.c_void_p)))
-        _lib.check(lib.gtk_ipc_get_handle(self.flags, handles[64:].ctypes.data_as(ctypes.c_void_p)))
-        allh = [torch.zeros(128, dtype=torch.uint8) for _ in range(group.world)]
-        dist.all_gather(allh, torch.from_numpy(handles), group=group.gloo)
+        handle = np.zeros(64, dtype=np.uint8)
+        _lib.check(lib.gtk_ipc_get_handle(self.inbox, handle.ctypes.data_as(ctypes.c_void_p)))
+        allh = [torch.zeros(64, dtype=torch.uint8) for _ in range(group.world)]
+        dist.all_gather(allh, torch.from_numpy(handle), group=group.gloo)
         W = group.world
         self.peer_inbox = (ctypes.c_void_p * W)()
-        self.peer_flags = (ctypes.c_void_p * W)()
         self._opened = []
         for r in range(W):
             if r == group.rank:
                 self.peer_inbox[r] = self.inbox.value
-                self.peer_flags[r] = self.flags.value
                 continue
             h = allh[r].numpy()
-            pi, pf = ctypes.c_void_p(), ctypes.c_void_p()
-            _lib.check(lib.gtk_ipc_open_handle(h[:64].ctypes.data_as(ctypes.c_void_p), ctypes.byref(pi)))
-            _lib.check(lib.gtk_ipc_open_handle(h[64:].ctypes.data_as(ctypes.c_void_p), ctypes.byref(pf)))
+            pi = ctypes.c_void_p()
+            _lib.check(lib.gtk_ipc_open_handle(h.ctypes.data_as(ctypes.c_void_p), ctypes.byref(pi)))
             self.peer_inbox[r] = pi.value
-            self.peer_flags[r] = pf.value
-            self._opened += [pi, pf]
+            self._opened.append(pi)
         dev = group.device
         self.acc = DeviceList(group.dim_hint, k, dev)
         self.ws = _dev.merge_workspace(k, k, dev)
@@ -95,14 +88,24 @@ class _ExchangePlan:
         else:
             self.schedule_prepushed = None
         dist.barrier(group=group.gloo)  # every rank mapped every peer before first use
+        self._gloo = group.gloo
 
     def close(self):
+        """Unmap the peers' inboxes and free our own -- only once every rank's
+        kernels are done with them: drain this device, then a host barrier
+        (a peer may still be writing into our inbox until it has finished)."""
         lib = _lib.load()
+        torch.cuda.synchronize(self.acc.device)
+        try:
+            dist.barrier(group=self._gloo)
+        except Exception:  # noqa: BLE001 - a dead peer: nothing left to wait for
+            pass
         for p in self._opened:
             lib.gtk_ipc_close_handle(p)
         self._opened = []
-        lib.gtk_dev_free(self.inbox)
-        lib.gtk_dev_free(self.flags)
+        if self.inbox:
+            lib.gtk_dev_free(self.inbox)
+            self.inbox = ctypes.c_void_p()
 
 
 class DistDeviceGroup:
@@ -120,10 +123,21 @@ class DistDeviceGroup:
         self.dim_hint = 0
         self._plans: dict[int, _ExchangePlan] = {}
         self.aborted = False
-        self._abort_host = None
+        # abort word: pinned host memory mapped into the device; the exchange
+        # kernel polls it while it waits for a partner (transport.py:210-214)
+        lib = _lib.load()
+        self._abort_host = ctypes.POINTER(ctypes.c_uint32)()
+        self._abort_dev = ctypes.POINTER(ctypes.c_uint32)()
+        with torch.cuda.device(device):
+            _lib.check(lib.gtk_abort_word_create(ctypes.byref(self._abort_host), ctypes.byref(self._abort_dev)),
+                       "gtk_abort_word_create")
 
     def abort(self) -> None:
+        """Wake this rank's waiting exchange kernel: it stops polling, the step
+        raises TransportError("cluster aborted"); later calls raise at once."""
         self.aborted = True
+        if self._abort_host:
+            _lib.load().gtk_abort_word_set(self._abort_host, 1)
 
     def plan(self, k: int, dim: int) -> _ExchangePlan:
         p = self._plans.get(k)
@@ -175,8 +189,9 @@ class DistDeviceGroup:
             raise ValueError("no first-step partner to have pushed to")
         sched = plan.schedule_prepushed if prepushed else plan.schedule
         args = [self.rank, self.world, sched, plan.nsteps, plan.peer_inbox,
-                plan.peer_flags, P(plan.epoch), P(plan.acc.idx), P(plan.acc.val), P(plan.acc.count),
-                plan.k, P(status), None, ctypes.c_int64(int(self.timeout * 1e9)), P(plan.step_counts),
+                P(plan.epoch), P(plan.acc.idx), P(plan.acc.val), P(plan.acc.count),
+                plan.k, P(status), ctypes.cast(self._abort_dev, ctypes.c_void_p),
+                ctypes.c_int64(int(self.timeout * 1e9)), P(plan.step_counts),
                 P(src.idx if src else None), P(src.val if src else None), P(src.count if src else None),
                 P(plan.ws), ctypes.c_size_t(plan.ws.numel())]
         if update is not None and src is not None and plan.nsteps > 0:
@@ -216,13 +231,7 @@ class DistDeviceGroup:
     # -- dense baseline: NCCL allreduce (sum) -----------------------------------
     def dense(self, ep: Endpoint, g: torch.Tensor) -> torch.Tensor:
         W = self.world
-        m = torch.tensor([g.numel()], dtype=torch.int64)
-        ms = [torch.zeros(1, dtype=torch.int64) for _ in range(W)]
-        dist.all_gather(ms, m, group=self.gloo)
-        if any(int(x) != g.numel() for x in ms):
-            from .transport import ProtocolError
-
-            raise ProtocolError("ring chunk size mismatch across ranks")
+        self._check_dims(g.numel())
         out = g.clone()
         if W > 1:
             dist.all_reduce(out, op=dist.ReduceOp.SUM)
@@ -233,10 +242,41 @@ class DistDeviceGroup:
         ep.stats.bytes_recv += 2 * (W - 1) * chunk * 4
         return out
 
+    # -- rank-order dense sum: NCCL allgather + one rank-ordered sum kernel ------
+    def dense_rank_order(self, ep: Endpoint, g: torch.Tensor) -> torch.Tensor:
+        """optimizer.py:105-115: the reference's allgather of whole vectors and
+        +0-seeded accumulation in rank order (bitwise, unlike NCCL's sum)."""
+        W, m = self.world, g.numel()
+        self._check_dims(m)
+        parts = torch.empty(W * m, dtype=torch.float32, device=self.device)
+        if W > 1:
+            dist.all_gather_into_tensor(parts, g)
+        else:
+            parts.copy_(g)
+        out = torch.empty(m, dtype=torch.float32, device=self.device)
+        _dev.dense_sum([parts[r * m:(r + 1) * m] for r in range(W)], m, out)
+        ep.stats.msgs_sent += W - 1
+        ep.stats.msgs_recv += W - 1
+        ep.stats.bytes_sent += (W - 1) * 4 * m
+        ep.stats.bytes_recv += (W - 1) * 4 * m
+        return out
+
+    def _check_dims(self, m: int) -> None:
+        ms = [torch.zeros(1, dtype=torch.int64) for _ in range(self.world)]
+        dist.all_gather(ms, torch.tensor([m], dtype=torch.int64), group=self.gloo)
+        if any(int(x) != m for x in ms):
+            from .transport import ProtocolError
+
+            raise ProtocolError("ring chunk size mismatch across ranks")
+
     def close(self) -> None:
         for p in self._plans.values():
             p.close()
         self._plans.clear()
+        if self._abort_host:
+            torch.cuda.synchronize(self.device)
+            _lib.load().gtk_abort_word_destroy(self._abort_host)
+            self._abort_host = ctypes.POINTER(ctypes.c_uint32)()
 
 
 class DistEndpoint(Endpoint):

@@ -87,6 +87,11 @@ class OptimizerState:
         self.momentum = momentum
         self.update_scaling = update_scaling
         self.schedule = schedule if schedule is not None else DensitySchedule()
+        # a chained P = 1 select (gtk_select_update + GTK_SELECT_CHAIN) leaves its
+        # winners pending in the live residual: (selection, key-window record)
+        # until `_settle` zeroes them (lazily: the next chained step does it on
+        # the fly, anything else that reads the residual settles first)
+        self._pending = None
         if not 0.0 <= self.momentum < 1.0:
             raise ValueError("momentum must be in [0, 1)")
         if self.update_scaling not in ("average", "sum"):
@@ -98,10 +103,20 @@ class OptimizerState:
     def m(self) -> int:
         return self._w.numel() if self._w is not None else self._w_np.size
 
+    def _settle(self) -> None:
+        """Materialise the residual the reference keeps (+0.0 at the last
+        chained step's winners, optimizer.py:230)."""
+        if self._pending is not None:
+            sel, win = self._pending
+            self._pending = None
+            _dev.settle(self._res, sel, win)
+            self._host_cache.pop("r", None)
+
     def to_device(self, device) -> None:
         """Move the state into HBM on `device` (no-op if already there)."""
         if self._w is not None and self._w.device == device:
             return
+        self._settle()
         if self._w is not None:  # move between devices
             self._w, self._res = self._w.to(device), self._res.to(device)
             self._vel = None if self._vel is None else self._vel.to(device)
@@ -143,10 +158,12 @@ class OptimizerState:
     def residual(self):
         if self._res is None:
             return self._res_np
+        self._settle()
         return self._res if self._device_mode else self._host("r", self._res)
 
     @residual.setter
     def residual(self, value) -> None:
+        self._settle()
         if self._res is not None:
             v = value if _is_cuda(value) else torch.from_numpy(as_dense(value).copy())
             self._res.copy_(v.reshape(-1))
@@ -265,17 +282,21 @@ class _Timer:
 def _select_checked(state, g, k, sel: DeviceList, status, fused_update: bool = False) -> None:
     """K1 into the spare residual; raises FloatingPointError with the state
     untouched (the live residual is never written; with fused_update the
-    weights are only written when the input is finite)."""
+    weights are only written when the input is finite).  fused_update (P = 1)
+    runs chained: res_in's pending winners are zeroed on the fly and this
+    step's stay pending (state._pending) until the residual is read."""
     m = state.m
     if not 1 <= k <= m:
         raise ValueError(f"k must be in [1, {m}], got {k}")
     win = getattr(state, "_window", None)
     if win is None or win.device != g.device:
+        state._settle()
         win = state._window = _dev.new_window(g.device)  # this residual's key window (K1 hint)
     if fused_update:
         _dev.select_update(state._res, g, state._res2, k, sel, status[0:1], win, state._w,
-                           float(np.float32(state.lr)), 1, _scaling_code(state))
+                           float(np.float32(state.lr)), 1, _scaling_code(state), chain=True)
     else:
+        state._settle()
         _dev.select(state._res, g, state._res2, k, sel, status[0:1], window=win)
 
 
@@ -307,6 +328,7 @@ def gtopk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float =
         word, gnnz = _finish(status, sel.n)
         _dev.raise_status(word)
         state._commit(swap_residual=True)
+        state._pending = (sel, state._window)  # this step's winners, pending in the new residual
         return StepReport(loss=loss, t_compute_ms=t_compute_ms, t_compress_ms=tm.ms(0, 1),
                           t_communicate_ms=tm.ms(1, 2), selected_k=gnnz)
     _select_checked(state, g, k, sel, status)
@@ -382,9 +404,8 @@ def dense_step(state: OptimizerState, ep, grad, P: int, *, loss: float = 0.0,
     state._ensure_velocity()
     t0 = time.perf_counter()
     if rank_order_sum:
-        # allgather + rank-order accumulation (optimizer.py:108-115); the
-        # in-process dense sum is already rank-ordered
-        total = _coll.dense_ring_allreduce(ep, g)
+        # allgather + rank-order accumulation (optimizer.py:108-115)
+        total = _coll.rank_order_dense_sum(ep, g)
     else:
         total = _coll.dense_ring_allreduce(ep, g)
     t_comm = (time.perf_counter() - t0) * 1e3

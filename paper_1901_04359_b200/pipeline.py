@@ -42,6 +42,7 @@ class GTopKPipeline:
         self.P = ep.world_size
         self.dev = self.group.device
         state.to_device(self.dev)
+        state._settle()  # the pipeline's own key-window record starts with nothing pending
         state._ensure_velocity()
         self.state = state
         self.m = state.m
@@ -71,15 +72,19 @@ class GTopKPipeline:
         self.block_graph = None
         self.kernels_per_step = None
         self.use_graph = use_graph
+        self.chained = False  # steps leave their winners pending (settled by sync_state)
 
     # -- one step's launches (current stream) --------------------------------
     def _enqueue(self, parity: int) -> None:
         grad = self.grads[parity % len(self.grads)]
         res_in, res_out = self.res[parity], self.res[1 - parity]
         if self.P == 1 and _dev.sparse_update_fusable(self.lr, self.mom):
-            # one rank: the global top-k is the selection; K3 rides on K1's finish
+            # one rank: the global top-k is the selection; K3 rides on K1's
+            # finish; chained selects (two launches per step: no sampling
+            # kernel, the winners' residual zeroed by the next step's stream)
             _dev.select_update(res_in, grad, res_out, self.k, self.sel, self.status, self.window,
-                               self.state._w, self.lr, 1, self.scaling)
+                               self.state._w, self.lr, 1, self.scaling, chain=True)
+            self.chained = True
             return
         if self.P > 1 and _dev.sparse_update_fusable(self.lr, self.mom) and self.plan.push_slot0 is not None:
             # the selection goes to the first partner as it is written
@@ -224,6 +229,10 @@ class GTopKPipeline:
         and iteration count)."""
         st = self.state
         p = self.t % 2
+        if self.chained and self.t > 0:
+            # materialise the residual of the last step (+0.0 at its winners);
+            # the next chained step would have zeroed them on the fly
+            _dev.settle(self.res[p], self.sel, self.window)
         st._res, st._res2 = self.res[p], self.res[1 - p]
         st.iteration += self.t - getattr(self, "_synced_t", 0)
         self._synced_t = self.t

@@ -23,11 +23,10 @@
 
 from __future__ import annotations
 
+import collections
 import logging
-import queue
 import struct
 import threading
-import time
 
 import numpy as np
 
@@ -169,8 +168,17 @@ class TransportStats:
 # ---------------------------------------------------------------------------
 
 
+def _dissemination_rounds(rank: int, P: int):
+    """(send_to, recv_from) of each round of a dissemination barrier: round r
+    pairs rank with rank +- 2^r (mod P), ceil(log2 P) rounds (transport.py:197-206)."""
+    return [((rank + (1 << r)) % P, (rank - (1 << r)) % P) for r in range((P - 1).bit_length())]
+
+
 class Endpoint:
-    """One rank's handle (transport.py:156-220) plus its device group."""
+    """One rank's handle (transport.py:156-220): blocking byte messages to and
+    from the other ranks, matched on (peer, tag) in FIFO order, plus the
+    device group the GPU collectives run on.  Backends implement the
+    reference's plug points `_send_impl` / `_recv_impl`."""
 
     def __init__(self, rank: int, world_size: int, timeout: float = DEFAULT_TIMEOUT):
         self.rank = rank
@@ -179,43 +187,36 @@ class Endpoint:
         self.stats = TransportStats()
         self.group = None  # device group used by the GPU collectives
 
-    def send(self, dest: int, tag: int, payload: bytes) -> None:
-        self._check_peer(dest)
-        self._check_tag(tag)
-        if len(payload) > _MAX_PAYLOAD:
-            raise ValueError("payload too large")
-        self._send_impl(dest, tag, bytes(payload))
-        self.stats.msgs_sent += 1
-        self.stats.bytes_sent += len(payload)
-
-    def recv(self, source: int, tag: int) -> bytes:
-        self._check_peer(source)
-        self._check_tag(tag)
-        payload = self._recv_impl(source, tag)
-        self.stats.msgs_recv += 1
-        self.stats.bytes_recv += len(payload)
-        return payload
-
-    def _check_peer(self, other: int) -> None:
-        if other == self.rank:
+    def _validate(self, peer: int, tag: int) -> None:
+        # argument errors are ValueError, raised before any transfer
+        if peer == self.rank:
             raise ValueError("send/recv to self is not allowed")
-        if not 0 <= other < self.world_size:
-            raise ValueError(f"rank {other} out of range [0, {self.world_size})")
-
-    @staticmethod
-    def _check_tag(tag: int) -> None:
-        if not 0 <= tag < 2**32:
+        if peer < 0 or peer >= self.world_size:
+            raise ValueError(f"rank {peer} out of range [0, {self.world_size})")
+        if tag < 0 or tag >= 1 << 32:
             raise ValueError(f"tag must fit in 32 bits, got {tag}")
 
+    def send(self, dest: int, tag: int, payload: bytes) -> None:
+        self._validate(dest, tag)
+        data = bytes(payload)
+        if len(data) > _MAX_PAYLOAD:
+            raise ValueError("payload too large")
+        self._send_impl(dest, tag, data)
+        self.stats.msgs_sent += 1
+        self.stats.bytes_sent += len(data)
+
+    def recv(self, source: int, tag: int) -> bytes:
+        self._validate(source, tag)
+        data = self._recv_impl(source, tag)
+        self.stats.msgs_recv += 1
+        self.stats.bytes_recv += len(data)
+        return data
+
     def barrier(self) -> None:
-        """Dissemination barrier, ceil(log2 P) rounds (transport.py:197-206)."""
-        P = self.world_size
-        if P == 1:
-            return
-        for r in range((P - 1).bit_length()):
-            step = 1 << r
-            self.send((self.rank + step) % P, BARRIER_TAG + r, b"")
-            self.recv((self.rank - step) % P, BARRIER_TAG + r)
+        """Dissemination barrier: ceil(log2 P) rounds of empty messages."""
+        for r, (to, frm) in enumerate(_dissemination_rounds(self.rank, self.world_size)):
+            self.send(to, BARRIER_TAG + r, b"")
+            self.recv(frm, BARRIER_TAG + r)
 
     def abort(self) -> None:
         """Wake blocked peers with TransportError."""
@@ -230,53 +231,59 @@ class Endpoint:
         raise NotImplementedError
 
 
-class _LocalRouter:
-    """FIFO byte channels of one in-process cluster (transport.py:228-248)."""
+class _Mailboxes:
+    """Byte channels of one in-process cluster: one mailbox per destination
+    rank, each a condition variable over per-(source, tag) FIFOs, so a receiver
+    sleeps until its own mailbox changes (no polling) and an abort wakes every
+    receiver at once."""
 
     def __init__(self, P: int):
-        self.P = P
-        self._queues: dict = {}
-        self._lock = threading.Lock()
+        self._cond = [threading.Condition() for _ in range(P)]
+        self._fifo: list[dict] = [collections.defaultdict(collections.deque) for _ in range(P)]
         self.aborted = False
 
-    def channel(self, src: int, dst: int, tag: int) -> queue.SimpleQueue:
-        key = (src, dst, tag)
-        with self._lock:
-            q = self._queues.get(key)
-            if q is None:
-                q = self._queues[key] = queue.SimpleQueue()
-            return q
+    def post(self, src: int, dst: int, tag: int, payload: bytes) -> None:
+        if self.aborted:
+            raise TransportError("cluster aborted")
+        with self._cond[dst]:
+            self._fifo[dst][(src, tag)].append(payload)
+            self._cond[dst].notify_all()
+
+    def take(self, src: int, dst: int, tag: int, timeout: float) -> bytes:
+        key = (src, tag)
+        cond, fifo = self._cond[dst], self._fifo[dst]
+        with cond:
+            ready = cond.wait_for(lambda: self.aborted or bool(fifo.get(key)), timeout)
+            if fifo.get(key):  # delivered messages are still handed out after an abort
+                return fifo[key].popleft()
+            if self.aborted:
+                raise TransportError("cluster aborted")
+            assert not ready
+            raise TransportError(f"rank {dst}: recv from {src} tag {tag} timed out")
 
     def abort(self) -> None:
         self.aborted = True
+        for cond in self._cond:
+            with cond:
+                cond.notify_all()
 
 
 class LocalEndpoint(Endpoint):
-    def __init__(self, rank, world_size, router: _LocalRouter, group, timeout):
+    """Endpoint of an in-process cluster (transport.py:250-276)."""
+
+    def __init__(self, rank, world_size, boxes: _Mailboxes, group, timeout):
         super().__init__(rank, world_size, timeout)
-        self._router = router
+        self._boxes = boxes
         self.group = group
 
     def _send_impl(self, dest, tag, payload):
-        if self._router.aborted:
-            raise TransportError("cluster aborted")
-        self._router.channel(self.rank, dest, tag).put(payload)
+        self._boxes.post(self.rank, dest, tag, payload)
 
     def _recv_impl(self, source, tag):
-        q = self._router.channel(source, self.rank, tag)
-        deadline = time.monotonic() + self.timeout
-        while True:
-            remaining = deadline - time.monotonic()
-            if remaining <= 0:
-                raise TransportError(f"rank {self.rank}: recv from {source} tag {tag} timed out")
-            try:
-                return q.get(timeout=min(0.1, remaining))
-            except queue.Empty:
-                if self._router.aborted:
-                    raise TransportError("cluster aborted") from None
+        return self._boxes.take(source, self.rank, tag, self.timeout)
 
     def abort(self):
-        self._router.abort()
+        self._boxes.abort()
         if self.group is not None:
             self.group.abort()
 
@@ -284,20 +291,24 @@ class LocalEndpoint(Endpoint):
 class LocalDeviceGroup:
     """Rendezvous for the in-process GPU collectives.
 
-    Every rank thread deposits its operand, one leader thread runs the whole
-    collective as a chain of kernels on one stream (no device-side waits
-    between separately launched kernels -- they would not be guaranteed to
-    be co-scheduled on one GPU), then every rank picks up its result.
+    Every rank thread deposits its operand; the LAST rank to arrive runs the
+    whole collective as a chain of kernels on its stream (kernels that waited
+    on each other would not be guaranteed to be co-scheduled on one GPU) and
+    publishes the result; every rank returns it.  One condition-variable
+    rendezvous per collective: a rank can only enter the next collective after
+    it has read this one's result, and the next result is only written once
+    every rank has entered, so results alternate between two slots.
     """
 
     def __init__(self, P: int, device=None, timeout: float = DEFAULT_TIMEOUT):
         self.P = P
         self._device = device
         self.timeout = timeout
-        self._slots = [None] * P
-        self._result = None
-        self._error = None
-        self._barrier = threading.Barrier(P)
+        self._cond = threading.Condition()
+        self._operands = [None] * P
+        self._arrived = 0
+        self._generation = 0
+        self._outcome = [None, None]  # (result, error) per generation parity
         self.aborted = False
 
     @property
@@ -309,37 +320,35 @@ class LocalDeviceGroup:
         return self._device
 
     def abort(self) -> None:
-        self.aborted = True
-        self._barrier.abort()
-
-    def _wait(self) -> None:
-        if self.aborted:
-            raise TransportError("cluster aborted")
-        try:
-            self._barrier.wait(timeout=self.timeout)
-        except threading.BrokenBarrierError:
-            if self.aborted:
-                raise TransportError("cluster aborted") from None
-            raise TransportError("collective rendezvous timed out") from None
+        with self._cond:
+            self.aborted = True
+            self._cond.notify_all()
 
     def run(self, rank: int, operand, leader_fn):
-        """Collective call: returns leader_fn(all operands) to every rank."""
-        self._slots[rank] = operand
-        self._wait()
-        if rank == 0:
-            try:
-                self._result = leader_fn(list(self._slots))
-                self._error = None
-            except BaseException as exc:  # noqa: BLE001 - re-raised on every rank
-                self._result = None
-                self._error = exc
-        self._wait()
-        res, err = self._result, self._error
-        self._slots[rank] = None
-        self._wait()
+        """Collective call: returns leader_fn(all operands, rank order) to every rank."""
+        with self._cond:
+            if self.aborted:
+                raise TransportError("cluster aborted")
+            gen = self._generation
+            self._operands[rank] = operand
+            self._arrived += 1
+            if self._arrived == self.P:
+                ops, self._operands = self._operands, [None] * self.P
+                self._arrived = 0
+                try:
+                    self._outcome[gen & 1] = (leader_fn(ops), None)
+                except BaseException as exc:  # noqa: BLE001 - re-raised on every rank
+                    self._outcome[gen & 1] = (None, exc)
+                self._generation += 1
+                self._cond.notify_all()
+            elif not self._cond.wait_for(lambda: self._generation != gen or self.aborted, self.timeout):
+                raise TransportError("collective rendezvous timed out")
+            if self._generation == gen:  # woken by an abort before completion
+                raise TransportError("cluster aborted")
+            result, err = self._outcome[gen & 1]
         if err is not None:
             raise err
-        return res
+        return result
 
 
 def create_local_cluster(P: int, timeout: float = DEFAULT_TIMEOUT, device=None) -> list[Endpoint]:
@@ -347,51 +356,53 @@ def create_local_cluster(P: int, timeout: float = DEFAULT_TIMEOUT, device=None) 
     share one GPU device group."""
     if P < 1:
         raise ValueError(f"P must be >= 1, got {P}")
-    router = _LocalRouter(P)
+    boxes = _Mailboxes(P)
     group = LocalDeviceGroup(P, device, timeout)
-    return [LocalEndpoint(r, P, router, group, timeout) for r in range(P)]
+    return [LocalEndpoint(r, P, boxes, group, timeout) for r in range(P)]
+
+
+def _root_cause(failures: dict) -> BaseException:
+    """The failure to report: a rank's own error before the TransportErrors
+    the abort induced in the others, lowest rank first (transport.py:535-538)."""
+    own = sorted(r for r, e in failures.items() if not isinstance(e, TransportError))
+    return failures[own[0] if own else min(failures)]
 
 
 def run_workers(endpoints: list[Endpoint], fn) -> list:
-    """Run fn(ep) on one thread per endpoint (transport.py:507-539); on any
-    failure abort the cluster and re-raise the root cause (non-TransportError
-    preferred, lowest rank first).  Worker threads inherit the caller's CUDA
-    device."""
-    results = [None] * len(endpoints)
+    """fn(ep) for every endpoint concurrently, one host thread per rank
+    (transport.py:507-539); results in rank order.  The first failure aborts
+    every endpoint (waking blocked receives and rendezvous) and the root
+    cause is re-raised.  Worker threads run on the caller's CUDA device."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    n = len(endpoints)
+    results: list = [None] * n
     failures: dict[int, BaseException] = {}
-    lock = threading.Lock()
-    dev_idx = None
+    device = None
     try:
         import torch
 
         if torch.cuda.is_available():
-            dev_idx = torch.cuda.current_device()
-    except Exception:  # pragma: no cover
-        dev_idx = None
+            device = torch.cuda.current_device()
+    except Exception:  # pragma: no cover - torch absent
+        device = None
 
-    def runner(i: int, ep: Endpoint):
+    def body(i: int) -> None:
         try:
-            if dev_idx is not None:
+            if device is not None:
                 import torch
 
-                torch.cuda.set_device(dev_idx)
-            results[i] = fn(ep)
-        except BaseException as exc:  # noqa: BLE001
-            with lock:
-                failures[i] = exc
-            for other in endpoints:
-                other.abort()
+                torch.cuda.set_device(device)
+            results[i] = fn(endpoints[i])
+        except BaseException as exc:  # noqa: BLE001 - reported to the caller
+            failures[i] = exc
+            for ep in endpoints:
+                ep.abort()
 
-    threads = [
-        threading.Thread(target=runner, args=(i, ep), name=f"gtopk-b200-worker-{i}")
-        for i, ep in enumerate(endpoints)
-    ]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join()
+    if n:
+        with ThreadPoolExecutor(max_workers=n, thread_name_prefix="gtopk-b200-rank") as pool:
+            for fut in [pool.submit(body, i) for i in range(n)]:
+                fut.result()
     if failures:
-        primary = [r for r, e in failures.items() if not isinstance(e, TransportError)]
-        rank = min(primary) if primary else min(failures)
-        raise failures[rank]
+        raise _root_cause(failures)
     return results

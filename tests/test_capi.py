@@ -58,8 +58,8 @@ def test_workspace_sizes(lib):
     assert lib.gtk_select_workspace_bytes(1 << 31, 10, ctypes.byref(n)) == 1  # m >= 2^31
     assert lib.gtk_merge_workspace_bytes(25_600, 25_600, ctypes.byref(n)) == 0 and n.value > 0
     assert lib.gtk_exchange_inbox_bytes(1000, 3, ctypes.byref(n)) == 0
-    assert n.value >= 2 * 3 * (16 + 8 * 1000)
-    assert lib.gtk_exchange_flags_bytes(3, ctypes.byref(n)) == 0 and n.value == 24
+    assert n.value >= 2 * 3 * (16 + 16 * 1000)  # 2 call parities x 3 steps of LL slots
+    assert lib.gtk_exchange_inbox_bytes(1000, 65, ctypes.byref(n)) == 1  # > kMaxSteps
 
 
 def test_argument_validation_without_gpu(lib):
@@ -69,8 +69,10 @@ def test_argument_validation_without_gpu(lib):
     # invalid arguments are rejected before any CUDA call
     assert lib.gtk_select(null, null, null, 10, 1, null, null, null, null, null, 0, 0, null) == _lib.GTK_EINVAL
     assert lib.gtk_top_op(null, null, null, null, null, null, 1, 0, null, null, null, null, 0, null) == _lib.GTK_EINVAL
-    assert lib.gtk_gtopk_exchange(0, 0, null, 0, null, null, null, null, null, null, 1, null, null, 0, null,
+    assert lib.gtk_gtopk_exchange(0, 0, null, 0, null, null, null, null, null, 1, null, null, 0, null,
                                   null, null, null, null, 0, null) == _lib.GTK_EINVAL
+    assert lib.gtk_abort_word_create(None, None) == _lib.GTK_EINVAL
+    assert lib.gtk_abort_word_set(None, 1) == _lib.GTK_EINVAL
     with pytest.raises(ValueError):
         _lib.check(_lib.GTK_EINVAL, "x")
     with pytest.raises(FloatingPointError):

@@ -467,3 +467,68 @@ def test_windowed_recovers_after_nonfinite(dev):
         assert words[-1] & 0x1 == 0, (step, words)
         res = wres
     assert all(w & 0x2 == 0 for w in words[4:]), words
+
+
+@pytest.mark.parametrize("kind", ["normal", "ties", "flat"])
+def test_chained_select_update_trajectory(dev, kind):
+    """GTK_SELECT_CHAIN (the P = 1 pipeline's select): no sampling kernel,
+    each call zeroes the previous call's pending winners on the fly (exact
+    predicate key > tau || key == tau && idx <= cut) and leaves its own
+    pending.  Checked step by step against the oracle: selection, w and the
+    settled residual -- through heavy ties at the k-th key (integer
+    gradients: the predicate's index cut), a k change mid-chain, a
+    non-finite step (state rolled back, pending winners kept) and a tail tile
+    (m not a multiple of 4096)."""
+    import torch
+
+    from oracle import gtopk_oracle as orc
+
+    d = torch.device("cuda", 0)
+    m, lr = 1_000_003, 0.05
+    rng = np.random.default_rng({"normal": 1, "ties": 2, "flat": 3}[kind])
+
+    def grad(t):
+        if kind == "ties":
+            return rng.integers(-3, 4, m).astype(F32)
+        if kind == "flat":
+            return (rng.random(m) < 0.5).astype(F32) * F32(0.25) + F32(1.0)
+        return rng.standard_normal(m).astype(F32)
+
+    ref = orc.State(np.zeros(m, F32), lr)
+    R = [torch.zeros(m, device=d), torch.empty(m, device=d)]
+    w = torch.zeros(m, device=d)
+    win = dev.new_window(d)
+    st = torch.zeros(1, dtype=torch.int32, device=d)
+    cur = 0
+    for t in range(24):
+        k = 1000 if t < 14 else 1500
+        g = grad(t)
+        lst = dev.DeviceList(m, k, d)
+        if t == 9:  # a non-finite step: nothing changes, the pending winners stay recorded
+            bad = g.copy()
+            bad[m - 2] = np.inf
+            st.zero_()
+            w_before = w.clone()
+            dev.select_update(R[cur], torch.from_numpy(bad).to(d), R[1 - cur], k, lst, st, win, w,
+                              float(F32(lr)), 1, 0, chain=True)
+            assert int(st.item()) & 0x1
+            assert torch.equal(w, w_before)
+        st.zero_()
+        dev.select_update(R[cur], torch.from_numpy(g).to(d), R[1 - cur], k, lst, st, win, w, float(F32(lr)), 1, 0,
+                          chain=True)
+        (gi, gv), _ = orc.gtopk_step_all([ref], [g], k)
+        word = int(st.item())
+        assert word & 0x1D == 0, hex(word)
+        i, v = lst.to_host()
+        assert np.array_equal(i, gi), (kind, t)
+        assert np.array_equal(v.view(np.uint32), gv.view(np.uint32)), (kind, t)
+        assert np.array_equal(w.cpu().numpy().view(np.uint32), ref.weights.view(np.uint32)), (kind, t)
+        cur = 1 - cur
+        settled = R[cur].clone()
+        dev.settle(settled, lst, win.clone())
+        assert np.array_equal(settled.cpu().numpy().view(np.uint32), ref.residual.view(np.uint32)), (kind, t)
+    # settling in place clears the record's pending flag; the next chained
+    # call then leaves the (already +0.0) winners alone
+    dev.settle(R[cur], lst, win)
+    assert int(win[0].item()) & 0x2 == 0
+    assert np.array_equal(R[cur].cpu().numpy().view(np.uint32), ref.residual.view(np.uint32))

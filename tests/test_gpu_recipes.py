@@ -1,0 +1,146 @@
+"""Oracle parity at the BASELINE.json configurations the bench times, through
+the public API and the CUDA-graph pipeline (bitwise: indices, values,
+residual, weights).
+
+* headline: m = 25.6M, rho = 0.001 (k = 25,600), the reference bench's first
+  gradient (cli.py:249-251: default_rng(seed 0), rank 0 = draw 0);
+* BASELINE config 5 at its extreme: m = 66M (LSTM-PTB size), rho = 0.01
+  (k = 660,000) -- the density sweep's largest selection, with the fused
+  update (gtk_select_update);
+* the regime bench.py times: the graph-replayed pipeline (select + fused K3,
+  carried key window, 20-step block graphs) for 2,000 steps = 2/rho at
+  ResNet-20 size, compared with the oracle's trajectory step by step.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA GPU")]
+
+F32 = np.float32
+
+
+def bits(a):
+    return np.ascontiguousarray(a, F32).view(np.uint32)
+
+
+def k_from_density(rho, m):
+    return max(1, min(m, round(rho * m)))
+
+
+def test_headline_recipe_select_and_step():
+    import torch
+
+    import paper_1901_04359_b200 as gtopk
+    from oracle import gtopk_oracle as orc
+
+    m = 25_600_000
+    k = k_from_density(0.001, m)
+    g = np.random.default_rng(0).standard_normal(m).astype(F32)  # cli.run_bench draw 0
+    wi, wv, wres = orc.top_k_select(g, k)
+    sel, res = gtopk.top_k_select(g, k)
+    assert np.array_equal(sel.indices, wi)
+    assert np.array_equal(bits(sel.values), bits(wv))
+    assert np.array_equal(bits(res), bits(wres))
+    # one gtopk_step at P = 1 (K1 + fused K3) from a nonzero residual
+    w0 = np.random.default_rng(1).standard_normal(m).astype(F32)
+    r0 = (np.random.default_rng(2).standard_normal(m) * 0.1).astype(F32)
+    ref = orc.State(w0, 0.01)
+    ref.residual = r0.copy()
+    orc.gtopk_step_all([ref], [g], k)
+    ep = gtopk.create_local_cluster(1)[0]
+    st = gtopk.OptimizerState(torch.from_numpy(w0).cuda(), torch.from_numpy(r0).cuda(), 0.01)
+    rep = gtopk.gtopk_step(st, ep, torch.from_numpy(g).cuda(), k, 1)
+    assert rep.selected_k == k
+    assert np.array_equal(bits(st.weights.cpu().numpy()), bits(ref.weights))
+    assert np.array_equal(bits(st.residual.cpu().numpy()), bits(ref.residual))
+
+
+def test_config5_extreme_66m_rho_001():
+    """m = 66M, k = 660K: 12K candidates per finish block in dynamic shared
+    memory, 660K winners written with the fused w update."""
+    import torch
+
+    import paper_1901_04359_b200 as gtopk
+    from oracle import gtopk_oracle as orc
+
+    m = 66_000_000
+    k = k_from_density(0.01, m)
+    assert k == 660_000
+    rng = np.random.default_rng(0)
+    g = rng.standard_normal(m).astype(F32)
+    r0 = (rng.standard_normal(m) * 0.3).astype(F32)
+    w0 = np.ones(m, F32)
+    ref = orc.State(w0, 0.05)
+    ref.residual = r0.copy()
+    (gi, gv), _ = orc.gtopk_step_all([ref], [g], k)
+    ep = gtopk.create_local_cluster(1)[0]
+    st = gtopk.OptimizerState(torch.from_numpy(w0).cuda(), torch.from_numpy(r0).cuda(), 0.05)
+    rep = gtopk.gtopk_step(st, ep, torch.from_numpy(g).cuda(), k, 1)
+    assert rep.selected_k == k
+    sel = st._list("sel", k)
+    si, sv_ = sel.to_host()
+    assert np.array_equal(si, gi) and np.array_equal(bits(sv_), bits(gv))
+    assert np.array_equal(bits(st.weights.cpu().numpy()), bits(ref.weights))
+    assert np.array_equal(bits(st.residual.cpu().numpy()), bits(ref.residual))
+
+
+def test_graph_pipeline_steady_state_trajectory():
+    """bench.py's timed regime at ResNet-20 size: 2,000 graph-replayed steps
+    (2/rho: the residual builds up and settles), weights and residual equal
+    to the oracle's after every step of the first 100 and every 20-step block
+    graph after that."""
+    import torch
+
+    import paper_1901_04359_b200 as gtopk
+    from oracle import gtopk_oracle as orc
+    from paper_1901_04359_b200.pipeline import GTopKPipeline
+
+    m = 270_000
+    k = k_from_density(0.001, m)
+    rng = np.random.default_rng(0)
+    grads = [rng.standard_normal(m).astype(F32) for _ in range(2)]
+    lr = 0.01
+    ep = gtopk.create_local_cluster(1)[0]
+    st = gtopk.make_state(torch.zeros(m, device="cuda"), lr=lr)
+    pipe = GTopKPipeline(ep, st, k, [torch.from_numpy(x).cuda() for x in grads])
+    ref = orc.State(np.zeros(m, F32), lr)
+
+    def ref_steps(n, t0):
+        for t in range(t0, t0 + n):
+            orc.gtopk_step_all([ref], [grads[t % 2]], k)
+
+    from paper_1901_04359_b200 import device as dv
+
+    def check(t):
+        # after t steps the live residual is res[t % 2]; chained steps leave
+        # the last step's winners pending (the next step zeroes them on the
+        # fly): compare a settled COPY, so the live pipeline keeps exercising
+        # the on-the-fly path
+        res = pipe.res[t % 2].clone()
+        dv.settle(res, pipe.sel, pipe.window.clone())
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(st._w.cpu().numpy()), bits(ref.weights)), f"weights after step {t}"
+        assert np.array_equal(bits(res.cpu().numpy()), bits(ref.residual)), f"residual after step {t}"
+
+    pipe.capture()  # two eager steps, then the per-parity and block graphs
+    ref_steps(2, 0)
+    check(2)
+    t = 2
+    while t < 100:  # single-step graph replays
+        pipe.run(1)
+        ref_steps(1, t)
+        t += 1
+        check(t)
+    while t < 2000:  # 20-step block graphs (t even)
+        pipe.run(GTopKPipeline.kBlockSteps)
+        ref_steps(GTopKPipeline.kBlockSteps, t)
+        t += GTopKPipeline.kBlockSteps
+        check(t)
+    pipe.check()
+    assert ref.iteration == t
+    pipe.sync_state()  # the state's own residual, settled in place
+    assert st._res is pipe.res[t % 2]
+    assert np.array_equal(bits(st.residual.cpu().numpy()), bits(ref.residual))

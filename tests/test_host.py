@@ -275,3 +275,49 @@ def test_make_state_validation():
     with pytest.raises(ValueError):
         opt.OptimizerState(np.ones(4, F32), np.zeros(3, F32), 0.1)
     assert set(opt.STEP_FNS) == {"dense", "topk", "gtopk", "gtopk-naive"}
+
+
+# ---- drop-in surface ----------------------------------------------------------
+
+# reference pkg/src/gtopk/__init__.py:3-44, minus the out-of-scope modules
+# (cost_model, models: SURVEY.md §2) and the TCP mesh (ClusterConfig,
+# connect_tcp_cluster: SURVEY.md §8(f) row 4)
+REFERENCE_HOT_PATH_EXPORTS = [
+    "CollectiveStats", "GTopKResult", "allgather", "binomial_bcast", "dense_ring_allreduce", "gtopk_allreduce",
+    "topk_allreduce", "DensitySchedule", "OptimizerState", "StepReport", "dense_step", "density_at",
+    "gtopk_naive_step", "gtopk_step", "make_state", "topk_step", "IndexMask", "SparseVector", "densify",
+    "k_from_density", "masked_extract", "top_k_select", "top_op", "Endpoint", "ProtocolError", "TransportError",
+    "create_local_cluster", "decode_sparse", "encode_sparse", "run_workers",
+]
+OUT_OF_SCOPE = {"CostParams", "FitResult", "fit_alpha_beta", "scaling_efficiency", "t_dense", "t_gtopk", "t_topk",
+                "SyntheticDataset", "ToyModel", "gen_dataset", "grad", "shard_batches", "ClusterConfig",
+                "connect_tcp_cluster"}
+
+
+def test_top_level_exports_every_reference_hot_path_name():
+    import paper_1901_04359_b200 as gtopk
+
+    for name in REFERENCE_HOT_PATH_EXPORTS:
+        assert hasattr(gtopk, name), name
+        assert name in dir(gtopk) and name in gtopk.__all__, name
+    # the lazily resolved names are the submodules' own objects
+    assert gtopk.gtopk_step is opt.gtopk_step and gtopk.gtopk_allreduce is coll.gtopk_allreduce
+    assert gtopk.STEP_FNS["gtopk"] is opt.gtopk_step
+    with pytest.raises(AttributeError):
+        gtopk.no_such_name  # noqa: B018
+
+
+def test_export_list_matches_reference_init():
+    """The list above is the reference's own __init__ (checked where the
+    reference checkout exists, i.e. in the build container)."""
+    import ast
+    import os
+
+    path = "/root/reference/pkg/src/gtopk/__init__.py"
+    if not os.path.exists(path):
+        pytest.skip("reference checkout not present")
+    names = set()
+    for node in ast.parse(open(path).read()).body:
+        if isinstance(node, ast.ImportFrom):
+            names |= {a.name for a in node.names}
+    assert names == set(REFERENCE_HOT_PATH_EXPORTS) | OUT_OF_SCOPE
