@@ -50,7 +50,8 @@ extern "C" {
 #define GTK_DEV_TIMEOUT 0x4u    /* peer flag wait timed out */
 #define GTK_DEV_ABORTED 0x8u    /* abort flag observed */
 #define GTK_DEV_PEER_FAILED 0x10u /* a peer's step failed (poisoned message received) */
-#define GTK_DEV_ERROR_MASK 0x1Du  /* every bit except the informational FALLBACK */
+#define GTK_DEV_PENDING 0x20u   /* plain select of a residual with unsettled chained winners (gtk_select_settle) */
+#define GTK_DEV_ERROR_MASK 0x3Du  /* every bit except the informational FALLBACK */
 
 /* gtk_select flags */
 #define GTK_SELECT_FORCE_EXACT 0x1 /* skip the sampled-threshold fast path (testing) */

@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgtopk_b200.so")
+# GTK_LIB_PATH: an alternative in-tree build (A/B measurements of compile-time variants)
+LIB_PATH = os.environ.get("GTK_LIB_PATH") or os.path.join(_HERE, "libgtopk_b200.so")
 
 GTK_OK = 0
 GTK_EINVAL = 1
@@ -28,7 +29,8 @@ DEV_FALLBACK = 0x2
 DEV_TIMEOUT = 0x4
 DEV_ABORTED = 0x8
 DEV_PEER_FAILED = 0x10
-DEV_ERROR_MASK = 0x1D
+DEV_PENDING = 0x20
+DEV_ERROR_MASK = 0x3D
 
 SELECT_FORCE_EXACT = 0x1
 SELECT_CHAIN = 0x2

@@ -128,6 +128,10 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   bool pushed = (a.steps[0].tag & kStepPrepushed) != 0;
   for (int s = 0; s < a.nsteps; ++s) {
     const Step st = a.steps[s];
+    // the merges' predicted-band gather counter of the step after this one
+    // (see MergeCtl::spec_n)
+    const uint32_t seq = (uint32_t)(epoch * (uint64_t)a.nsteps + (uint64_t)s);
+    if (blk == 0 && threadIdx.x == 0) a.merge.ctl->spec_n[(seq + 1u) & 1u] = 0u;
     // the next step sends the list this step's merge / copy produces: fuse
     const bool fuse_next = s + 1 < a.nsteps && a.steps[s + 1].send_to >= 0;
     if (st.send_to >= 0 && !pushed) {
@@ -202,7 +206,7 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
           m.ll_head = out_slot;
           m.ll_tag = tag;
         }
-        merge_device(m, n_in, n_own, hint_in, hint_own, G, S, wrec, wv);
+        merge_device(m, n_in, n_own, hint_in, hint_own, G, S, wrec, wv, seq);
       } else {
         const uint32_t per = (n_in + G - 1) / G;
         const uint32_t e0 = min(n_in, blk * per), e1 = min(n_in, e0 + per);
@@ -465,12 +469,11 @@ static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32
   a.merge = MergeArgs{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, (uint32_t)k, nullptr, nullptr,
                       nullptr, (MergeCtl*)(base + L.ctl), (EngineWS*)(base + L.engine),
                       (int32_t*)(base + L.u_idx), (float*)(base + L.u_val)};
-  uint32_t sc = 0;
-  int G = merge_grid_for((const void*)exchange_kernel, k, &sc);
-  if (G <= 0) return GTK_ECUDA;
-  a.merge.slice_cap = sc;
+  MergeGrid g;
+  if (!merge_grid_for((const void*)exchange_kernel, k, &g)) return GTK_ECUDA;
+  a.merge.slice_cap = g.slice_cap;
   void* args[] = {&a};
   ProfScope prof(kProfExchange, (cudaStream_t)stream);
-  return coop_launch((const void*)exchange_kernel, G, kMergeThreads, args, merge_smem_bytes(sc), (cudaStream_t)stream,
-                     true);
+  return merge_launch((const void*)exchange_kernel, g, args, merge_smem_bytes(g.slice_cap), (cudaStream_t)stream,
+                      true);
 }

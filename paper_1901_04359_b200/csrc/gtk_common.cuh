@@ -216,7 +216,27 @@ __device__ __forceinline__ uint64_t ld_acquire_gpu_u64(const uint64_t* p) {
 // generation with one more release add; the others acquire the new
 // generation; bar.sync then extends the ordering to the whole block.
 // Cross-block data is read with ld.global.cg.
+//
+// A grid that is one thread-block cluster (cluster-mode merges) synchronises
+// with barrier.cluster instead: release/acquire at cluster scope orders the
+// blocks' global-memory writes too, and no global word is touched.
+__device__ __forceinline__ uint32_t cluster_ncta() {
+  uint32_t n;
+  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(n));
+  return n;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void grid_sync(GridBarrier* b, unsigned nblocks) {
+  if (nblocks == 1) {
+    __syncthreads();
+    return;
+  }
+  if (cluster_ncta() == nblocks) {
+    cluster_sync_all();
+    return;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     uint64_t* word = reinterpret_cast<uint64_t*>(b);

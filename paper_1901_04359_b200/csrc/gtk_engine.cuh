@@ -357,6 +357,206 @@ __device__ void engine_write(const Src& src, uint32_t s0, uint32_t s1, uint32_t 
   }
 }
 
+// ---- finish from a band [blo, bhi) of keys that holds the rank-kt key ----
+// Every block gathers its in-band entries (key, idx, block | slot) into the
+// shared gather buffer (gcount: its global counter; nullptr = G == 1, all in
+// shared memory) and counts its entries above the band; after ONE grid
+// barrier every block ranks the gathered keys (tau = the kt-th largest key,
+// ties at tau by index), derives its output offset and writes its winners.
+// t_band > 0: the rank of the target inside the band, known from a
+// histogram (the band holds it by construction).  t_band = 0: a band
+// predicted from the previous call (merge_device): the blocks sum their
+// above-band counts after the barrier, t_band = kt - that sum, and they
+// return false -- consistently -- when rank kt is not inside the band or the
+// band overflowed the gather buffer; the caller then runs the histogram path
+// (nothing was written but the gather buffer and ws->cta_a).
+// clear_hists: block 0 zeroes the round histograms at the end (they were used).
+// *tau_out (nullable, block 0): the k-th key.
+template <int NT, class Src>
+__device__ bool engine_band_finish(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt, uint32_t t_band,
+                               uint64_t blo, uint64_t bhi, uint32_t* gcount, EngineWS* ws,
+                               EngineSmem<NT>& sm, const Sink& out, unsigned G, bool clear_hists,
+                               uint32_t* tau_out = nullptr) {
+  const unsigned blk = blockIdx.x;
+  const bool solo = gcount == nullptr;
+  const bool above_known = t_band != 0;
+  uint32_t n_above = 0, above_all = 0;
+  if (solo && threadIdx.x == 0) sm.ng = 0;
+  if (solo) __syncthreads();
+  // (block-uniform trip count: the in-bin slots are reserved with one
+  // atomic per warp)
+  for (uint32_t sb0 = s0; sb0 < s1; sb0 += NT) {
+    const uint32_t s = sb0 + threadIdx.x;
+    uint32_t key = 0;
+    int32_t i = 0;
+    float v;
+    const bool valid = s < s1 && src.get(s, key, i, v);
+    n_above += valid && (uint64_t)key >= bhi;
+    const bool inb = valid && (uint64_t)key < bhi && key >= blo;
+    // a potential winner: its w line (fused update) heads for L2 now, so
+    // the write phase's read-modify-write after the barrier hits there
+    if (out.upd_w && valid && key >= blo) prefetch_l2(out.upd_w + i);
+    const unsigned bal = __ballot_sync(kFull, inb);
+    if (bal == 0u) continue;
+    uint32_t p0 = 0;
+    if (lane_id() == (unsigned)(__ffs(bal) - 1))
+      p0 = atomicAdd(solo ? &sm.ng : gcount, (uint32_t)__popc(bal));
+    p0 = __shfl_sync(kFull, p0, __ffs(bal) - 1);
+    if (inb) {
+      const uint32_t p = p0 + __popc(bal & lanemask_lt());
+      if (p >= (uint32_t)kGatherCap) continue;  // overflow: only a predicted band (checked below)
+      if (solo) {
+        sm.keys[p] = key;
+        sm.gidx[p] = i;
+        sm.gblk[p] = (blk << kSlotBits) | min(s - s0, kSlotMax);
+      } else {
+        ws->gather_key[p] = key;
+        ws->gather_idx[p] = i;
+        ws->gather_blk[p] = (blk << kSlotBits) | min(s - s0, kSlotMax);
+      }
+    }
+  }
+  n_above = block_sum<NT>(n_above, sm.scan);
+  uint32_t above_before = 0;
+  if (!solo) {
+    if (threadIdx.x == 0) ws->cta_a[blk] = n_above;
+    grid_sync(&ws->bar, G);
+    // one round trip: the count, the (at most kGatherMax) gathered entries
+    // and the per-block counts are independent loads
+    const uint32_t ng = min(__ldcg(gcount), (uint32_t)kGatherCap + 1u);
+    for (uint32_t j = threadIdx.x; j < (uint32_t)kGatherMax; j += NT) {
+      sm.keys[j] = __ldcg(&ws->gather_key[j]);
+      sm.gidx[j] = __ldcg(&ws->gather_idx[j]);
+      sm.gblk[j] = __ldcg(&ws->gather_blk[j]);
+    }
+    for (uint32_t j = kGatherMax + threadIdx.x; j < ng; j += NT) {  // last-round bins up to kGatherCap
+      sm.keys[j] = __ldcg(&ws->gather_key[j]);
+      sm.gidx[j] = __ldcg(&ws->gather_idx[j]);
+      sm.gblk[j] = __ldcg(&ws->gather_blk[j]);
+    }
+    for (unsigned j = threadIdx.x; j < (above_known ? blk : G); j += NT) {
+      const uint32_t c = __ldcg(&ws->cta_a[j]);
+      if (j < blk) above_before += c;
+      else above_all += c;
+    }
+    if (threadIdx.x == 0) sm.ng = ng;
+  }
+  above_before = block_sum<NT>(above_before, sm.scan);  // also publishes sm.keys / sm.ng
+  uint32_t t_in = t_band;  // rank of the target inside the band
+  if (!above_known) {
+    const uint32_t above = solo ? n_above : above_before + block_sum<NT>(above_all, sm.scan);
+    const uint32_t ngc = sm.ng;
+    if (ngc > (uint32_t)kGatherCap || above >= kt || kt > above + ngc) return false;  // the band missed
+    t_in = kt - above;
+  }
+  sink_stamp(out, 1);
+  const uint32_t ng = sm.ng;
+  // tau = t_in-th largest gathered key; gt = # gathered keys > tau.  A
+  // large gather is first narrowed in shared memory: a 2048-way histogram
+  // of the bin [blo, bhi) over the gathered keys (every block holds the
+  // same gathered set, so no barrier), then the O(n^2) rank runs only over
+  // the sub-bin holding t_in.
+  const uint32_t* rk = sm.keys;  // the keys ranked below
+  uint32_t nr = ng, r_t = t_in, r_above = 0;
+  if (ng > (uint32_t)kRankDirect) {
+    const uint64_t width = bhi - blo;
+    const uint32_t ss = width <= (uint64_t)kBins ? 0u : ceil_log2_u64((width + kBins - 1) / kBins);
+    for (int b = threadIdx.x; b < kHistLen; b += NT) sm.hist[b] = 0;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < ng; j += NT) atomicAdd(&sm.hist[(sm.keys[j] - (uint32_t)blo) >> ss], 1u);
+    __syncthreads();
+    uint32_t sb, sab, sin;
+    engine_find_bin<NT>(sm.hist, true, t_in, sm, sb, sab, sin);
+    const uint32_t r_lo = (uint32_t)blo + (sb << ss), r_hi = r_lo + ((1u << ss) - 1u);  // inclusive
+    if (threadIdx.x == 0) sm.bcast[7] = 0;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < ng; j += NT) {  // the sub-bin's keys -> sm.hist[0, sin)
+      const uint32_t x = sm.keys[j];
+      if (x >= r_lo && x <= r_hi) sm.hist[atomicAdd(&sm.bcast[7], 1u)] = x;
+    }
+    rk = sm.hist;
+    nr = sin;
+    r_t = t_in - sab;
+    r_above = sab;
+  }
+  if (threadIdx.x == 0) sm.bcast[3] = sm.bcast[4] = 0;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < nr; j += NT) {
+    const uint32_t x = rk[j];
+    uint32_t gt = 0, ge = 0;
+    for (uint32_t q = 0; q < nr; ++q) {
+      const uint32_t y = rk[q];
+      gt += (y > x);
+      ge += (y >= x);
+    }
+    if (gt < r_t && ge >= r_t) {
+      sm.bcast[3] = x;
+      sm.bcast[4] = r_above + gt;
+    }
+  }
+  __syncthreads();
+  const uint32_t tau = sm.bcast[3];
+  const uint32_t need = t_in - sm.bcast[4];  // entries with key == tau to keep, lowest idx first
+  sink_stamp(out, 2);
+  // kept flags of the gathered entries: winners of my slice go to a
+  // bitmap indexed by slot (O(1) lookup in the write), the ones of
+  // earlier blocks shift my output offset
+  // the gathered entries equal to tau (their indices) -> sm.hist[0, n_eq):
+  // the index-order tie ranks run over that short list only
+  for (uint32_t w = threadIdx.x; w < kKeptBits / 32; w += NT) sm.kept_bits[w] = 0;
+  if (threadIdx.x == 0) sm.bcast[7] = 0;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < ng; j += NT)
+    if (sm.keys[j] == tau) sm.hist[atomicAdd(&sm.bcast[7], 1u)] = (uint32_t)sm.gidx[j];
+  __syncthreads();
+  const uint32_t n_eq = sm.bcast[7];
+  uint32_t extra = 0;
+  for (uint32_t j = threadIdx.x; j < ng; j += NT) {
+    const uint32_t x = sm.keys[j];
+    bool kept = x > tau;
+    if (x == tau) {
+      uint32_t rank = 0;
+      const int32_t ij = sm.gidx[j];
+      for (uint32_t q = 0; q < n_eq; ++q) rank += (int32_t)sm.hist[q] < ij;
+      kept = rank < need;
+      if (out.pend_rec && blk == 0 && rank + 1 == need) out.pend_rec[7] = (uint32_t)ij;  // the last kept tie
+    }
+    const uint32_t gb = sm.gblk[j] >> kSlotBits, slot = sm.gblk[j] & ((1u << kSlotBits) - 1);
+    if (kept) {
+      if (gb < blk) ++extra;
+      // (a slot beyond the bitmap -- large global-mode slice -- is found
+      // by the scan in keep_fn instead)
+      if (gb == blk && slot < kKeptBits) atomicOr(&sm.kept_bits[slot >> 5], 1u << (slot & 31));
+    } else {
+      sm.gblk[j] = 0xFFFFFFFFu;  // mark "not kept" for the large-slice scan
+    }
+  }
+  extra = block_sum<NT>(extra, sm.scan);
+  const uint32_t bl = (uint32_t)blo, bh32 = (uint32_t)min(bhi, (uint64_t)0xFFFFFFFFu);
+  const bool bh_max = bhi > 0xFFFFFFFFull;
+  auto keep_fn = [&](uint32_t key, int32_t i, uint32_t slot) -> bool {
+    if (!bh_max && key >= bh32) return true;
+    if (key < bl) return false;
+    if (slot < kKeptBits) return (sm.kept_bits[slot >> 5] >> (slot & 31)) & 1u;
+    for (uint32_t q = 0; q < ng; ++q)
+      if (sm.gidx[q] == i) return sm.gblk[q] != 0xFFFFFFFFu;
+    return false;
+  };
+  engine_write<NT>(src, s0, s1, above_before + extra, keep_fn, sm, out);
+  sink_stamp(out, 3);
+  if (blk == 0) {  // every block is past its last histogram read
+    if (clear_hists)
+      for (int rr = 0; rr < kRounds; ++rr)
+        for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[rr][b] = 0;
+    if (threadIdx.x == 0) {
+      sink_count(out, kt, tau);
+      sink_pending(out, tau);
+      if (tau_out) *tau_out = tau;
+    }
+  }
+  return true;
+}
+
 // The engine proper.  Every block calls it with its own slice [s0, s1).
 // hist0: the round-0 histogram over [lo0, 2^31) with bin width 2^shift0,
 //        already complete (global: built before a grid barrier / by an earlier
@@ -499,167 +699,8 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
     const bool single_key = (bhi - blo == 1);
     // the last round always gathers if it can (a bin is then at most 8 keys wide)
     if (in_bin <= (uint32_t)kGatherCap) {
-      // ---- finish with one barrier: gather (key, idx, block) of the bin ------
-      uint32_t n_above = 0;
-      if (solo && threadIdx.x == 0) sm.ng = 0;
-      if (solo) __syncthreads();
-      // (block-uniform trip count: the in-bin slots are reserved with one
-      // atomic per warp)
-      for (uint32_t sb0 = s0; sb0 < s1; sb0 += NT) {
-        const uint32_t s = sb0 + threadIdx.x;
-        uint32_t key = 0;
-        int32_t i = 0;
-        float v;
-        const bool valid = s < s1 && src.get(s, key, i, v);
-        n_above += valid && (uint64_t)key >= bhi;
-        const bool inb = valid && (uint64_t)key < bhi && key >= blo;
-        // a potential winner: its w line (fused update) heads for L2 now, so
-        // the write phase's read-modify-write after the barrier hits there
-        if (out.upd_w && valid && key >= blo) prefetch_l2(out.upd_w + i);
-        const unsigned bal = __ballot_sync(kFull, inb);
-        if (bal == 0u) continue;
-        uint32_t p0 = 0;
-        if (lane_id() == (unsigned)(__ffs(bal) - 1))
-          p0 = atomicAdd(solo ? &sm.ng : &ws->gather_n[r], (uint32_t)__popc(bal));
-        p0 = __shfl_sync(kFull, p0, __ffs(bal) - 1);
-        if (inb) {
-          const uint32_t p = p0 + __popc(bal & lanemask_lt());
-          if (solo) {
-            sm.keys[p] = key;
-            sm.gidx[p] = i;
-            sm.gblk[p] = (blk << kSlotBits) | min(s - s0, kSlotMax);
-          } else {
-            ws->gather_key[p] = key;
-            ws->gather_idx[p] = i;
-            ws->gather_blk[p] = (blk << kSlotBits) | min(s - s0, kSlotMax);
-          }
-        }
-      }
-      n_above = block_sum<NT>(n_above, sm.scan);
-      uint32_t above_before = 0;
-      if (!solo) {
-        if (threadIdx.x == 0) ws->cta_a[blk] = n_above;
-        grid_sync(&ws->bar, G);
-        // one round trip: the count, the (at most kGatherMax) gathered entries
-        // and the per-block counts are independent loads
-        const uint32_t ng = __ldcg(&ws->gather_n[r]);
-        for (uint32_t j = threadIdx.x; j < (uint32_t)kGatherMax; j += NT) {
-          sm.keys[j] = __ldcg(&ws->gather_key[j]);
-          sm.gidx[j] = __ldcg(&ws->gather_idx[j]);
-          sm.gblk[j] = __ldcg(&ws->gather_blk[j]);
-        }
-        for (uint32_t j = kGatherMax + threadIdx.x; j < ng; j += NT) {  // last-round bins up to kGatherCap
-          sm.keys[j] = __ldcg(&ws->gather_key[j]);
-          sm.gidx[j] = __ldcg(&ws->gather_idx[j]);
-          sm.gblk[j] = __ldcg(&ws->gather_blk[j]);
-        }
-        for (unsigned j = threadIdx.x; j < blk; j += NT) above_before += __ldcg(&ws->cta_a[j]);
-        if (threadIdx.x == 0) sm.ng = ng;
-      }
-      above_before = block_sum<NT>(above_before, sm.scan);  // also publishes sm.keys / sm.ng
-      sink_stamp(out, 1);
-      const uint32_t ng = sm.ng;
-      // tau = t_in-th largest gathered key; gt = # gathered keys > tau.  A
-      // large gather is first narrowed in shared memory: a 2048-way histogram
-      // of the bin [blo, bhi) over the gathered keys (every block holds the
-      // same gathered set, so no barrier), then the O(n^2) rank runs only over
-      // the sub-bin holding t_in.
-      const uint32_t* rk = sm.keys;  // the keys ranked below
-      uint32_t nr = ng, r_t = t_in, r_above = 0;
-      if (ng > (uint32_t)kRankDirect) {
-        const uint64_t width = bhi - blo;
-        const uint32_t ss = width <= (uint64_t)kBins ? 0u : ceil_log2_u64((width + kBins - 1) / kBins);
-        for (int b = threadIdx.x; b < kHistLen; b += NT) sm.hist[b] = 0;
-        __syncthreads();
-        for (uint32_t j = threadIdx.x; j < ng; j += NT) atomicAdd(&sm.hist[(sm.keys[j] - (uint32_t)blo) >> ss], 1u);
-        __syncthreads();
-        uint32_t sb, sab, sin;
-        engine_find_bin<NT>(sm.hist, true, t_in, sm, sb, sab, sin);
-        const uint32_t r_lo = (uint32_t)blo + (sb << ss), r_hi = r_lo + ((1u << ss) - 1u);  // inclusive
-        if (threadIdx.x == 0) sm.bcast[7] = 0;
-        __syncthreads();
-        for (uint32_t j = threadIdx.x; j < ng; j += NT) {  // the sub-bin's keys -> sm.hist[0, sin)
-          const uint32_t x = sm.keys[j];
-          if (x >= r_lo && x <= r_hi) sm.hist[atomicAdd(&sm.bcast[7], 1u)] = x;
-        }
-        rk = sm.hist;
-        nr = sin;
-        r_t = t_in - sab;
-        r_above = sab;
-      }
-      if (threadIdx.x == 0) sm.bcast[3] = sm.bcast[4] = 0;
-      __syncthreads();
-      for (uint32_t j = threadIdx.x; j < nr; j += NT) {
-        const uint32_t x = rk[j];
-        uint32_t gt = 0, ge = 0;
-        for (uint32_t q = 0; q < nr; ++q) {
-          const uint32_t y = rk[q];
-          gt += (y > x);
-          ge += (y >= x);
-        }
-        if (gt < r_t && ge >= r_t) {
-          sm.bcast[3] = x;
-          sm.bcast[4] = r_above + gt;
-        }
-      }
-      __syncthreads();
-      const uint32_t tau = sm.bcast[3];
-      const uint32_t need = t_in - sm.bcast[4];  // entries with key == tau to keep, lowest idx first
-      sink_stamp(out, 2);
-      // kept flags of the gathered entries: winners of my slice go to a
-      // bitmap indexed by slot (O(1) lookup in the write), the ones of
-      // earlier blocks shift my output offset
-      // the gathered entries equal to tau (their indices) -> sm.hist[0, n_eq):
-      // the index-order tie ranks run over that short list only
-      for (uint32_t w = threadIdx.x; w < kKeptBits / 32; w += NT) sm.kept_bits[w] = 0;
-      if (threadIdx.x == 0) sm.bcast[7] = 0;
-      __syncthreads();
-      for (uint32_t j = threadIdx.x; j < ng; j += NT)
-        if (sm.keys[j] == tau) sm.hist[atomicAdd(&sm.bcast[7], 1u)] = (uint32_t)sm.gidx[j];
-      __syncthreads();
-      const uint32_t n_eq = sm.bcast[7];
-      uint32_t extra = 0;
-      for (uint32_t j = threadIdx.x; j < ng; j += NT) {
-        const uint32_t x = sm.keys[j];
-        bool kept = x > tau;
-        if (x == tau) {
-          uint32_t rank = 0;
-          const int32_t ij = sm.gidx[j];
-          for (uint32_t q = 0; q < n_eq; ++q) rank += (int32_t)sm.hist[q] < ij;
-          kept = rank < need;
-          if (out.pend_rec && blk == 0 && rank + 1 == need) out.pend_rec[7] = (uint32_t)ij;  // the last kept tie
-        }
-        const uint32_t gb = sm.gblk[j] >> kSlotBits, slot = sm.gblk[j] & ((1u << kSlotBits) - 1);
-        if (kept) {
-          if (gb < blk) ++extra;
-          // (a slot beyond the bitmap -- large global-mode slice -- is found
-          // by the scan in keep_fn instead)
-          if (gb == blk && slot < kKeptBits) atomicOr(&sm.kept_bits[slot >> 5], 1u << (slot & 31));
-        } else {
-          sm.gblk[j] = 0xFFFFFFFFu;  // mark "not kept" for the large-slice scan
-        }
-      }
-      extra = block_sum<NT>(extra, sm.scan);
-      const uint32_t bl = (uint32_t)blo, bh32 = (uint32_t)min(bhi, (uint64_t)0xFFFFFFFFu);
-      const bool bh_max = bhi > 0xFFFFFFFFull;
-      auto keep_fn = [&](uint32_t key, int32_t i, uint32_t slot) -> bool {
-        if (!bh_max && key >= bh32) return true;
-        if (key < bl) return false;
-        if (slot < kKeptBits) return (sm.kept_bits[slot >> 5] >> (slot & 31)) & 1u;
-        for (uint32_t q = 0; q < ng; ++q)
-          if (sm.gidx[q] == i) return sm.gblk[q] != 0xFFFFFFFFu;
-        return false;
-      };
-      engine_write<NT>(src, s0, s1, above_before + extra, keep_fn, sm, out);
-      sink_stamp(out, 3);
-      if (blk == 0) {  // every block is past its last histogram read
-        for (int rr = 0; rr < kRounds; ++rr)
-          for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[rr][b] = 0;
-        if (threadIdx.x == 0) {
-          sink_count(out, kt, tau);
-          sink_pending(out, tau);
-        }
-      }
+      engine_band_finish<NT>(src, s0, s1, kt, t_in, blo, bhi, solo ? nullptr : &ws->gather_n[r], ws, sm, out, G,
+                             true);
       return true;
     }
     if (single_key) {

@@ -19,8 +19,19 @@ int coop_launch(const void* func, int grid, int threads, void** args, size_t sme
                 bool pdl = false);
 // opt a kernel into > 48 KB of dynamic shared memory (once per device); false on error
 bool ensure_dyn_smem(const void* func, size_t bytes);
-// blocks for a cooperative ⊤-merge kernel over lists of <= cap entries
-int merge_grid_for(const void* func, int32_t cap, uint32_t* slice_cap);
+// grid of a ⊤-merge kernel (merge_kernel / exchange_kernel) over lists of
+// <= cap entries: G blocks of kMergeThreads, slice_cap union slots staged in
+// shared memory per block, and either one thread-block cluster of G CTAs
+// (cluster = true: the engine's grid barriers become barrier.cluster) or a
+// cooperative grid
+struct MergeGrid {
+  int G;
+  uint32_t slice_cap;
+  bool cluster;
+};
+bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out);
+// launch a merge-type kernel on its MergeGrid (cluster or cooperative)
+int merge_launch(const void* func, const MergeGrid& g, void** args, size_t smem, cudaStream_t st, bool pdl);
 
 // Launch with the programmatic-stream-serialization attribute: the kernel may
 // start as soon as the previous kernel in the stream executes

@@ -3,6 +3,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 
 #include "gtk_internal.h"
 #include "gtk_merge.cuh"
@@ -17,37 +21,128 @@ __global__ void __launch_bounds__(kMergeThreads, 1) merge_kernel(MergeArgs a) {
   merge_device(a, na, nb, ha, hb, gridDim.x, S);
 }
 
-// blocks and shared-memory slice capacity for a merge of two lists of <= cap
-// entries: ~512 merged slots per block (the engine's phases are latency-bound,
-// more blocks shorten each: measured 2048 -> 512 takes k = 25.6K from 21 to
-// 16.5 us), at most one block per SM; the slice capacity covers the expected
-// slice (large k) up to kMergeSliceCapMax
-int merge_grid_for(const void* func, int32_t cap, uint32_t* slice_cap) {
-  if (!ensure_dyn_smem(func, merge_smem_bytes(kMergeSliceCapMax))) return 0;
+// Grid of a merge over two lists of <= cap entries.
+//  * cluster (default while the union fits the shared memory of <= 16 CTAs):
+//    one thread-block cluster of G CTAs, ~kMergeClusterSlots union slots each;
+//    the engine's barriers are barrier.cluster (~0.2 us) instead of the
+//    global-atomic grid barrier (~2-5 us with block skew).
+//  * cooperative grid: ~512 merged slots per block (the engine's phases are
+//    latency-bound, more blocks shorten each: measured 2048 -> 512 takes
+//    k = 25.6K from 21 to 16.5 us), at most one block per SM.
+// Either way the slice capacity covers the expected slice up to
+// kMergeSliceCapMax.  GTK_MERGE_GRID=n / GTK_MERGE_CLUSTER=0|1 override the
+// choice (measurements).
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
+static bool cluster_fits(const void* func, int cs, size_t smem) {
+  static std::mutex mu;
+  static std::unordered_map<unsigned long long, bool> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  const unsigned long long key = ((unsigned long long)(uintptr_t)func) ^ ((unsigned long long)dev << 56) ^
+                                 ((unsigned long long)cs << 40) ^ (unsigned long long)smem;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  bool ok = true;
+  if (cs > 8 && cudaFuncSetAttribute(func, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) ok = false;
+  if (ok) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kMergeThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = cs;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    ok = cudaOccupancyMaxActiveClusters(&n, func, &cfg) == cudaSuccess && n >= 1;
+  }
+  cudaGetLastError();  // a refused size is an answer, not an error
+  cache[key] = ok;
+  return ok;
+}
+
+bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out) {
+  if (!ensure_dyn_smem(func, merge_smem_bytes(kMergeSliceCapMax))) return false;
   const int lim = num_sms();
-  if (lim <= 0) return 0;
-  const int want = (int)((2LL * cap + kMergeSlotsPerBlock - 1) / kMergeSlotsPerBlock);
-  int g = want < lim ? (want < 1 ? 1 : want) : lim;
+  if (lim <= 0) return false;
+  const uint64_t slots = 2ull * (uint64_t)(cap < 1 ? 1 : cap);
+  const int force_g = env_int("GTK_MERGE_GRID", 0), force_c = env_int("GTK_MERGE_CLUSTER", -1);
+  auto cap_for = [&](int g) {
+    const uint64_t per = (slots + g - 1) / g;
+    uint32_t sc = kMergeSliceCap;
+    if (per > sc) sc = (uint32_t)std::min<uint64_t>((per + 255) & ~255ull, kMergeSliceCapMax);
+    return sc;
+  };
+  // cluster candidate
+  const uint64_t want_c = slots <= (uint64_t)kMergeSoloSlots ? 1 : (slots + kMergeClusterSlots - 1) / kMergeClusterSlots;
+  int gc = (int)std::min<uint64_t>(want_c, kMergeMaxCluster);
+  if (force_g > 0) gc = std::min(force_g, kMergeMaxCluster);
+  if (gc < 1) gc = 1;
+  const bool c_smem = (slots + gc - 1) / gc <= (uint64_t)kMergeSliceCapMax;
+  // cluster mode only where the union spreads over <= 16 CTAs at the target density
+  bool use_cluster = force_c != 0 && c_smem && (force_g > 0 ? force_g <= kMergeMaxCluster
+                                                             : (force_c == 1 || want_c <= (uint64_t)kMergeMaxCluster));
+  if (force_c == 1 && !c_smem) return false;
+  if (use_cluster) {
+    const uint32_t sc = cap_for(gc);
+    if (gc == 1 || cluster_fits(func, gc, merge_smem_bytes(sc))) {
+      *out = MergeGrid{gc, sc, gc > 1};
+      return true;
+    }
+    if (force_c == 1) return false;
+  }
+  const int want = (int)((slots + kMergeSlotsPerBlock - 1) / kMergeSlotsPerBlock);
+  int g = force_g > 0 ? force_g : (want < lim ? (want < 1 ? 1 : want) : lim);
   if (g > kMaxBlocks) g = kMaxBlocks;
-  const uint64_t per = (2ull * (uint64_t)cap + g - 1) / g;
-  uint32_t sc = kMergeSliceCap;
-  if (per > sc) sc = (uint32_t)std::min<uint64_t>((per + 255) & ~255ull, kMergeSliceCapMax);
+  const uint32_t sc = cap_for(g);
   const int co = coop_grid(func, kMergeThreads, merge_smem_bytes(sc));
-  if (co <= 0) return 0;
+  if (co <= 0) return false;
   if (g > co) g = co;
-  *slice_cap = sc;
-  return g;
+  *out = MergeGrid{g, sc, false};
+  return true;
+}
+
+int merge_launch(const void* func, const MergeGrid& g, void** args, size_t smem, cudaStream_t st, bool pdl) {
+  if (!g.cluster) return coop_launch(func, g.G, kMergeThreads, args, smem, st, pdl);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.G);
+  cfg.blockDim = dim3(kMergeThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = g.G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 2 : 1;
+  const cudaError_t e = cudaLaunchKernelExC(&cfg, func, args);
+  if (e != cudaSuccess) {
+    set_last_cuda_error(e);
+    return GTK_ECUDA;
+  }
+  count_launch();
+  return GTK_OK;
 }
 
 int launch_merge(const MergeArgs& args, int32_t cap, cudaStream_t st) {
-  uint32_t sc = 0;
-  const int G = merge_grid_for((const void*)merge_kernel, cap, &sc);
-  if (G <= 0) return GTK_ECUDA;
+  MergeGrid g;
+  if (!merge_grid_for((const void*)merge_kernel, cap, &g)) return GTK_ECUDA;
   MergeArgs a = args;
-  a.slice_cap = sc;
+  a.slice_cap = g.slice_cap;
   void* p[] = {&a};
   ProfScope prof(kProfMerge, st);
-  return coop_launch((const void*)merge_kernel, G, kMergeThreads, p, merge_smem_bytes(sc), st);
+  return merge_launch((const void*)merge_kernel, g, p, merge_smem_bytes(g.slice_cap), st, false);
 }
 
 }  // namespace gtk

@@ -51,12 +51,13 @@ constexpr uint32_t kOvfBit = 0x80000000u;
 constexpr uint32_t kMinWindowLevel = 2;  // carried-window margin: from k (1 + 2^2 / 2) = 3k candidates
 constexpr uint32_t kMaxWindowLevel = 4;  // ... up to k (1 + 2^4 / 2) = 9k
 
+constexpr uint32_t kCtlPendingViolation = 2u;
 struct SelectCtl {
   uint32_t lo;
   uint32_t shift;
   uint32_t ovf_cursor;
   uint32_t overflow;
-  uint32_t nonfinite;
+  uint32_t nonfinite;  // 1: non-finite input (main pass); kCtlPendingViolation (sample kernel)
   uint32_t sample_done;  // sample-block ticket (atomicInc, wraps to 0 per launch)
   uint32_t pad[10];
 };
@@ -285,6 +286,14 @@ __device__ __forceinline__ void sample_stamp(const SampleArgs& a, int i, bool wh
   }
 }
 
+// a plain (unchained) select of a residual whose winners a chained call left
+// pending (include/gtopk_b200.h: settle first): the finish fails the call with
+// GTK_DEV_PENDING (the main pass never reads the record: any dependent load
+// there measured +9 us per pass)
+__device__ __forceinline__ uint32_t pending_violation(const SampleArgs& a) {
+  return (a.window && a.res && (__ldcg(a.window) & kRecPending)) ? kCtlPendingViolation : 0u;
+}
+
 __global__ void __launch_bounds__(kSampleThreads) select_sample_kernel(SampleArgs a) {
   __shared__ LevelSmem sm;
   __shared__ uint32_t s_n, s_last;
@@ -304,7 +313,7 @@ __global__ void __launch_bounds__(kSampleThreads) select_sample_kernel(SampleArg
         ctl->shift = __ldcg(a.window + 2);
         ctl->ovf_cursor = 0;
         ctl->overflow = 0;
-        ctl->nonfinite = 0;
+        ctl->nonfinite = pending_violation(a);
       }
     }
     return;
@@ -396,7 +405,7 @@ __global__ void __launch_bounds__(kSampleThreads) select_sample_kernel(SampleArg
     ctl->shift = shift;
     ctl->ovf_cursor = 0;
     ctl->overflow = 0;
-    ctl->nonfinite = 0;
+    ctl->nonfinite = pending_violation(a);
   }
 }
 
@@ -471,7 +480,7 @@ __device__ __forceinline__ bool main_tile(const MainArgs& a, uint32_t tile, cons
       nonfinite |= in && key >= kInfKey;
       if (in && key >= lo) flags |= 1u << (q * 4 + j);
     }
-  if (__any_sync(kFull, nonfinite) && lane == 0) a.ctl->nonfinite = 1u;
+  if (__any_sync(kFull, nonfinite) && lane == 0) atomicOr(&a.ctl->nonfinite, 1u);
 
   // index-ordered in-tile offsets, order (q, warp, lane, j): per-lane counts of
   // the four q segments packed two per word (16-bit fields: a warp's segment
@@ -566,7 +575,12 @@ __device__ __forceinline__ bool main_tile(const MainArgs& a, uint32_t tile, cons
 }
 
 
-__global__ void __launch_bounds__(kMainThreads, 3) select_main_kernel(MainArgs a) {
+// kChain: GTK_SELECT_CHAIN calls (window from the record, pending winners of
+// res settled on the fly); the plain instance reads nothing but the sample
+// kernel's window words after griddepcontrol.wait (every dependent load there
+// delays the whole pass: the chained instance measured +2 us)
+template <bool kChain>
+__global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
   __shared__ uint32_t s_wt[2][16];  // per warp: packed candidate totals of the q segments
   __shared__ int32_t* s_didx[2];
   __shared__ float* s_dval[2];
@@ -608,7 +622,7 @@ __global__ void __launch_bounds__(kMainThreads, 3) select_main_kernel(MainArgs a
   uint32_t lo, shift;
   bool pend = false;
   uint32_t ptau = 0, pcut = 0;
-  if (a.window) {
+  if (kChain && a.window) {
     const uint32_t w0 = __ldcg(a.window);
     pend = a.res != nullptr && (w0 & kRecPending) != 0;
     ptau = __ldcg(a.window + 6);
@@ -768,13 +782,14 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
   const uint32_t wlevel = (a.window && blk == 0) ? min(kMaxWindowLevel, max(kMinWindowLevel, __ldcg(a.window) >> 8)) : kMinWindowLevel;
   const bool wsame = a.window && blk == 0 && __ldcg(a.window + 3) == a.k;
   const uint32_t wtau = wsame ? __ldcg(a.window + 4) : 0u, wtau2 = wsame ? __ldcg(a.window + 5) : 0u;
-  if (__ldcg(&a.ctl->nonfinite)) {
+  if (const uint32_t bad = __ldcg(&a.ctl->nonfinite)) {
     grid_sync(&a.ews->bar, G);  // every block has read the counters
     if (blk == 0) {
       for (int b = threadIdx.x; b < kHistLen; b += kFinishThreads) a.ews->hist[0][b] = 0;
       reset_select_counters(a, G);
       if (threadIdx.x == 0) {
-        atomicOr(a.d_status, GTK_DEV_NONFINITE);
+        atomicOr(a.d_status, ((bad & 1u) ? GTK_DEV_NONFINITE : 0u) |
+                                 ((bad & kCtlPendingViolation) ? GTK_DEV_PENDING : 0u));
         if (a.ll_base) {  // the exchange's first partner learns it at once: count -1 (poisoned)
           const uint32_t tag = (uint32_t)(__ldcg((const unsigned long long*)a.ll_epoch) + 1ull);
           st_ll_pair(a.ll_base + (size_t)(tag & 1u) * a.ll_slot_words, 0xFFFFFFFFu, 0u, tag);
@@ -961,7 +976,7 @@ using namespace gtk;
 // main-pass grid: two tiles per block, except that about one wave of resident
 // blocks at the end of the grid takes one tile each (a shorter drain)
 static uint32_t main_grid(uint32_t ntiles, uint32_t* n2) {
-  const int slots = coop_grid((const void*)select_main_kernel, kMainThreads, 0);  // resident blocks, all SMs
+  const int slots = coop_grid((const void*)select_main_kernel<false>, kMainThreads, 0);  // resident blocks, all SMs
   if (slots <= 0) return 0;
   uint32_t n1 = std::min<uint32_t>(ntiles, (uint32_t)slots);
   uint32_t two = (ntiles - n1) / 2;
@@ -1135,7 +1150,7 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
     const uint32_t gmain = main_grid(L.ntiles, &ma.n2);
     if (gmain == 0) return GTK_ECUDA;
     ma.trace = trace_buffer() ? trace_buffer() + 112 : nullptr;
-    GTK_CUDA(launch_pdl(select_main_kernel, dim3(gmain), dim3(kMainThreads), 0, st, ma));
+    GTK_CUDA(launch_pdl(chain ? select_main_kernel<true> : select_main_kernel<false>, dim3(gmain), dim3(kMainThreads), 0, st, ma));
     GTK_CHECK_LAUNCH();
   }
 
@@ -1202,7 +1217,7 @@ extern "C" int gtk_select_main_pass(const float* res_in, const float* grad, floa
   const uint32_t gmain = main_grid(L.ntiles, &ma.n2);
   if (gmain == 0) return GTK_ECUDA;
   for (int r = 0; r < reps; ++r) {
-    select_main_kernel<<<gmain, kMainThreads, 0, st>>>(ma);
+    select_main_kernel<false><<<gmain, kMainThreads, 0, st>>>(ma);
     GTK_CHECK_LAUNCH();
   }
   // the repeated passes accumulated histogram / counter state: clear it

@@ -290,6 +290,8 @@ def raise_status(word: int) -> None:
 
     if word & _lib.DEV_NONFINITE:
         raise FloatingPointError("non-finite values in dense input")
+    if word & _lib.DEV_PENDING:
+        raise RuntimeError("residual holds a chained select's pending winners: gtk_select_settle it first")
     if word & _lib.DEV_ABORTED:
         raise TransportError("cluster aborted")
     if word & _lib.DEV_TIMEOUT:

@@ -72,6 +72,9 @@ class GTopKPipeline:
         self.block_graph = None
         self.kernels_per_step = None
         self.use_graph = use_graph
+        # GTK_PIPE_CHAIN=1: chained selects (no sampling kernel; measured 3 us
+        # per step slower than the plain select at the headline, A/B only)
+        self.chain_ok = os.environ.get("GTK_PIPE_CHAIN", "0") == "1"
         self.chained = False  # steps leave their winners pending (settled by sync_state)
 
     # -- one step's launches (current stream) --------------------------------
@@ -79,12 +82,13 @@ class GTopKPipeline:
         grad = self.grads[parity % len(self.grads)]
         res_in, res_out = self.res[parity], self.res[1 - parity]
         if self.P == 1 and _dev.sparse_update_fusable(self.lr, self.mom):
+            chain = self.chain_ok
             # one rank: the global top-k is the selection; K3 rides on K1's
             # finish; chained selects (two launches per step: no sampling
             # kernel, the winners' residual zeroed by the next step's stream)
             _dev.select_update(res_in, grad, res_out, self.k, self.sel, self.status, self.window,
-                               self.state._w, self.lr, 1, self.scaling, chain=True)
-            self.chained = True
+                               self.state._w, self.lr, 1, self.scaling, chain=chain)
+            self.chained = chain
             return
         if self.P > 1 and _dev.sparse_update_fusable(self.lr, self.mom) and self.plan.push_slot0 is not None:
             # the selection goes to the first partner as it is written

@@ -476,3 +476,53 @@ def test_select_push_then_prepushed_exchange(P):
         assert int(lb.status.item()) & DEV_NONFINITE
         n, _h, _i, _v = decode_slot(lb.sent_slot(0, tag + 1), k, tag + 1)
         assert n == POISON
+
+
+@pytest.mark.parametrize("P,k,grid", [(2, 1500, "auto"), (4, 1500, "auto"), (4, 25_600, "auto"),
+                                      (2, 270, "auto"), (4, 3000, "grid")])
+def test_exchange_carried_band_hits_and_misses(P, k, grid, monkeypatch):
+    """Successive calls of one exchange plan: from the second call on, every
+    merge gathers a band of keys predicted from the previous call's k-th key
+    (csrc/gtk_merge.cuh predicted_band: one grid barrier instead of two).
+    The call sequence drives hits (same distribution), misses (every value
+    scaled x8: tau jumps out of the band), gather overflows (integer ties:
+    thousands of keys equal to tau) and cancellations (fewer than k union
+    entries); every call's global list is checked bitwise against the
+    oracle's tree fold, with the fused K3."""
+    import torch
+
+    from oracle import gtopk_oracle as orc
+
+    if grid == "grid":  # the cooperative grid path (cluster merges are the default at this k)
+        monkeypatch.setenv("GTK_MERGE_CLUSTER", "0")
+    rng = np.random.default_rng(4242 + P + k)
+    m = max(200_000, 12 * k)
+    scheds = schedules_for(P, "butterfly")
+    rank = P - 1
+    lb = Loopback(rank, P, scheds[rank], k, m)
+    w = torch.zeros(m, device=lb.d)
+    res = torch.zeros(m, device=lb.d)
+    seq = ["normal", "normal", "normal", "scaled", "scaled", "normal", "ties", "normal", "cancel", "normal",
+           "normal"]
+    for call, kind in enumerate(seq):
+        tag = call + 1
+        if kind == "scaled":
+            lists = [(i, (v * F32(8.0 ** (call - 2))).astype(F32)) for i, v in _lists(rng, P, m, k, "normal")]
+        else:
+            lists = _lists(rng, P, m, k, kind)
+        _sent, recv, final = simulate(lists, k, scheds)
+        for s, got in enumerate(recv[rank]):
+            if got is not None:
+                lb.prefill(s, tag, encode_slot(k, tag, *got))
+        lb.status.zero_()
+        w0 = w.cpu().numpy()
+        res0 = res.cpu().numpy()
+        word = lb.call(lists[rank], w=w, res=res, lr=0.01)
+        assert word == 0, (call, kind, hex(word))
+        want_i, want_v = orc.tree_fold(lists, k)
+        ai, av = lb.acc.to_host()
+        assert np.array_equal(ai, want_i), (P, k, call, kind)
+        assert np.array_equal(bits(av), bits(want_v)), (P, k, call, kind)
+        ew, er = _k3_expect(w0, res0, lists[rank], final[rank], 0.01, P, 0)
+        assert np.array_equal(bits(w.cpu().numpy()), bits(ew)), (P, k, call, kind)
+        assert np.array_equal(bits(res.cpu().numpy()), bits(er)), (P, k, call, kind)

@@ -527,6 +527,11 @@ def test_chained_select_update_trajectory(dev, kind):
         settled = R[cur].clone()
         dev.settle(settled, lst, win.clone())
         assert np.array_equal(settled.cpu().numpy().view(np.uint32), ref.residual.view(np.uint32)), (kind, t)
+    # a plain select of the unsettled residual is refused on the device
+    # (GTK_DEV_PENDING) instead of selecting from stale winners
+    st.zero_()
+    dev.select(R[cur], torch.from_numpy(grad(0)).to(d), R[1 - cur], k, dev.DeviceList(m, k, d), st, window=win)
+    assert int(st.item()) & 0x20, hex(int(st.item()))
     # settling in place clears the record's pending flag; the next chained
     # call then leaves the (already +0.0) winners alone
     dev.settle(R[cur], lst, win)
