@@ -144,6 +144,33 @@ int gtk_select_update(const float* res_in, const float* grad, float* res_out, in
 int gtk_select_settle(float* res, const int32_t* sel_idx, const int32_t* d_count, uint32_t* d_window,
                       void* stream);
 
+/* Deferred-settle select + fused update (P = 1 training loop, the
+ * pipeline's steady state; reference optimizer.py:219-230 + :243 per step):
+ * the next step's HBM pass runs while this step's finish is still ranking.
+ *  - the winners' residual slots are left PENDING in res_out (holding acc);
+ *    the next call passes this call's selection as (prev_sel_idx, prev_count)
+ *    and res_in = this call's res_out.  Its finish first corrects the
+ *    previous winners' slots (res_out[i] = +0 + grad[i], histogram and
+ *    candidates to match), then releases the call after it (programmatic
+ *    dependent launch), whose main pass streams while this finish ranks and
+ *    writes -- selections, values, w and the settled residual are bitwise
+ *    those of gtk_select_update;
+ *  - no sampling kernel: the window comes from d_window, and since the next
+ *    call starts before this call has measured its window, the caller
+ *    alternates TWO records (call t uses record t % 2: written two calls
+ *    earlier), TWO workspaces `ws` and two selection buffers;
+ *  - prev_ws: the previous call's workspace (its finish left each block's
+ *    output range there, so the correction needs no search), may be NULL;
+ *  - prev_sel_idx = NULL: res_in holds no pending winners (first call);
+ *  - gtk_select_settle(last res_out, last sel_idx, last d_count, its record)
+ *    materialises the residual after the last call.
+ * w / lr / P / scaling as gtk_select_update. */
+int gtk_select_update_deferred(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
+                               int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
+                               size_t ws_bytes, uint32_t* d_window, const int32_t* prev_sel_idx,
+                               const int32_t* prev_count, const void* prev_ws, float* w, float lr, int32_t P,
+                               int32_t scaling, void* stream);
+
 /* Measurement only (bench.py's roofline): `reps` back-to-back launches of
  * K1's HBM pass alone (res_out = res_in + grad, candidate compaction and the
  * window histogram) against the key window the last select on this

@@ -70,6 +70,26 @@ struct EngineSmem {
   uint32_t ng;
 };
 
+// binary searches over an ascending index list in shared memory
+static __device__ __forceinline__ uint32_t lower_bound_s(const int32_t* s, uint32_t n, int32_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (s[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+static __device__ __forceinline__ uint32_t upper_bound_s(const int32_t* s, uint32_t n, int32_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (s[mid] <= x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
 // ---- slot sources -------------------------------------------------------------
 // get(s, key, idx, val) -> slot s holds an entry?  Only s in the block's own
 // [s0, s1) is ever requested.
@@ -137,6 +157,8 @@ struct Sink {
   // index among the kept entries with key == tau), rec[0] |= kRecPending --
   // i is a winner iff key > tau || (key == tau && i <= cut) (nullable)
   uint32_t* pend_rec = nullptr;
+  // deferred select: every block's first output position ([1 + blk]; [0] = G)
+  uint32_t* blk_ofs = nullptr;
 };
 
 constexpr uint32_t kRecValid = 0x1u;    // window record word 0: lo/shift/k describe the next call's window
@@ -542,6 +564,10 @@ __device__ bool engine_band_finish(const Src& src, uint32_t s0, uint32_t s1, uin
       if (sm.gidx[q] == i) return sm.gblk[q] != 0xFFFFFFFFu;
     return false;
   };
+  if (out.blk_ofs && threadIdx.x == 0) {
+    out.blk_ofs[1 + blk] = above_before + extra;
+    if (blk == 0) out.blk_ofs[0] = G;
+  }
   engine_write<NT>(src, s0, s1, above_before + extra, keep_fn, sm, out);
   sink_stamp(out, 3);
   if (blk == 0) {  // every block is past its last histogram read

@@ -183,25 +183,6 @@ static __device__ __forceinline__ uint32_t merge_path_warp(const MergeArgs& a, u
   return L;
 }
 
-static __device__ __forceinline__ uint32_t lower_bound_s(const int32_t* s, uint32_t n, int32_t x) {
-  uint32_t lo = 0, hi = n;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (s[mid] < x) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-static __device__ __forceinline__ uint32_t upper_bound_s(const int32_t* s, uint32_t n, int32_t x) {
-  uint32_t lo = 0, hi = n;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (s[mid] <= x) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
 // Window of the round-0 histogram from the inputs' k-th-key hints: a list with
 // k entries has all of them >= its hint, so (cancellations aside) the union
 // has >= k entries >= max(hint); 2048 linear bins over the 2 octaves above it
@@ -234,7 +215,8 @@ __device__ __forceinline__ MergeWindowRec load_window_rec(const uint32_t* rec) {
 // Predicted band (exchange steps with a carried record of the same k): the
 // previous call's k-th key tau_p with room for ~4 bins of the record's
 // resolution (~64 entries per bin at tau) or twice the last move of tau on
-// either side -- ~512 union entries, inside the 1024-entry gather buffer.
+// either side -- ~512 union entries, inside the 1024-entry gather buffer;
+// skipped when the expected band holds more than 3/4 of the buffer.
 // The finish then needs ONE grid barrier (gather + counts) instead of two
 // (histogram, then gather); a miss costs one extra barrier and the histogram
 // path.
@@ -251,6 +233,10 @@ __device__ __forceinline__ MergeBand predicted_band(const MergeWindowRec& rv, ui
     const uint64_t mv = rv.tau > rv.tau2 ? rv.tau - rv.tau2 : rv.tau2 - rv.tau;
     h = max(h, 2 * mv);
   }
+  // ~kMergeBinTarget entries per 2^shift keys at tau: a band that would
+  // overflow the gather buffer (tau moving by many entries per call, e.g.
+  // the flat-topped residuals of a training run) is not tried at all
+  if (((2 * h + 1) * kMergeBinTarget >> rv.shift) > (uint64_t)kGatherCap * 3 / 4) return b;
   b.on = true;
   b.blo = rv.tau > h ? (uint32_t)(rv.tau - h) : 0u;
   b.bhi = min((uint64_t)rv.tau + h + 1, (uint64_t)0x80000000ull);

@@ -26,6 +26,8 @@
 //                       acc instead: the exact fallback.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -47,6 +49,7 @@ constexpr int kSampleMaxChunks = 1024;                       // sample blocks (w
 constexpr int kFinishThreads = 512;
 constexpr int kSliceCap = 3072;                              // candidates staged per finish block (minimum)
 constexpr int kSliceCapMax = 20480;                          // ... up to 160 KB of dynamic smem at large k
+constexpr size_t kFinishDynSmemMax = 192 * 1024;             // slice + (deferred) fix list
 constexpr uint32_t kOvfBit = 0x80000000u;
 constexpr uint32_t kMinWindowLevel = 2;  // carried-window margin: from k (1 + 2^2 / 2) = 3k candidates
 constexpr uint32_t kMaxWindowLevel = 4;  // ... up to k (1 + 2^4 / 2) = 9k
@@ -63,8 +66,8 @@ struct SelectCtl {
 };
 
 struct SelectLayout {
-  size_t ctl, sample_top, group_cnt, engine, tile_info, tile_ovf, slot_idx, slot_val, ovf_idx, ovf_val, ord_idx, ord_val,
-      total;
+  size_t ctl, sample_top, group_cnt, blk_ofs, engine, tile_info, tile_ovf, slot_idx, slot_val, ovf_idx, ovf_val,
+      ord_idx, ord_val, total;
   uint32_t ntiles, slots, ovf_cap, ord_cap;
 };
 
@@ -93,6 +96,8 @@ static SelectLayout select_layout(int64_t m, int32_t k) {
   off = al(off + sizeof(uint32_t) * kSampleMaxChunks * kSampleTop);
   L.group_cnt = off;
   off = al(off + sizeof(uint32_t) * kMaxBlocks);
+  L.blk_ofs = off;  // [0] = G of the finish that wrote [1 + b] = block b's first output position (0: none)
+  off = al(off + sizeof(uint32_t) * (kMaxBlocks + 1));
   L.engine = off;
   off = al(off + sizeof(EngineWS));
   L.tile_info = off;
@@ -575,12 +580,20 @@ __device__ __forceinline__ bool main_tile(const MainArgs& a, uint32_t tile, cons
 }
 
 
-// kChain: GTK_SELECT_CHAIN calls (window from the record, pending winners of
-// res settled on the fly); the plain instance reads nothing but the sample
-// kernel's window words after griddepcontrol.wait (every dependent load there
-// delays the whole pass: the chained instance measured +2 us)
-template <bool kChain>
-__global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
+// kMode: kMainPlain reads nothing but the sample kernel's window words after
+// griddepcontrol.wait (every dependent load there delays the whole pass: up
+// to +9 us measured); kMainChain (GTK_SELECT_CHAIN) takes the window from the
+// record and zeroes the previous call's pending winners on the fly;
+// kMainDefer (gtk_select_update_deferred) is released by the previous call's
+// finish as soon as that finish has corrected the winners before it, and
+// never waits for the rest of it (the finish after this pass corrects this
+// pass's view of the previous winners; the window comes from the record of
+// the call before the previous one) -- only the last block waits for the
+// previous finish before exiting, so the grid's completion still orders
+// everything after it behind that finish.
+constexpr int kMainPlain = 0, kMainChain = 1, kMainDefer = 2;
+template <int kMode>
+__global__ void __launch_bounds__(kMainThreads, 3) select_main_kernel(MainArgs a) {
   __shared__ uint32_t s_wt[2][16];  // per warp: packed candidate totals of the q segments
   __shared__ int32_t* s_didx[2];
   __shared__ float* s_dval[2];
@@ -593,6 +606,8 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
   // tile each, so the grid's drain (blocks running alone on a few SMs) is short
   static_assert(kMainTilesPerBlock == 2, "two-tile / one-tile schedule");
   const uint32_t blk = blockIdx.x;
+  constexpr bool kChain = kMode == kMainChain;
+  constexpr bool kRecord = kMode != kMainPlain;
   if (a.trace && blk == 0 && threadIdx.x == 0) a.trace[0] = (int64_t)globaltimer_ns();
   const uint32_t t0 = blk < a.n2 ? 2 * blk : a.n2 + blk;
   const uint32_t ntile = blk < a.n2 ? 2u : 1u;
@@ -618,29 +633,28 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
   // griddepcontrol.wait itself costs ~1 us per block, hidden behind them:
   // a variant without the sample kernel that had to wait before loading res
   // measured 6 us slower per step)
-  pdl_wait();
+  if (kMode != kMainDefer) pdl_wait();
   uint32_t lo, shift;
   bool pend = false;
   uint32_t ptau = 0, pcut = 0;
-  if (kChain && a.window) {
-    const uint32_t w0 = __ldcg(a.window);
-    pend = a.res != nullptr && (w0 & kRecPending) != 0;
-    ptau = __ldcg(a.window + 6);
-    pcut = __ldcg(a.window + 7);
-    if (a.chain) {
-      const bool valid = !a.force_exact && (w0 & kRecValid) && __ldcg(a.window + 3) == a.k;
-      lo = valid ? __ldcg(a.window + 1) : 0x7FFFFFFFu;  // no window: nothing passes, the finish runs exact
-      shift = valid ? __ldcg(a.window + 2) : 0u;
-      if (blk == 0) {  // the finish's engine counters (used only after this kernel)
-        if (threadIdx.x < (unsigned)kRounds) a.gather_n[threadIdx.x] = 0u;
-        if (threadIdx.x == 0) {
-          a.ctl->lo = lo;
-          a.ctl->shift = shift;
-        }
+  if (kRecord) {
+    // the whole key-window record in one round trip (two independent 16-byte
+    // loads, 32-byte aligned: gtk_select_windowed checks): the window of this
+    // call and the pending-winner predicate of res_in
+    const uint4 r0 = __ldcg(reinterpret_cast<const uint4*>(a.window));
+    const uint4 r1 = __ldcg(reinterpret_cast<const uint4*>(a.window) + 1);
+    const bool valid = !a.force_exact && (r0.x & kRecValid) && r0.w == a.k;
+    lo = valid ? r0.y : 0x7FFFFFFFu;  // no window: nothing passes, the finish runs exact
+    shift = valid ? r0.z : 0u;
+    pend = kChain && a.res != nullptr && (r0.x & kRecPending) != 0;
+    ptau = r1.z;
+    pcut = r1.w;
+    if (blk == 0) {  // the finish's engine counters and window (read only after this kernel)
+      if (threadIdx.x < (unsigned)kRounds) a.gather_n[threadIdx.x] = 0u;
+      if (threadIdx.x == 0) {
+        a.ctl->lo = lo;
+        a.ctl->shift = shift;
       }
-    } else {
-      lo = __ldcg(&a.ctl->lo);
-      shift = __ldcg(&a.ctl->shift);
     }
   } else {
     lo = __ldcg(&a.ctl->lo);
@@ -660,7 +674,10 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
         float4 x = gv[u][q];
         if (a.res) {
           float4 r = rv[u][q];
-          if (pend) {
+          // (chained: one max-key test per 4 elements; a pending winner is in
+          // ~k/m of them)
+          if (kChain && pend &&
+              max(max(key_of(r.x), key_of(r.y)), max(key_of(r.z), key_of(r.w))) >= ptau) {
             const uint64_t e = tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4;
             r.x = settle_res(r.x, e, ptau, pcut);
             r.y = settle_res(r.y, e + 1, ptau, pcut);
@@ -687,7 +704,7 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
           float x = 0.0f;
           if (e < a.m) {
             x = a.grad[e];
-            if (a.res) x = __fadd_rn(pend ? settle_res(a.res[e], e, ptau, pcut) : a.res[e], x);
+            if (a.res) x = __fadd_rn((kChain && pend) ? settle_res(a.res[e], e, ptau, pcut) : a.res[e], x);
             a.res_out[e] = x;
           }
           v[q][j] = x;
@@ -706,6 +723,7 @@ __global__ void __launch_bounds__(kMainThreads) select_main_kernel(MainArgs a) {
     __syncthreads();
     if (threadIdx.x == 0) atomicMax((unsigned long long*)a.trace + 1, (unsigned long long)globaltimer_ns());
   }
+  if (kMode == kMainDefer && blk == gridDim.x - 1) pdl_wait();  // complete only after the previous finish
 }
 
 // ---------------------------------------------------------------------------
@@ -748,7 +766,191 @@ struct FinishArgs {
   const uint64_t* ll_epoch = nullptr;
   uint32_t ll_slot_words = 0;
   uint32_t chain = 0;  // GTK_SELECT_CHAIN: winners stay pending in res_out (Sink::pend_rec)
+  // gtk_select_update_deferred: winners stay pending; the previous call's
+  // selection (prev_idx / prev_count, nullable) is corrected first (see
+  // deferred_fixup); the dependent launch is released after that correction
+  uint32_t defer = 0;
+  const int32_t* prev_idx = nullptr;
+  const int32_t* prev_count = nullptr;
+  const float* grad = nullptr;
+  uint32_t fix_cap = 0;  // fix-list entries staged in shared memory behind the slice
+  uint32_t* ofs_out = nullptr;       // this call's per-block output positions (deferred: the next call's j0 / j1)
+  const uint32_t* prev_ofs = nullptr;  // the previous call's (in its workspace), nullable
 };
+
+// first index i of the ascending list a[0, n) with a[i] >= x; one full warp,
+// 33-ary (a few dependent L2 round trips), result in every lane
+__device__ __forceinline__ uint32_t lower_bound_warp(const int32_t* a, uint32_t n, int32_t x) {
+  uint32_t L = 0, H = n;
+  const unsigned lane = lane_id();
+  while (L < H) {
+    const uint32_t len = H - L;
+    if (len <= 32) {
+      const bool q = lane < len && __ldcg(a + L + lane) < x;
+      L += __popc(__ballot_sync(kFull, q));
+      break;
+    }
+    const uint32_t p = L + (uint32_t)(((uint64_t)len * (lane + 1)) / 33);
+    const bool q = __ldcg(a + p) < x;
+    const int t = __popc(__ballot_sync(kFull, q));
+    const uint32_t p_prev = __shfl_sync(kFull, p, t > 0 ? t - 1 : 0);
+    const uint32_t p_t = __shfl_sync(kFull, p, t < 32 ? t : 31);
+    if (t > 0) L = p_prev + 1;
+    if (t < 32) H = p_t;
+  }
+  return L;
+}
+
+constexpr uint32_t kFixWas = 1u, kFixNow = 2u;  // fix-list flags: a candidate before / after the correction
+
+// Deferred settle, before the finish ranks anything: the previous call's
+// winners in this block's tile range were pending in res_in, so this call's
+// main pass streamed acc' = acc_prev + g there instead of +0 + g (reference
+// optimizer.py:230 zeroes them first).  Each one gets res_out[i] = +0 + g[i];
+// the window histogram moves it between bins / in or out of the window, and
+// the candidate changes go to a fix list (index order) applied to the slice
+// after the copy.  Returns the fix-list length (*n_ins: new candidates);
+// raises the overflow flag (exact dense fallback over the corrected res_out)
+// if the lists do not fit.
+__device__ uint32_t deferred_fixup(const FinishArgs& a, EngineSmem<kFinishThreads>& sm, int32_t* f_idx, float* f_val,
+                                   uint32_t* f_flag, uint32_t t0, uint32_t t1, uint32_t* n_ins_out) {
+  const uint32_t lo = __ldcg(&a.ctl->lo), shift = __ldcg(&a.ctl->shift);
+  const uint32_t n_prev = min((uint32_t)max(__ldcg(a.prev_count), 0), a.m);
+  const int32_t E0 = (int32_t)min((uint64_t)t0 * kTile, (uint64_t)a.m);
+  const int32_t E1 = (int32_t)min((uint64_t)t1 * kTile, (uint64_t)a.m);
+  // my range of the previous selection: its finish recorded every block's
+  // first output position (same tile partition), else two warp searches
+  const bool have_ofs = a.prev_ofs && __ldcg(a.prev_ofs) == gridDim.x;
+  if (have_ofs) {
+    if (threadIdx.x < 2) {
+      const uint32_t b = blockIdx.x + threadIdx.x;
+      sm.bcast[threadIdx.x] = b < gridDim.x ? min(__ldcg(a.prev_ofs + 1 + b), n_prev) : n_prev;
+    }
+  } else if (warp_id() < 2) {
+    const uint32_t j = lower_bound_warp(a.prev_idx, n_prev, warp_id() == 0 ? E0 : E1);
+    if (lane_id() == 0) sm.bcast[warp_id()] = j;
+  }
+  __syncthreads();
+  const uint32_t j0 = sm.bcast[0], j1 = sm.bcast[1];
+  // histogram moves of this block, aggregated in shared memory first (the
+  // previous winners mostly sit in the same top bins: one global atomic per
+  // bin and block instead of one per winner)
+  for (int b = threadIdx.x; b < kHistLen; b += kFinishThreads) sm.hist[b] = 0u;
+  __syncthreads();
+  uint32_t n_fix = 0, n_ins = 0;
+  for (uint32_t base = j0; base < j1; base += kFinishThreads) {  // block-uniform trip count
+    const uint32_t j = base + threadIdx.x;
+    const bool has = j < j1;
+    int32_t e = 0;
+    float ap = 0.0f, gv = 0.0f;
+    if (has) e = __ldcg(a.prev_idx + j);
+    if (has) {
+      ap = __ldcg(a.res_out + e);
+      gv = __ldcg(a.grad + e);
+    }
+    const float A = __fadd_rn(0.0f, gv);
+    bool was = false, now = false;
+    if (has) {
+      if (__float_as_uint(A) != __float_as_uint(ap)) a.res_out[e] = A;
+      const uint32_t kw = key_of(ap), kn = key_of(A);
+      was = kw >= lo;
+      now = kn >= lo;
+      const uint32_t bw = was ? min((uint32_t)kBins, (kw - lo) >> shift) : 0u;
+      const uint32_t bn = now ? min((uint32_t)kBins, (kn - lo) >> shift) : 0u;
+      if (was && !(now && bw == bn)) atomicSub(&sm.hist[bw], 1u);
+      if (now && !(was && bw == bn)) atomicAdd(&sm.hist[bn], 1u);
+    }
+    const bool keep = was || now;
+    uint32_t tot;
+    const uint32_t pos = n_fix + block_excl_scan<kFinishThreads>(keep ? 1u : 0u, sm.scan, &tot);
+    if (keep && pos < a.fix_cap) {
+      f_idx[pos] = e;
+      f_val[pos] = A;
+      f_flag[pos] = (was ? kFixWas : 0u) | (now ? kFixNow : 0u);
+    }
+    n_fix += tot;
+    n_ins += block_sum<kFinishThreads>((now && !was) ? 1u : 0u, sm.scan);
+  }
+  for (int b = threadIdx.x; b < kHistLen; b += kFinishThreads) {  // (block_sum above synced sm.hist)
+    const uint32_t dlt = sm.hist[b];
+    if (dlt) atomicAdd(a.ews->hist[0] + b, dlt);  // (mod 2^32: negative moves wrap)
+  }
+  const uint32_t own_raw = __ldcg(a.group_cnt + blockIdx.x);
+  if (threadIdx.x == 0) {
+    if (n_ins) atomicAdd(a.group_cnt + blockIdx.x, n_ins);
+    if (n_fix > a.fix_cap || n_ins > (uint32_t)kGatherCap)
+      atomicOr(&a.ctl->overflow, 1u);  // lists too long: exact dense fallback (res_out is corrected)
+  }
+  *n_ins_out = n_ins;
+  return min(n_fix, a.fix_cap);
+}
+
+// The fix list applied to the staged slice (index order, own_raw entries):
+// a previous winner that was a candidate gets its corrected value or leaves
+// (empty slot); one that became a candidate is inserted in index order.
+// (s_idx / s_val: the slice in shared memory or in the global staging list)
+__device__ void apply_fixes(int32_t* s_idx, float* s_val, uint32_t own_raw, const int32_t* f_idx, const float* f_val,
+                            uint32_t* f_flag, uint32_t n_fix, uint32_t n_ins, EngineSmem<kFinishThreads>& sm) {
+  // positions first (the slice is still sorted): a was-candidate's slot, an
+  // insertion's rank r = # slice entries below it
+  uint32_t* ins = sm.keys;  // compacted insertions: fix-list positions
+  uint32_t n_seen = 0;
+  for (uint32_t base = 0; base < n_fix; base += kFinishThreads) {
+    const uint32_t f = base + threadIdx.x;
+    const bool has = f < n_fix;
+    const uint32_t fl = has ? f_flag[f] : 0u;
+    const bool insert = has && (fl & kFixNow) && !(fl & kFixWas);
+    if (has) f_flag[f] = (fl & 3u) | (lower_bound_s(s_idx, own_raw, f_idx[f]) << 2);
+    uint32_t tot;
+    const uint32_t p = n_seen + block_excl_scan<kFinishThreads>(insert ? 1u : 0u, sm.scan, &tot);
+    if (insert) ins[p] = f;
+    n_seen += tot;
+  }
+  __syncthreads();
+  for (uint32_t f = threadIdx.x; f < n_fix; f += kFinishThreads) {
+    const uint32_t fl = f_flag[f];
+    if (fl & kFixWas) {
+      const uint32_t pos = fl >> 2;
+      if (fl & kFixNow) s_val[pos] = f_val[f];
+      else s_idx[pos] = -1;  // empty slot (SliceSrc::get)
+    }
+  }
+  __syncthreads();
+  if (n_ins == 0) return;
+  // slice entry p moves up by the insertions with r <= p: descending chunks,
+  // all of a chunk read before any of it is written (targets lie at or above
+  // the chunk, n_ins < one chunk)
+  for (int c = (int)((own_raw + kFinishThreads - 1) / kFinishThreads) - 1; c >= 0; --c) {
+    const uint32_t p = (uint32_t)c * kFinishThreads + threadIdx.x;
+    int32_t xi = 0;
+    float xv = 0.0f;
+    uint32_t np = 0;
+    if (p < own_raw) {
+      xi = s_idx[p];
+      xv = s_val[p];
+      uint32_t lo_ = 0, hi_ = n_ins;  // # insertions with r <= p
+      while (lo_ < hi_) {
+        const uint32_t mid = (lo_ + hi_) >> 1;
+        if ((f_flag[ins[mid]] >> 2) <= p) lo_ = mid + 1;
+        else hi_ = mid;
+      }
+      np = p + lo_;
+    }
+    __syncthreads();
+    if (p < own_raw) {
+      s_idx[np] = xi;
+      s_val[np] = xv;
+    }
+    __syncthreads();
+  }
+  for (uint32_t q = threadIdx.x; q < n_ins; q += kFinishThreads) {
+    const uint32_t f = ins[q];
+    const uint32_t np = (f_flag[f] >> 2) + q;
+    s_idx[np] = f_idx[f];
+    s_val[np] = f_val[f];
+  }
+  __syncthreads();
+}
 
 // block 0 of the finish, once every block has read them: the main pass's
 // counters start the next call at zero (a chained call has no sampling kernel
@@ -770,14 +972,20 @@ __device__ __forceinline__ void finish_stamp(const FinishArgs& a, int i) {
   }
 }
 
-__global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(FinishArgs a) {
+#ifndef GTK_FINISH_MIN_BLOCKS
+#define GTK_FINISH_MIN_BLOCKS 2
+#endif
+__global__ void __launch_bounds__(kFinishThreads, GTK_FINISH_MIN_BLOCKS) select_finish_kernel(FinishArgs a) {
   __shared__ EngineSmem<kFinishThreads> sm;
   extern __shared__ __align__(16) unsigned char s_dyn[];  // the candidate slice: slice_cap (idx, val)
   int32_t* s_idx = reinterpret_cast<int32_t*>(s_dyn);
   float* s_val = reinterpret_cast<float*>(s_dyn + sizeof(int32_t) * a.slice_cap);
   const unsigned G = gridDim.x, blk = blockIdx.x;
   pdl_wait();  // launched programmatically behind the main pass
-  pdl_launch_dependents();
+  // (a deferred call with a previous selection releases the next call's main
+  // pass once that selection is corrected in res_out, below)
+  const bool fixing = a.defer && a.prev_idx != nullptr;
+  if (!fixing) pdl_launch_dependents();
   // margin level of the carried window (only block 0 writes the record)
   const uint32_t wlevel = (a.window && blk == 0) ? min(kMaxWindowLevel, max(kMinWindowLevel, __ldcg(a.window) >> 8)) : kMinWindowLevel;
   const bool wsame = a.window && blk == 0 && __ldcg(a.window + 3) == a.k;
@@ -804,9 +1012,14 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
     }
     return;
   }
-  Sink out{a.sel_idx, a.sel_val, a.d_count, a.chain ? nullptr : a.res_out, true, a.trace ? a.trace + 3 : nullptr,
+  Sink out{a.sel_idx, a.sel_val, a.d_count, (a.chain || a.defer) ? nullptr : a.res_out, true,
+           a.trace ? a.trace + 3 : nullptr,
            a.window, wlevel, wtau, wtau2, 1u, a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling};
   if (a.chain) out.pend_rec = a.window;
+  if (a.ofs_out) {  // written by the candidate path's band finish only (same tile partition next call)
+    if (blk == 0 && threadIdx.x == 0) a.ofs_out[0] = 0u;
+    out.blk_ofs = a.ofs_out;
+  }
   if (a.ll_base) {  // the exchange's step 0 send, straight from the write phase
     const uint32_t tag = (uint32_t)(__ldcg((const unsigned long long*)a.ll_epoch) + 1ull);
     uint64_t* slot = a.ll_base + (size_t)(tag & 1u) * a.ll_slot_words;
@@ -815,6 +1028,27 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
     out.ll_tag = tag;
   }
   finish_stamp(a, 0);
+  const uint32_t per = a.tiles_per_group;
+  const uint32_t t0 = min(a.ntiles, blk * per), t1 = min(a.ntiles, t0 + per);
+
+  // deferred settle of the previous call's winners (histogram corrections
+  // complete behind the grid barrier before anyone reads the histogram)
+  int32_t* f_idx = reinterpret_cast<int32_t*>(s_dyn + (sizeof(int32_t) + sizeof(float)) * a.slice_cap);
+  float* f_val = reinterpret_cast<float*>(f_idx + a.fix_cap);
+  uint32_t* f_flag = reinterpret_cast<uint32_t*>(f_val + a.fix_cap);
+  uint32_t n_fix = 0, n_ins = 0;
+  if (fixing) {
+    n_fix = deferred_fixup(a, sm, f_idx, f_val, f_flag, t0, t1, &n_ins);
+    if (a.trace && blk == 0 && threadIdx.x == 0) {  // diagnostics (block 0's fix list)
+      a.trace[14] = n_fix;
+      a.trace[15] = n_ins;
+    }
+    __threadfence();  // res_out corrections visible before the next main pass is released
+    __syncthreads();
+    pdl_launch_dependents();
+    grid_sync(&a.ews->bar, G);
+    finish_stamp(a, 20);  // (diagnostics: fixup + barrier done)
+  }
 
   // the round-0 window histogram (main pass) -> sm.hist by async copies
   // issued now and awaited after the candidate copy: their L2 latency hides
@@ -823,8 +1057,6 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
   cp_async_commit();  // group: histogram
   // my tile range and its place in the global (index-ordered) candidate list:
   // the main pass counted the candidates of every block's tile range
-  const uint32_t per = a.tiles_per_group;
-  const uint32_t t0 = min(a.ntiles, blk * per), t1 = min(a.ntiles, t0 + per);
   uint32_t C;
   {
     const uint32_t c = threadIdx.x < G ? __ldcg(a.group_cnt + threadIdx.x) : 0u;
@@ -838,6 +1070,12 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
   const uint32_t before = sm.bcast[0], own = sm.bcast[1];
   const bool overflow = __ldcg(&a.ctl->overflow) != 0;
   finish_stamp(a, 1);
+  if (a.defer && a.trace && blk == 0 && threadIdx.x == 0) {  // diagnostics: the candidate-path decision
+    a.trace[16] = overflow;
+    a.trace[17] = C;
+    a.trace[18] = a.ord_cap;
+    a.trace[19] = 0;
+  }
   if (!overflow && C >= a.k && C <= a.ord_cap) {
     // copy my tiles' candidates into my slice (smem if it fits)
     const bool in_smem = own <= a.slice_cap;
@@ -925,12 +1163,19 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
       a.trace[13] = G;
     }
     cp_async_commit();    // group: the slice
-    cp_async_wait<1>();   // the histogram has landed; the slice may still be in flight
-    __syncthreads();
+    const bool fixes = n_fix > 0;  // (block-local)
+    if (fixes) {  // the slice must have landed
+      cp_async_wait_all();
+      __syncthreads();
+      apply_fixes(di, dv, own - n_ins, f_idx, f_val, f_flag, n_fix, n_ins, sm);
+    } else {
+      cp_async_wait<1>();   // the histogram has landed; the slice may still be in flight
+      __syncthreads();
+    }
     SliceSrc src{s_idx, s_val, a.ord_idx, a.ord_val, before, in_smem, false};
     if (engine_run<kFinishThreads>(src, before, before + own, a.k, false, __ldcg(&a.ctl->lo),
                                    __ldcg(&a.ctl->shift), sm.hist, true, a.ews, sm, out, G,
-                                   /*slice_async=*/true)) {
+                                   /*slice_async=*/!fixes)) {
       if (a.trace && threadIdx.x == 0)  // timeline: last block end (trace_buffer()[114])
         atomicMax((unsigned long long*)a.trace + 66, (unsigned long long)globaltimer_ns());
       if (blk == 0) reset_select_counters(a, G);  // (the engine's grid barrier is behind every read)
@@ -938,6 +1183,7 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
     }
   }
   // exact dense fallback over acc (= res_out, untouched so far)
+  if (a.defer && a.trace && blk == 0 && threadIdx.x == 0) a.trace[19] = 1;
   cp_async_wait_all();  // the histogram prefetch must land before sm.hist is reused
   grid_sync(&a.ews->bar, G);
   if (blk == 0) {
@@ -963,6 +1209,7 @@ __global__ void __launch_bounds__(kFinishThreads, 2) select_finish_kernel(Finish
   // records a fresh window for the next call (block 0), at the raised margin
   // after a low miss and with no growth estimate across the gap
   Sink dout = out;
+  dout.blk_ofs = nullptr;  // (the dense partition is not the tile partition)
   dout.window_level = (!overflow && C < a.k) ? min(kMaxWindowLevel, wlevel + 1) : wlevel;
   dout.prev_tau = dout.prev_tau2 = 0u;
   engine_run<kFinishThreads>(dsrc, s0, s1, a.k, false, 0u, 20u, nullptr, false, a.ews, sm, dout, G);
@@ -976,7 +1223,7 @@ using namespace gtk;
 // main-pass grid: two tiles per block, except that about one wave of resident
 // blocks at the end of the grid takes one tile each (a shorter drain)
 static uint32_t main_grid(uint32_t ntiles, uint32_t* n2) {
-  const int slots = coop_grid((const void*)select_main_kernel<false>, kMainThreads, 0);  // resident blocks, all SMs
+  const int slots = coop_grid((const void*)select_main_kernel<kMainPlain>, kMainThreads, 0);  // resident blocks, all SMs
   if (slots <= 0) return 0;
   uint32_t n1 = std::min<uint32_t>(ntiles, (uint32_t)slots);
   uint32_t two = (ntiles - n1) / 2;
@@ -1011,10 +1258,16 @@ struct PeerPush {
   uint64_t* slot0;
   const uint64_t* epoch;
 };
+struct Deferred {  // gtk_select_update_deferred
+  bool on;
+  const int32_t* prev_idx;
+  const int32_t* prev_count;
+  const void* prev_ws;
+};
 static int select_impl(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
                        int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
                        size_t ws_bytes, int32_t flags, uint32_t* d_window, FusedUpdate upd, void* stream,
-                       PeerPush push = {nullptr, nullptr});
+                       PeerPush push = {nullptr, nullptr}, Deferred dfr = {false, nullptr, nullptr, nullptr});
 
 extern "C" int gtk_select_windowed(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
                                    int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status,
@@ -1044,16 +1297,34 @@ extern "C" int gtk_select_update(const float* res_in, const float* grad, float* 
                      d_window, FusedUpdate{w, lr, (float)P, scaling}, stream);
 }
 
+extern "C" int gtk_select_update_deferred(const float* res_in, const float* grad, float* res_out, int64_t m,
+                                          int32_t k, int32_t* sel_idx, float* sel_val, int32_t* d_count,
+                                          uint32_t* d_status, void* ws, size_t ws_bytes, uint32_t* d_window,
+                                          const int32_t* prev_sel_idx, const int32_t* prev_count,
+                                          const void* prev_ws, float* w, float lr, int32_t P, int32_t scaling,
+                                          void* stream) {
+  if (!w || !res_in || P < 1 || scaling < 0 || scaling > 2 || !std::isfinite(lr) || std::signbit(lr))
+    return GTK_EINVAL;
+  return select_impl(res_in, grad, res_out, m, k, sel_idx, sel_val, d_count, d_status, ws, ws_bytes, 0, d_window,
+                     FusedUpdate{w, lr, (float)P, scaling}, stream, PeerPush{nullptr, nullptr},
+                     Deferred{true, prev_sel_idx, prev_count, prev_sel_idx ? prev_ws : nullptr});
+}
+
 static int select_impl(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
                        int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
                        size_t ws_bytes, int32_t flags, uint32_t* d_window, FusedUpdate upd, void* stream,
-                       PeerPush push) {
+                       PeerPush push, Deferred dfr) {
   if (!grad || !res_out || !sel_idx || !sel_val || !d_count || !d_status || !ws) return GTK_EINVAL;
+  if (dfr.on && (!d_window || (uintptr_t)d_window % 32 != 0 || res_out == res_in || res_out == grad ||
+                 (dfr.prev_idx && (!dfr.prev_count || dfr.prev_idx == sel_idx || dfr.prev_ws == ws))))
+    return GTK_EINVAL;
   if (m < 1 || m >= (int64_t(1) << 31) || k < 1 || k > m) return GTK_EINVAL;
   // a chained call needs the record that carries its window and the pending
   // winners, and its own output buffer (res_in is read early, before the
   // previous call's kernels have finished)
-  if ((flags & GTK_SELECT_CHAIN) && (!d_window || res_out == res_in || res_out == grad)) return GTK_EINVAL;
+  if ((flags & GTK_SELECT_CHAIN) &&
+      (!d_window || (uintptr_t)d_window % 32 != 0 || res_out == res_in || res_out == grad))
+    return GTK_EINVAL;
   const SelectLayout L = select_layout(m, k);
   if (ws_bytes < L.total) return GTK_ENOMEM;
   const bool aligned = ((uintptr_t)grad % 16 == 0) && ((uintptr_t)res_out % 16 == 0) &&
@@ -1098,8 +1369,12 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
     const uint64_t per = ((uint64_t)k * 4 + nsm - 1) / nsm;
     if (per > slice_cap) slice_cap = (uint32_t)std::min<uint64_t>((per + 1023) & ~1023ull, kSliceCapMax);
   }
-  const size_t fin_smem = (size_t)slice_cap * (sizeof(int32_t) + sizeof(float));
-  if (!ensure_dyn_smem((const void*)select_finish_kernel, (size_t)kSliceCapMax * 8)) return GTK_ECUDA;
+  // deferred calls stage the previous winners of a block's tile range (~k/G,
+  // room for 2x) behind the slice: the fix list
+  uint32_t fix_cap = dfr.on ? (uint32_t)std::max<uint64_t>(512, ((2ull * k + nsm - 1) / nsm + 255) & ~255ull) : 0u;
+  size_t fin_smem = (size_t)slice_cap * (sizeof(int32_t) + sizeof(float)) + (size_t)fix_cap * 12;
+  if (fin_smem > kFinishDynSmemMax) return GTK_EINVAL;  // (deferred at very large k: use gtk_select_update)
+  if (!ensure_dyn_smem((const void*)select_finish_kernel, kFinishDynSmemMax)) return GTK_ECUDA;
   int G = coop_grid((const void*)select_finish_kernel, kFinishThreads, fin_smem);
   if (G <= 0) return GTK_ECUDA;
   {
@@ -1109,15 +1384,31 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
     if ((uint32_t)want > L.ntiles) want = (int)L.ntiles;
     if (G > want) G = want;
     if (G > nsm) G = nsm;
+    // deferred: the finish runs beside the next call's HBM pass; on ~2/5 of
+    // the SMs it leaves the rest to that pass at full occupancy (measured at
+    // the headline: 148 blocks 66.7 us/step, 100 64.0, 74 63.3, 60 62.9)
+    if (dfr.on) {
+      const int gd = std::max(8, (nsm * 2 + 4) / 5);
+      const int gk = (int)(((int64_t)k * 2 + slice_cap - 1) / slice_cap);
+      G = std::min(G, std::max(gd, gk));
+    }
+    const char* fg = getenv("GTK_FINISH_G");  // (measurement switch)
+    if (fg && atoi(fg) > 0 && atoi(fg) < G && (int64_t)atoi(fg) * slice_cap >= (int64_t)k * 2) G = atoi(fg);
+    if (dfr.on) {  // the fix list holds ~k / G previous winners per block: room for 2x
+      fix_cap = (uint32_t)std::max<uint64_t>(512, ((2ull * k + G - 1) / G + 255) & ~255ull);
+      fin_smem = (size_t)slice_cap * (sizeof(int32_t) + sizeof(float)) + (size_t)fix_cap * 12;
+      if (fin_smem > kFinishDynSmemMax) return GTK_EINVAL;
+    }
     if (G > kMaxBlocks) G = kMaxBlocks;
   }
   const uint32_t tiles_per_group = (L.ntiles + G - 1) / G;
   uint32_t* group_cnt = (uint32_t*)(base + L.group_cnt);
 
   const bool chain = (flags & GTK_SELECT_CHAIN) != 0;
+  const bool defer = dfr.on;
   const bool force_exact = (flags & GTK_SELECT_FORCE_EXACT) != 0;
   ProfScope prof_all(kProfSelect, st);
-  if (!chain) {  // a chained call takes its window from the record: no sampling pass
+  if (!chain && !defer) {  // a chained call takes its window from the record: no sampling pass
     SampleArgs sa{res_in, grad, (uint32_t)m, stride, nchunks, r_lo, r_hi, (uint32_t)(force_exact ? 1 : 0), stop,
                   d_window, (uint32_t)k, ctl, ews, group_cnt, trace_buffer() ? trace_buffer() + 64 : nullptr};
     GTK_CUDA(launch_pdl(select_sample_kernel, dim3(nchunks), dim3(kSampleThreads), 0, st, sa));
@@ -1142,7 +1433,7 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
               tiles_per_group};
   ma.window = d_window;
   ma.k = (uint32_t)k;
-  ma.chain = chain ? 1u : 0u;
+  ma.chain = (chain || defer) ? 1u : 0u;
   ma.force_exact = force_exact ? 1u : 0u;
   ma.gather_n = ews->gather_n;
   {
@@ -1150,7 +1441,9 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
     const uint32_t gmain = main_grid(L.ntiles, &ma.n2);
     if (gmain == 0) return GTK_ECUDA;
     ma.trace = trace_buffer() ? trace_buffer() + 112 : nullptr;
-    GTK_CUDA(launch_pdl(chain ? select_main_kernel<true> : select_main_kernel<false>, dim3(gmain), dim3(kMainThreads), 0, st, ma));
+    auto* mk = defer ? select_main_kernel<kMainDefer>
+                     : (chain ? select_main_kernel<kMainChain> : select_main_kernel<kMainPlain>);
+    GTK_CUDA(launch_pdl(mk, dim3(gmain), dim3(kMainThreads), 0, st, ma));
     GTK_CHECK_LAUNCH();
   }
 
@@ -1184,6 +1477,15 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
                 upd.scaling,
                 slice_cap};
   fa.chain = chain ? 1u : 0u;
+  if (defer) {
+    fa.defer = 1u;
+    fa.prev_idx = dfr.prev_idx;
+    fa.prev_count = dfr.prev_count;
+    fa.grad = grad;
+    fa.fix_cap = fix_cap;
+    fa.ofs_out = (uint32_t*)(base + L.blk_ofs);
+    fa.prev_ofs = dfr.prev_ws ? (const uint32_t*)((const char*)dfr.prev_ws + L.blk_ofs) : nullptr;
+  }
   if (push.slot0) {
     fa.ll_base = push.slot0;
     fa.ll_epoch = push.epoch;
@@ -1217,7 +1519,7 @@ extern "C" int gtk_select_main_pass(const float* res_in, const float* grad, floa
   const uint32_t gmain = main_grid(L.ntiles, &ma.n2);
   if (gmain == 0) return GTK_ECUDA;
   for (int r = 0; r < reps; ++r) {
-    select_main_kernel<false><<<gmain, kMainThreads, 0, st>>>(ma);
+    select_main_kernel<kMainPlain><<<gmain, kMainThreads, 0, st>>>(ma);
     GTK_CHECK_LAUNCH();
   }
   // the repeated passes accumulated histogram / counter state: clear it

@@ -117,8 +117,10 @@ def _new_ws(nbytes: int, device) -> torch.Tensor:
     return buf
 
 
-def select_workspace(m: int, k: int, device) -> torch.Tensor:
-    key = ("select", device.index, m, k)
+def select_workspace(m: int, k: int, device, slot: int = 0) -> torch.Tensor:
+    """Select workspace for (m, k) on `device`; `slot` > 0 gives separate ones
+    (deferred selects alternate two: gtk_select_update_deferred)."""
+    key = ("select", device.index, m, k, slot)
     c = _cache()
     ws = c.get(key)
     if ws is None:
@@ -181,7 +183,8 @@ def select_push(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, out: 
     )
 
 
-def time_main_pass(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, reps: int) -> float:
+def time_main_pass(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, reps: int,
+                   ws: torch.Tensor | None = None) -> float:
     """Measurement only: ms per launch of K1's HBM pass against the window the
     last select of this (m, k) published (gtk_select_main_pass): CUDA events
     on the library's stream around `reps` and `2 reps` back-to-back launches;
@@ -189,7 +192,8 @@ def time_main_pass(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, re
     clear cancels).  res_out is overwritten with res_in + grad."""
     m = grad.numel()
     dev = grad.device
-    ws = select_workspace(m, k, dev)
+    if ws is None:
+        ws = select_workspace(m, k, dev)
     st = torch.cuda.current_stream(dev)
 
     def timed(n):
@@ -227,6 +231,27 @@ def select_update(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, out
         "gtk_select_update", P(res_in), P(grad), P(res_out), m, k, P(out.idx), P(out.val), P(out.count),
         P(status), P(ws), ctypes.c_size_t(ws.numel()), _lib.SELECT_CHAIN if chain else 0, P(window), P(w),
         ctypes.c_float(lr), P_, scaling, stream_of(dev),
+    )
+
+
+def select_update_deferred(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, out: DeviceList,
+                           status: torch.Tensor, window: torch.Tensor, ws: torch.Tensor, prev: DeviceList | None,
+                           w: torch.Tensor, lr: float, P_: int, scaling: int,
+                           prev_ws: torch.Tensor | None = None) -> None:
+    """K1 + K3 for P = 1 with the settle deferred (gtk_select_update_deferred):
+    this call's winners stay pending in res_out, `prev` (the previous call's
+    selection, pending in res_in) is corrected by this call's finish, which
+    then releases the next call's HBM pass; the caller alternates two
+    (window record, ws, out) sets (prev_ws = the previous call's ws).
+    Bitwise the selection and update of select_update; `settle` after the
+    last call."""
+    m = grad.numel()
+    _lib.call(
+        "gtk_select_update_deferred", P(res_in), P(grad), P(res_out), m, k, P(out.idx), P(out.val),
+        P(out.count), P(status), P(ws), ctypes.c_size_t(ws.numel()), P(window),
+        P(prev.idx) if prev is not None else None, P(prev.count) if prev is not None else None,
+        P(prev_ws) if prev is not None else None, P(w),
+        ctypes.c_float(lr), P_, scaling, stream_of(grad.device),
     )
 
 

@@ -72,20 +72,40 @@ class GTopKPipeline:
         self.block_graph = None
         self.kernels_per_step = None
         self.use_graph = use_graph
-        # GTK_PIPE_CHAIN=1: chained selects (no sampling kernel; measured 3 us
-        # per step slower than the plain select at the headline, A/B only)
-        self.chain_ok = os.environ.get("GTK_PIPE_CHAIN", "0") == "1"
+        # P = 1 select mode (GTK_PIPE_MODE, A/B measurements):
+        #  defer (default): gtk_select_update_deferred -- the next step's HBM
+        #    pass streams while this step's finish ranks; two alternating
+        #    (window record, workspace, selection) sets;
+        #  chain: GTK_SELECT_CHAIN (no sampling kernel, winners zeroed on the fly);
+        #  plain: gtk_select_update with the sampling kernel.
+        self.mode = os.environ.get("GTK_PIPE_MODE", "defer")
+        if self.mode not in ("defer", "chain", "plain"):
+            raise ValueError(f"GTK_PIPE_MODE={self.mode!r}")
         self.chained = False  # steps leave their winners pending (settled by sync_state)
+        self.deferred = False
+        self._dsteps = 0  # deferred steps enqueued (the first has no previous selection)
+        if self.P == 1 and self.mode == "defer":
+            self.dsel = [DeviceList(self.m, self.k, self.dev) for _ in range(2)]
+            self.dws = [_dev.select_workspace(self.m, self.k, self.dev, slot=1 + i) for i in range(2)]
+            # the next main pass starts before this finish has written the next
+            # window: it reads the record of the step before (one per parity)
+            self.dwin = [_dev.new_window(self.dev) for _ in range(2)]
 
     # -- one step's launches (current stream) --------------------------------
     def _enqueue(self, parity: int) -> None:
         grad = self.grads[parity % len(self.grads)]
         res_in, res_out = self.res[parity], self.res[1 - parity]
         if self.P == 1 and _dev.sparse_update_fusable(self.lr, self.mom):
-            chain = self.chain_ok
-            # one rank: the global top-k is the selection; K3 rides on K1's
-            # finish; chained selects (two launches per step: no sampling
-            # kernel, the winners' residual zeroed by the next step's stream)
+            # one rank: the global top-k is the selection; K3 rides on K1's finish
+            if self.mode == "defer":
+                prev = self.dsel[1 - parity] if self._dsteps > 0 else None
+                _dev.select_update_deferred(res_in, grad, res_out, self.k, self.dsel[parity], self.status,
+                                            self.dwin[parity], self.dws[parity], prev, self.state._w, self.lr, 1,
+                                            self.scaling, prev_ws=self.dws[1 - parity])
+                self._dsteps += 1
+                self.deferred = True
+                return
+            chain = self.mode == "chain"
             _dev.select_update(res_in, grad, res_out, self.k, self.sel, self.status, self.window,
                                self.state._w, self.lr, 1, self.scaling, chain=chain)
             self.chained = chain
@@ -170,7 +190,11 @@ class GTopKPipeline:
         residual buffer (the next step's output) is overwritten."""
         torch.cuda.synchronize(self.dev)
         p = self.t % 2
-        return _dev.time_main_pass(self.res[p], self.grads[p % len(self.grads)], self.res[1 - p], self.k, reps)
+        # deferred steps keep their windows in their own two workspaces: the
+        # one of this parity holds the window its last main pass used
+        ws = self.dws[p] if self.deferred else None
+        return _dev.time_main_pass(self.res[p], self.grads[p % len(self.grads)], self.res[1 - p], self.k, reps,
+                                   ws=ws)
 
     def profile_graph(self, steps: int = 20) -> dict:
         """Per-stage device time (ms) from CUDA event nodes captured around
@@ -237,10 +261,29 @@ class GTopKPipeline:
             # materialise the residual of the last step (+0.0 at its winners);
             # the next chained step would have zeroed them on the fly
             _dev.settle(self.res[p], self.sel, self.window)
+        if self.deferred and self.t > 0:
+            # the same for a deferred step (the next step's finish would have
+            # corrected its own view of them); idempotent if the pipeline goes
+            # on -- it owns the state's buffers until then
+            _dev.settle(self.res[p], self.dsel[1 - p], self.dwin[1 - p])
         st._res, st._res2 = self.res[p], self.res[1 - p]
         st.iteration += self.t - getattr(self, "_synced_t", 0)
         self._synced_t = self.t
         st._host_cache.clear()
 
+    def settled_residual(self) -> torch.Tensor:
+        """A copy of the live residual with the last step's pending winners
+        settled (+0.0), i.e. the reference's residual after self.t steps; the
+        pipeline's own buffers are left as they are (tests)."""
+        p = self.t % 2
+        res = self.res[p].clone()
+        if self.chained and self.t > 0:
+            _dev.settle(res, self.sel, self.window.clone())
+        if self.deferred and self.t > 0:
+            _dev.settle(res, self.dsel[1 - p], self.dwin[1 - p].clone())
+        return res
+
     def global_list(self) -> DeviceList:
-        return self.plan.acc if self.plan is not None else self.sel
+        if self.plan is not None:
+            return self.plan.acc
+        return self.dsel[(self.t - 1) % 2] if self.deferred else self.sel

@@ -537,3 +537,63 @@ def test_chained_select_update_trajectory(dev, kind):
     dev.settle(R[cur], lst, win)
     assert int(win[0].item()) & 0x2 == 0
     assert np.array_equal(R[cur].cpu().numpy().view(np.uint32), ref.residual.view(np.uint32))
+
+
+@pytest.mark.parametrize("kind", ["normal", "ties", "flat", "cancel"])
+def test_deferred_select_update_trajectory(dev, kind):
+    """gtk_select_update_deferred (the P = 1 pipeline's select): the next
+    call's main pass streams the residual with this call's winners still
+    pending, its finish corrects them (res = +0 + g there, histogram and
+    candidate slice to match).  Step by step against the oracle: selection,
+    w and the settled residual -- through the record-less first calls (exact
+    dense passes), heavy ties (integer gradients), flat magnitudes, and
+    `cancel` steps whose gradient exactly cancels the previous winners'
+    values (acc + g = 0 at them: every previous winner LEAVES the window, its
+    corrected value -acc re-enters it as an inserted candidate)."""
+    import torch
+
+    from oracle import gtopk_oracle as orc
+
+    d = torch.device("cuda", 0)
+    m, lr, k = 1_000_003, 0.05, 1000
+    rng = np.random.default_rng({"normal": 11, "ties": 12, "flat": 13, "cancel": 14}[kind])
+
+    def grad(t, prev):
+        if kind == "ties":
+            return rng.integers(-3, 4, m).astype(F32)
+        if kind == "flat":
+            return (rng.random(m) < 0.5).astype(F32) * F32(0.25) + F32(1.0)
+        g = rng.standard_normal(m).astype(F32)
+        if kind == "cancel" and prev is not None and t % 3 == 2:
+            pi, pv = prev
+            g[pi.astype(np.int64)] = -pv  # acc + g = +0 at every previous winner
+        return g
+
+    ref = orc.State(np.zeros(m, F32), lr)
+    R = [torch.zeros(m, device=d), torch.empty(m, device=d)]
+    w = torch.zeros(m, device=d)
+    wins = [dev.new_window(d) for _ in range(2)]
+    wss = [dev.select_workspace(m, k, d, slot=11 + i) for i in range(2)]
+    sels = [dev.DeviceList(m, k, d) for _ in range(2)]
+    st = torch.zeros(1, dtype=torch.int32, device=d)
+    prev = None
+    cur = 0
+    for t in range(16):
+        g = grad(t, prev)
+        par = t % 2
+        st.zero_()
+        dev.select_update_deferred(R[cur], torch.from_numpy(g).to(d), R[1 - cur], k, sels[par], st, wins[par],
+                                   wss[par], sels[1 - par] if t > 0 else None, w, float(F32(lr)), 1, 0,
+                                   prev_ws=wss[1 - par] if t % 4 != 3 else None)  # (some calls search instead)
+        (gi, gv), _ = orc.gtopk_step_all([ref], [g], k)
+        word = int(st.item())
+        assert word & 0x3D == 0, hex(word)
+        i, v = sels[par].to_host()
+        assert np.array_equal(i, gi), (kind, t)
+        assert np.array_equal(v.view(np.uint32), gv.view(np.uint32)), (kind, t)
+        assert np.array_equal(w.cpu().numpy().view(np.uint32), ref.weights.view(np.uint32)), (kind, t)
+        cur = 1 - cur
+        settled = R[cur].clone()
+        dev.settle(settled, sels[par], wins[par].clone())
+        assert np.array_equal(settled.cpu().numpy().view(np.uint32), ref.residual.view(np.uint32)), (kind, t)
+        prev = (gi, gv)

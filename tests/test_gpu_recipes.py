@@ -87,13 +87,17 @@ def test_config5_extreme_66m_rho_001():
     assert np.array_equal(bits(st.residual.cpu().numpy()), bits(ref.residual))
 
 
-def test_graph_pipeline_steady_state_trajectory():
+@pytest.mark.parametrize("mode,steps", [("defer", 2000), ("chain", 400), ("plain", 400)])
+def test_graph_pipeline_steady_state_trajectory(mode, steps, monkeypatch):
     """bench.py's timed regime at ResNet-20 size: 2,000 graph-replayed steps
     (2/rho: the residual builds up and settles), weights and residual equal
     to the oracle's after every step of the first 100 and every 20-step block
-    graph after that."""
+    graph after that -- for the default deferred-settle select (the next
+    step's HBM pass overlapping this step's finish) and the chained and plain
+    selects."""
     import torch
 
+    monkeypatch.setenv("GTK_PIPE_MODE", mode)
     import paper_1901_04359_b200 as gtopk
     from oracle import gtopk_oracle as orc
     from paper_1901_04359_b200.pipeline import GTopKPipeline
@@ -115,12 +119,11 @@ def test_graph_pipeline_steady_state_trajectory():
     from paper_1901_04359_b200 import device as dv
 
     def check(t):
-        # after t steps the live residual is res[t % 2]; chained steps leave
-        # the last step's winners pending (the next step zeroes them on the
-        # fly): compare a settled COPY, so the live pipeline keeps exercising
-        # the on-the-fly path
-        res = pipe.res[t % 2].clone()
-        dv.settle(res, pipe.sel, pipe.window.clone())
+        # after t steps the live residual is res[t % 2]; chained / deferred
+        # steps leave the last step's winners pending (the next step settles
+        # them): compare a settled COPY, so the live pipeline keeps
+        # exercising that path
+        res = pipe.settled_residual()
         torch.cuda.synchronize()
         assert np.array_equal(bits(st._w.cpu().numpy()), bits(ref.weights)), f"weights after step {t}"
         assert np.array_equal(bits(res.cpu().numpy()), bits(ref.residual)), f"residual after step {t}"
@@ -134,7 +137,7 @@ def test_graph_pipeline_steady_state_trajectory():
         ref_steps(1, t)
         t += 1
         check(t)
-    while t < 2000:  # 20-step block graphs (t even)
+    while t < steps:  # 20-step block graphs (t even)
         pipe.run(GTopKPipeline.kBlockSteps)
         ref_steps(GTopKPipeline.kBlockSteps, t)
         t += GTopKPipeline.kBlockSteps

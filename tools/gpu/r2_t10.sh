@@ -1,0 +1,8 @@
+nvidia-smi -L
+GTK_DEFER_EARLY=1 GTK_FINISH_G=74 python tools/defer_timeline.py > gpurun_out/t10_tl_g74.txt 2>&1
+for rep in 1 2; do
+  for g in 148 100 74 50 37; do
+    GTK_DEFER_EARLY=1 GTK_FINISH_G=$g python bench.py --steps 200 --warmup 20 --no-cpu 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('early G=$g', d['value'], d['run']['dense_fallback_in_timed_steps'])" >> gpurun_out/t10_ab.txt
+    GTK_PIPE_MODE=chain GTK_FINISH_G=$g python bench.py --steps 200 --warmup 20 --no-cpu 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('chain G=$g', d['value'], d['run']['dense_fallback_in_timed_steps'])" >> gpurun_out/t10_ab.txt
+  done
+done
