@@ -171,6 +171,27 @@ int gtk_select_update_deferred(const float* res_in, const float* grad, float* re
                                const int32_t* prev_count, const void* prev_ws, float* w, float lr, int32_t P,
                                int32_t scaling, void* stream);
 
+/* Deferred-settle select for the P > 1 step (the pipeline's steady state;
+ * reference optimizer.py:219-230): gtk_select_update_deferred's scheme
+ * without the fused update, with gtk_select_push's send of the selection to
+ * the exchange's first partner -- followed by gtk_gtopk_exchange_update with
+ * res = NULL (w updated, the residual untouched).  The previous winners are
+ * corrected by membership of the previous global list: prev_tags = the
+ * exchange plan's uint32[m] tags, d_epoch = its epoch counter (the previous
+ * exchange's epoch when this call's finish runs).  Settle the last step with
+ * gtk_select_settle_global. */
+int gtk_select_push_deferred(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
+                             int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
+                             size_t ws_bytes, uint32_t* d_window, const int32_t* prev_sel_idx,
+                             const int32_t* prev_count, const void* prev_ws, const uint32_t* prev_tags,
+                             void* peer_slot0, const uint64_t* d_epoch, void* stream);
+
+/* The residual after the last deferred P > 1 step: +0.0 at the local winners
+ * in the global list (tags[i] == low word of *d_epoch), +0 + acc elsewhere
+ * (optimizer.py:227-230). */
+int gtk_select_settle_global(float* res, const int32_t* sel_idx, const int32_t* d_count, const uint32_t* tags,
+                             const uint64_t* d_epoch, void* stream);
+
 /* Measurement only (bench.py's roofline): `reps` back-to-back launches of
  * K1's HBM pass alone (res_out = res_in + grad, candidate compaction and the
  * window histogram) against the key window the last select on this
@@ -290,7 +311,12 @@ int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedule, int32_t
  * :243.  Skipped on any GTK_DEV_* error bit, like gtk_scatter_update's d_skip.
  * Sparse-exact form only (finite lr, sign bit clear; no momentum); in_* is
  * required; nsteps > 0 (one rank: gtk_select_update).
- *   d_tags: device uint32[m], zeroed once, owned per exchange plan. */
+ *   d_tags: device uint32[m], zeroed once, owned per exchange plan.
+ *   res = NULL: the deferred step (gtk_select_push_deferred) -- no residual
+ *   restore (the local winners stay pending for the next select's settle),
+ *   the next kernel in the stream may launch at once (it is the next step's
+ *   HBM pass), and the merges run on one cluster of <= 16 SMs when the union
+ *   fits their shared memory, leaving the rest of the GPU to that pass. */
 int gtk_gtopk_exchange_update(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
                               void* const* peer_inbox, uint64_t* d_epoch,
                               int32_t* acc_idx, float* acc_val, int32_t* d_acc_n, int32_t k,

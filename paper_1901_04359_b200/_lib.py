@@ -50,6 +50,8 @@ EXPORTS = (
     "gtk_select_main_pass",
     "gtk_select_settle",
     "gtk_select_update_deferred",
+    "gtk_select_push_deferred",
+    "gtk_select_settle_global",
     "gtk_merge_workspace_bytes",
     "gtk_top_op",
     "gtk_scatter_update",
@@ -92,6 +94,11 @@ _SIGS = {
     "gtk_select": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _I32, _P], _I32),
     "gtk_select_windowed": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _I32, _P, _P], _I32),
     "gtk_select_update": ([_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _I32, _P, _P, _F, _I32, _I32, _P], _I32),
+    "gtk_select_push_deferred": (
+        [_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _P, _P, _P, _P, _P, _P, _P, _P],
+        _I32,
+    ),
+    "gtk_select_settle_global": ([_P, _P, _P, _P, _P, _P], _I32),
     "gtk_select_update_deferred": (
         [_P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _P, _P, _P, _P, _P, _F, _I32, _I32, _P],
         _I32,

@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include <cstring>
 
@@ -97,8 +98,13 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   __shared__ uint32_t s_n, s_hint;
   __shared__ bool s_poison;
   const unsigned G = gridDim.x, blk = blockIdx.x;
-  pdl_wait();               // launched programmatically behind the select
-  pdl_launch_dependents();  // K3 may become resident; it waits for our completion
+  // a deferred step (no residual to restore: the select left its winners
+  // pending, the next select's finish settles them) lets the next step's HBM
+  // pass launch at once -- it touches neither w nor anything we read or write
+  const bool deferred = a.upd_w && !a.upd_res;
+  if (deferred) pdl_launch_dependents();
+  pdl_wait();  // launched programmatically behind the select
+  if (!deferred) pdl_launch_dependents();
   // every block reads the counter before anyone advances it (block 0 does so
   // after the final grid barrier)
   const uint64_t epoch = __ldcg((const unsigned long long*)a.d_epoch) + 1;
@@ -128,10 +134,6 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   bool pushed = (a.steps[0].tag & kStepPrepushed) != 0;
   for (int s = 0; s < a.nsteps; ++s) {
     const Step st = a.steps[s];
-    // the merges' predicted-band gather counter of the step after this one
-    // (see MergeCtl::spec_n)
-    const uint32_t seq = (uint32_t)(epoch * (uint64_t)a.nsteps + (uint64_t)s);
-    if (blk == 0 && threadIdx.x == 0) a.merge.ctl->spec_n[(seq + 1u) & 1u] = 0u;
     // the next step sends the list this step's merge / copy produces: fuse
     const bool fuse_next = s + 1 < a.nsteps && a.steps[s + 1].send_to >= 0;
     if (st.send_to >= 0 && !pushed) {
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
           m.ll_head = out_slot;
           m.ll_tag = tag;
         }
-        merge_device(m, n_in, n_own, hint_in, hint_own, G, S, wrec, wv, seq);
+        merge_device(m, n_in, n_own, hint_in, hint_own, G, S, wrec, wv);
       } else {
         const uint32_t per = (n_in + G - 1) / G;
         const uint32_t e0 = min(n_in, blk * per), e1 = min(n_in, e0 + per);
@@ -259,7 +261,8 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
     grid_sync(&a.merge.ews->bar, G);  // every tag and the status word final
     if (!(__ldcg(a.d_status) & GTK_DEV_ERROR_MASK)) {
       const uint32_t gn = min((uint32_t)__ldcg(a.d_acc_n), (uint32_t)a.k);
-      const uint32_t ln = min((uint32_t)__ldcg(a.d_in_n), (uint32_t)a.k);
+      // (no residual: a deferred select keeps the local winners pending)
+      const uint32_t ln = a.upd_res ? min((uint32_t)__ldcg(a.d_in_n), (uint32_t)a.k) : 0u;
       const uint32_t ep32 = (uint32_t)epoch;
       const float Pf = (float)a.P;
       // kK3Batch entries per thread per round: every list load, then every
@@ -413,7 +416,10 @@ extern "C" int gtk_gtopk_exchange_update(int32_t rank, int32_t P, const int32_t*
                                          int32_t* step_counts, const int32_t* in_idx, const float* in_val,
                                          const int32_t* d_in_n, void* ws, size_t ws_bytes, float* w, float* res,
                                          float lr, int32_t scaling, uint32_t* d_tags, void* stream) {
-  if (!w || !res || !in_idx || !d_tags || scaling < 0 || scaling > 2 || !std::isfinite(lr) || std::signbit(lr))
+  // res = NULL: the deferred form -- the residual keeps every local winner
+  // pending (gtk_select_push_deferred), only w is updated and the membership
+  // tags written for the next select's settle
+  if (!w || !in_idx || !d_tags || scaling < 0 || scaling > 2 || !std::isfinite(lr) || std::signbit(lr))
     return GTK_EINVAL;
   if (nsteps == 0) return GTK_EINVAL;  // one rank: gtk_select_update
   return exchange_impl(rank, P, schedule, nsteps, peer_inbox, d_epoch, acc_idx, acc_val, d_acc_n, k,
@@ -470,7 +476,9 @@ static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32
                       nullptr, (MergeCtl*)(base + L.ctl), (EngineWS*)(base + L.engine),
                       (int32_t*)(base + L.u_idx), (float*)(base + L.u_val)};
   MergeGrid g;
-  if (!merge_grid_for((const void*)exchange_kernel, k, &g)) return GTK_ECUDA;
+  // deferred (no residual): the exchange runs beside the next step's HBM pass,
+  // so it stays on at most one cluster of SMs when the union fits there
+  if (!merge_grid_for((const void*)exchange_kernel, k, &g, upd_w && !upd_res)) return GTK_ECUDA;
   a.merge.slice_cap = g.slice_cap;
   void* args[] = {&a};
   ProfScope prof(kProfExchange, (cudaStream_t)stream);

@@ -379,30 +379,20 @@ __device__ void engine_write(const Src& src, uint32_t s0, uint32_t s1, uint32_t 
   }
 }
 
-// ---- finish from a band [blo, bhi) of keys that holds the rank-kt key ----
-// Every block gathers its in-band entries (key, idx, block | slot) into the
+// ---- finish from the bin [blo, bhi) of keys that holds the rank-kt key ----
+// Every block gathers its in-bin entries (key, idx, block | slot) into the
 // shared gather buffer (gcount: its global counter; nullptr = G == 1, all in
-// shared memory) and counts its entries above the band; after ONE grid
-// barrier every block ranks the gathered keys (tau = the kt-th largest key,
-// ties at tau by index), derives its output offset and writes its winners.
-// t_band > 0: the rank of the target inside the band, known from a
-// histogram (the band holds it by construction).  t_band = 0: a band
-// predicted from the previous call (merge_device): the blocks sum their
-// above-band counts after the barrier, t_band = kt - that sum, and they
-// return false -- consistently -- when rank kt is not inside the band or the
-// band overflowed the gather buffer; the caller then runs the histogram path
-// (nothing was written but the gather buffer and ws->cta_a).
-// clear_hists: block 0 zeroes the round histograms at the end (they were used).
-// *tau_out (nullable, block 0): the k-th key.
+// shared memory) and counts its entries above the bin; after ONE grid
+// barrier every block ranks the gathered keys (tau = the t_in-th largest of
+// them, t_in = rank of the target inside the bin, ties at tau by index),
+// derives its output offset and writes its winners.
 template <int NT, class Src>
-__device__ bool engine_band_finish(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt, uint32_t t_band,
-                               uint64_t blo, uint64_t bhi, uint32_t* gcount, EngineWS* ws,
-                               EngineSmem<NT>& sm, const Sink& out, unsigned G, bool clear_hists,
-                               uint32_t* tau_out = nullptr) {
+__device__ void engine_gather_finish(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt, uint32_t t_in,
+                                     uint64_t blo, uint64_t bhi, uint32_t* gcount, EngineWS* ws,
+                                     EngineSmem<NT>& sm, const Sink& out, unsigned G) {
   const unsigned blk = blockIdx.x;
   const bool solo = gcount == nullptr;
-  const bool above_known = t_band != 0;
-  uint32_t n_above = 0, above_all = 0;
+  uint32_t n_above = 0;
   if (solo && threadIdx.x == 0) sm.ng = 0;
   if (solo) __syncthreads();
   // (block-uniform trip count: the in-bin slots are reserved with one
@@ -426,7 +416,7 @@ __device__ bool engine_band_finish(const Src& src, uint32_t s0, uint32_t s1, uin
     p0 = __shfl_sync(kFull, p0, __ffs(bal) - 1);
     if (inb) {
       const uint32_t p = p0 + __popc(bal & lanemask_lt());
-      if (p >= (uint32_t)kGatherCap) continue;  // overflow: only a predicted band (checked below)
+      if (p >= (uint32_t)kGatherCap) continue;  // (cannot happen: in_bin <= kGatherCap)
       if (solo) {
         sm.keys[p] = key;
         sm.gidx[p] = i;
@@ -451,26 +441,15 @@ __device__ bool engine_band_finish(const Src& src, uint32_t s0, uint32_t s1, uin
       sm.gidx[j] = __ldcg(&ws->gather_idx[j]);
       sm.gblk[j] = __ldcg(&ws->gather_blk[j]);
     }
-    for (uint32_t j = kGatherMax + threadIdx.x; j < ng; j += NT) {  // last-round bins up to kGatherCap
+    for (uint32_t j = kGatherMax + threadIdx.x; j < min(ng, (uint32_t)kGatherCap); j += NT) {  // up to kGatherCap
       sm.keys[j] = __ldcg(&ws->gather_key[j]);
       sm.gidx[j] = __ldcg(&ws->gather_idx[j]);
       sm.gblk[j] = __ldcg(&ws->gather_blk[j]);
     }
-    for (unsigned j = threadIdx.x; j < (above_known ? blk : G); j += NT) {
-      const uint32_t c = __ldcg(&ws->cta_a[j]);
-      if (j < blk) above_before += c;
-      else above_all += c;
-    }
+    for (unsigned j = threadIdx.x; j < blk; j += NT) above_before += __ldcg(&ws->cta_a[j]);
     if (threadIdx.x == 0) sm.ng = ng;
   }
   above_before = block_sum<NT>(above_before, sm.scan);  // also publishes sm.keys / sm.ng
-  uint32_t t_in = t_band;  // rank of the target inside the band
-  if (!above_known) {
-    const uint32_t above = solo ? n_above : above_before + block_sum<NT>(above_all, sm.scan);
-    const uint32_t ngc = sm.ng;
-    if (ngc > (uint32_t)kGatherCap || above >= kt || kt > above + ngc) return false;  // the band missed
-    t_in = kt - above;
-  }
   sink_stamp(out, 1);
   const uint32_t ng = sm.ng;
   // tau = t_in-th largest gathered key; gt = # gathered keys > tau.  A
@@ -571,16 +550,13 @@ __device__ bool engine_band_finish(const Src& src, uint32_t s0, uint32_t s1, uin
   engine_write<NT>(src, s0, s1, above_before + extra, keep_fn, sm, out);
   sink_stamp(out, 3);
   if (blk == 0) {  // every block is past its last histogram read
-    if (clear_hists)
-      for (int rr = 0; rr < kRounds; ++rr)
-        for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[rr][b] = 0;
+    for (int rr = 0; rr < kRounds; ++rr)
+      for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[rr][b] = 0;
     if (threadIdx.x == 0) {
       sink_count(out, kt, tau);
       sink_pending(out, tau);
-      if (tau_out) *tau_out = tau;
     }
   }
-  return true;
 }
 
 // The engine proper.  Every block calls it with its own slice [s0, s1).
@@ -725,8 +701,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
     const bool single_key = (bhi - blo == 1);
     // the last round always gathers if it can (a bin is then at most 8 keys wide)
     if (in_bin <= (uint32_t)kGatherCap) {
-      engine_band_finish<NT>(src, s0, s1, kt, t_in, blo, bhi, solo ? nullptr : &ws->gather_n[r], ws, sm, out, G,
-                             true);
+      engine_gather_finish<NT>(src, s0, s1, kt, t_in, blo, bhi, solo ? nullptr : &ws->gather_n[r], ws, sm, out, G);
       return true;
     }
     if (single_key) {

@@ -29,7 +29,9 @@ struct MergeGrid {
   uint32_t slice_cap;
   bool cluster;
 };
-bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out);
+// compact: one cluster of up to 16 CTAs whenever the union fits their shared
+// memory (a merge that shares the GPU with an HBM pass)
+bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out, bool compact = false);
 // launch a merge-type kernel on its MergeGrid (cluster or cooperative)
 int merge_launch(const void* func, const MergeGrid& g, void** args, size_t smem, cudaStream_t st, bool pdl);
 

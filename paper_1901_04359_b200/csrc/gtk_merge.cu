@@ -69,7 +69,7 @@ static bool cluster_fits(const void* func, int cs, size_t smem) {
   return ok;
 }
 
-bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out) {
+bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out, bool compact) {
   if (!ensure_dyn_smem(func, merge_smem_bytes(kMergeSliceCapMax))) return false;
   const int lim = num_sms();
   if (lim <= 0) return false;
@@ -89,7 +89,8 @@ bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out) {
   const bool c_smem = (slots + gc - 1) / gc <= (uint64_t)kMergeSliceCapMax;
   // cluster mode only where the union spreads over <= 16 CTAs at the target density
   bool use_cluster = force_c != 0 && c_smem && (force_g > 0 ? force_g <= kMergeMaxCluster
-                                                             : (force_c == 1 || want_c <= (uint64_t)kMergeMaxCluster));
+                                                             : (force_c == 1 || compact ||
+                                                                want_c <= (uint64_t)kMergeMaxCluster));
   if (force_c == 1 && !c_smem) return false;
   if (use_cluster) {
     const uint32_t sc = cap_for(gc);

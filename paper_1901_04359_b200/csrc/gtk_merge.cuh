@@ -40,12 +40,7 @@ constexpr int kMergeSoloSlots = 1024;    // unions up to this many slots: one CT
 
 struct MergeCtl {
   uint32_t n_valid;
-  // gather counters of the predicted-band finish, double-buffered by the
-  // exchange's step sequence number: step q gathers into spec_n[q & 1] and
-  // block 0 zeroes spec_n[(q + 1) & 1] (last read in step q - 1, behind the
-  // barrier between the steps; next used in step q + 1, behind the next one)
-  uint32_t spec_n[2];
-  uint32_t pad[61];
+  uint32_t pad[63];
 };
 
 struct MergeLayout {
@@ -212,43 +207,9 @@ __device__ __forceinline__ MergeWindowRec load_window_rec(const uint32_t* rec) {
   return r;
 }
 
-// Predicted band (exchange steps with a carried record of the same k): the
-// previous call's k-th key tau_p with room for ~4 bins of the record's
-// resolution (~64 entries per bin at tau) or twice the last move of tau on
-// either side -- ~512 union entries, inside the 1024-entry gather buffer;
-// skipped when the expected band holds more than 3/4 of the buffer.
-// The finish then needs ONE grid barrier (gather + counts) instead of two
-// (histogram, then gather); a miss costs one extra barrier and the histogram
-// path.
-struct MergeBand {
-  bool on;
-  uint32_t blo;
-  uint64_t bhi;
-};
-__device__ __forceinline__ MergeBand predicted_band(const MergeWindowRec& rv, uint32_t k) {
-  MergeBand b{false, 0u, 0ull};
-  if (!(rv.w0 & 1u) || rv.k != k || rv.tau == 0u || rv.shift > 24u) return b;
-  uint64_t h = 4ull << rv.shift;
-  if (rv.tau2 != 0u) {
-    const uint64_t mv = rv.tau > rv.tau2 ? rv.tau - rv.tau2 : rv.tau2 - rv.tau;
-    h = max(h, 2 * mv);
-  }
-  // ~kMergeBinTarget entries per 2^shift keys at tau: a band that would
-  // overflow the gather buffer (tau moving by many entries per call, e.g.
-  // the flat-topped residuals of a training run) is not tried at all
-  if (((2 * h + 1) * kMergeBinTarget >> rv.shift) > (uint64_t)kGatherCap * 3 / 4) return b;
-  b.on = true;
-  b.blo = rv.tau > h ? (uint32_t)(rv.tau - h) : 0u;
-  b.bhi = min((uint64_t)rv.tau + h + 1, (uint64_t)0x80000000ull);
-  return b;
-}
-
-// seq: the exchange's step sequence number (predicted band enabled with rec);
-// ~0u = none (standalone merges)
 static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t na, uint32_t nb, uint32_t hint_a,
                                                     uint32_t hint_b, unsigned G, MergeSmem& S,
-                                                    uint32_t* rec = nullptr, MergeWindowRec rv = {},
-                                                    uint32_t seq = ~0u) {
+                                                    uint32_t* rec = nullptr, MergeWindowRec rv = {}) {
   EngineSmem<kMergeThreads>& esm = S.esm;
   const unsigned blk = blockIdx.x;
   const uint32_t N = na + nb;
@@ -407,46 +368,6 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   merge_stamp(a, 2);  // union slots + histogram built
   const bool solo = G == 1;
   const SliceSrc src{slice_idx, slice_val, a.u_idx, a.u_val, d0, in_smem, true};
-  const MergeBand band = (rec && seq != ~0u) ? predicted_band(rv, a.k) : MergeBand{false, 0u, 0ull};
-  if (band.on) {
-    if (!solo && threadIdx.x == 0 && S.s_valid) atomicAdd(&a.ctl->n_valid, S.s_valid);
-    __shared__ uint32_t s_tau;
-    const Sink bout{a.o_idx, a.o_val, a.d_no, nullptr, true, a.trace ? a.trace + 5 : nullptr,
-                    nullptr, 0u, 0u, 0u, 3u, a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling, a.tag, a.tag_val,
-                    a.ll_body, a.ll_head, a.ll_tag};
-    if (engine_band_finish<kMergeThreads>(src, d0, d1, a.k, 0u, band.blo, band.bhi,
-                                          solo ? nullptr : &a.ctl->spec_n[seq & 1u], a.ews, esm, bout, G, false,
-                                          &s_tau)) {
-      merge_stamp(a, 4);
-      if (blk == 0 && threadIdx.x == 0) {
-        // the next call's band: centred on this tau, resolution from the
-        // density the band just measured (~kMergeBinTarget entries per bin)
-        const uint32_t tau = s_tau, ng = esm.ng;
-        const uint64_t width = band.bhi - band.blo;
-        uint32_t sd = rv.shift + 1;
-        if (ng > 0) {
-          const uint64_t dens_w = ((uint64_t)kMergeBinTarget * width) / ng;
-          sd = 0;
-          while (sd < 24 && (2ull << sd) <= dens_w) ++sd;
-        }
-        const uint64_t half = (uint64_t)(kBins / 2) << sd;
-        rec[1] = tau > half ? (uint32_t)(tau - half) : 0u;
-        rec[2] = sd;
-        rec[3] = a.k;
-        rec[4] = tau;
-        rec[5] = rv.tau;
-        rec[0] = 1u | (max(2u, rv.w0 >> 8) << 8);
-        if (!solo) a.ctl->n_valid = 0;  // every block added before the band barrier; nobody reads it
-        if (a.trace) {
-          a.trace[13] = (int64_t)ng;  // diagnostics: gathered band entries
-          a.trace[14] = band.blo;
-          a.trace[15] = (int64_t)(band.bhi - band.blo);
-        }
-      }
-      return;
-    }
-    merge_stamp(a, 3);  // (the band missed: the histogram path below)
-  }
   uint32_t n_valid;
   if (solo) {
     n_valid = S.s_valid;  // the histogram stays in shared memory
@@ -455,7 +376,7 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
       const uint32_t c = esm.hist[b];
       if (c) atomicAdd(&a.ews->hist[0][b], c);
     }
-    if (!band.on && threadIdx.x == 0 && S.s_valid) atomicAdd(&a.ctl->n_valid, S.s_valid);
+    if (threadIdx.x == 0 && S.s_valid) atomicAdd(&a.ctl->n_valid, S.s_valid);
     grid_sync(&a.ews->bar, G);
     // the global histogram -> shared memory by async copies, landing while
     // the valid count is read: the engine's bin search then needs no second

@@ -774,6 +774,13 @@ struct FinishArgs {
   const int32_t* prev_count = nullptr;
   const float* grad = nullptr;
   uint32_t fix_cap = 0;  // fix-list entries staged in shared memory behind the slice
+  // P > 1 (gtk_select_push_deferred): only previous winners that made the
+  // previous global list were zeroed by the reference (optimizer.py:227-230
+  // returns the others to the residual): membership = prev_tags[i] == the
+  // low word of *prev_epoch (the exchange plan's tags / epoch); nullable (P = 1)
+  const uint32_t* prev_tags = nullptr;
+  const uint64_t* prev_epoch = nullptr;
+  const float* res_in = nullptr;
   uint32_t* ofs_out = nullptr;       // this call's per-block output positions (deferred: the next call's j0 / j1)
   const uint32_t* prev_ofs = nullptr;  // the previous call's (in its workspace), nullable
 };
@@ -816,6 +823,7 @@ __device__ uint32_t deferred_fixup(const FinishArgs& a, EngineSmem<kFinishThread
                                    uint32_t* f_flag, uint32_t t0, uint32_t t1, uint32_t* n_ins_out) {
   const uint32_t lo = __ldcg(&a.ctl->lo), shift = __ldcg(&a.ctl->shift);
   const uint32_t n_prev = min((uint32_t)max(__ldcg(a.prev_count), 0), a.m);
+  const uint32_t ep32 = a.prev_epoch ? (uint32_t)__ldcg((const unsigned long long*)a.prev_epoch) : 0u;
   const int32_t E0 = (int32_t)min((uint64_t)t0 * kTile, (uint64_t)a.m);
   const int32_t E1 = (int32_t)min((uint64_t)t1 * kTile, (uint64_t)a.m);
   // my range of the previous selection: its finish recorded every block's
@@ -842,13 +850,20 @@ __device__ uint32_t deferred_fixup(const FinishArgs& a, EngineSmem<kFinishThread
     const uint32_t j = base + threadIdx.x;
     const bool has = j < j1;
     int32_t e = 0;
-    float ap = 0.0f, gv = 0.0f;
+    float ap = 0.0f, gv = 0.0f, rp = 0.0f;
+    uint32_t tg = ep32;
     if (has) e = __ldcg(a.prev_idx + j);
     if (has) {
       ap = __ldcg(a.res_out + e);
       gv = __ldcg(a.grad + e);
+      if (a.prev_tags) {
+        tg = __ldcg(a.prev_tags + e);
+        rp = __ldcg(a.res_in + e);
+      }
     }
-    const float A = __fadd_rn(0.0f, gv);
+    // a member of the previous global list: res = +0 there; otherwise the
+    // reference returned the value: res = +0 + acc (acc itself unless -0)
+    const float A = (tg == ep32) ? __fadd_rn(0.0f, gv) : __fadd_rn(__fadd_rn(0.0f, rp), gv);
     bool was = false, now = false;
     if (has) {
       if (__float_as_uint(A) != __float_as_uint(ap)) a.res_out[e] = A;
@@ -1016,7 +1031,7 @@ __global__ void __launch_bounds__(kFinishThreads, GTK_FINISH_MIN_BLOCKS) select_
            a.trace ? a.trace + 3 : nullptr,
            a.window, wlevel, wtau, wtau2, 1u, a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling};
   if (a.chain) out.pend_rec = a.window;
-  if (a.ofs_out) {  // written by the candidate path's band finish only (same tile partition next call)
+  if (a.ofs_out) {  // written by the candidate path's gather finish only (same tile partition next call)
     if (blk == 0 && threadIdx.x == 0) a.ofs_out[0] = 0u;
     out.blk_ofs = a.ofs_out;
   }
@@ -1258,16 +1273,18 @@ struct PeerPush {
   uint64_t* slot0;
   const uint64_t* epoch;
 };
-struct Deferred {  // gtk_select_update_deferred
+struct Deferred {  // gtk_select_update_deferred / gtk_select_push_deferred
   bool on;
   const int32_t* prev_idx;
   const int32_t* prev_count;
   const void* prev_ws;
+  const uint32_t* prev_tags = nullptr;
+  const uint64_t* prev_epoch = nullptr;
 };
 static int select_impl(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
                        int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,
                        size_t ws_bytes, int32_t flags, uint32_t* d_window, FusedUpdate upd, void* stream,
-                       PeerPush push = {nullptr, nullptr}, Deferred dfr = {false, nullptr, nullptr, nullptr});
+                       PeerPush push = {nullptr, nullptr}, Deferred dfr = {false, nullptr, nullptr, nullptr, nullptr, nullptr});
 
 extern "C" int gtk_select_windowed(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
                                    int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status,
@@ -1308,6 +1325,17 @@ extern "C" int gtk_select_update_deferred(const float* res_in, const float* grad
   return select_impl(res_in, grad, res_out, m, k, sel_idx, sel_val, d_count, d_status, ws, ws_bytes, 0, d_window,
                      FusedUpdate{w, lr, (float)P, scaling}, stream, PeerPush{nullptr, nullptr},
                      Deferred{true, prev_sel_idx, prev_count, prev_sel_idx ? prev_ws : nullptr});
+}
+
+extern "C" int gtk_select_push_deferred(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
+                                        int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status,
+                                        void* ws, size_t ws_bytes, uint32_t* d_window, const int32_t* prev_sel_idx,
+                                        const int32_t* prev_count, const void* prev_ws, const uint32_t* prev_tags,
+                                        void* peer_slot0, const uint64_t* d_epoch, void* stream) {
+  if (!res_in || !peer_slot0 || !d_epoch || (prev_sel_idx && !prev_tags)) return GTK_EINVAL;
+  return select_impl(res_in, grad, res_out, m, k, sel_idx, sel_val, d_count, d_status, ws, ws_bytes, 0, d_window,
+                     FusedUpdate{nullptr, 0.0f, 1.0f, 0}, stream, PeerPush{(uint64_t*)peer_slot0, d_epoch},
+                     Deferred{true, prev_sel_idx, prev_count, prev_sel_idx ? prev_ws : nullptr, prev_tags, d_epoch});
 }
 
 static int select_impl(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
@@ -1483,6 +1511,9 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
     fa.prev_count = dfr.prev_count;
     fa.grad = grad;
     fa.fix_cap = fix_cap;
+    fa.prev_tags = dfr.prev_tags;
+    fa.prev_epoch = dfr.prev_epoch;
+    fa.res_in = res_in;
     fa.ofs_out = (uint32_t*)(base + L.blk_ofs);
     fa.prev_ofs = dfr.prev_ws ? (const uint32_t*)((const char*)dfr.prev_ws + L.blk_ofs) : nullptr;
   }
@@ -1535,6 +1566,26 @@ __global__ void settle_kernel(float* res, const int32_t* sel_idx, const int32_t*
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
     res[__ldg(sel_idx + e)] = 0.0f;
   if (blockIdx.x == 0 && threadIdx.x == 0) window[0] &= ~kRecPending;
+}
+
+// the residual after a deferred P > 1 step: +0.0 at the local winners that
+// made the global list (tags == low word of *d_epoch), +0 + acc at the others
+__global__ void settle_global_kernel(float* res, const int32_t* sel_idx, const int32_t* d_count, const uint32_t* tags,
+                                     const uint64_t* d_epoch) {
+  const uint32_t n = (uint32_t)__ldg(d_count);
+  const uint32_t ep32 = (uint32_t)__ldcg((const unsigned long long*)d_epoch);
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int32_t i = __ldg(sel_idx + e);
+    res[i] = __ldcg(tags + i) == ep32 ? 0.0f : __fadd_rn(0.0f, res[i]);
+  }
+}
+
+extern "C" int gtk_select_settle_global(float* res, const int32_t* sel_idx, const int32_t* d_count,
+                                        const uint32_t* tags, const uint64_t* d_epoch, void* stream) {
+  if (!res || !sel_idx || !d_count || !tags || !d_epoch) return GTK_EINVAL;
+  settle_global_kernel<<<num_sms(), 256, 0, (cudaStream_t)stream>>>(res, sel_idx, d_count, tags, d_epoch);
+  GTK_CHECK_LAUNCH();
+  return GTK_OK;
 }
 
 extern "C" int gtk_select_settle(float* res, const int32_t* sel_idx, const int32_t* d_count, uint32_t* d_window,

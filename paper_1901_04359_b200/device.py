@@ -255,6 +255,31 @@ def select_update_deferred(res_in, grad: torch.Tensor, res_out: torch.Tensor, k:
     )
 
 
+def select_push_deferred(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, out: DeviceList,
+                         status: torch.Tensor, window: torch.Tensor, ws: torch.Tensor, prev: DeviceList | None,
+                         prev_ws: torch.Tensor | None, tags: torch.Tensor, peer_slot0: int,
+                         epoch: torch.Tensor) -> None:
+    """K1 for the deferred P > 1 step (gtk_select_push_deferred): winners stay
+    pending in res_out, the selection goes to the exchange's first partner,
+    `prev` is settled by membership of the previous global list (`tags` /
+    `epoch`: the exchange plan's); the exchange then runs with res = None."""
+    m = grad.numel()
+    _lib.call(
+        "gtk_select_push_deferred", P(res_in), P(grad), P(res_out), m, k, P(out.idx), P(out.val), P(out.count),
+        P(status), P(ws), ctypes.c_size_t(ws.numel()), P(window),
+        P(prev.idx) if prev is not None else None, P(prev.count) if prev is not None else None,
+        P(prev_ws) if prev is not None else None, P(tags), ctypes.c_void_p(peer_slot0), P(epoch),
+        stream_of(grad.device),
+    )
+
+
+def settle_global(res: torch.Tensor, sel: DeviceList, tags: torch.Tensor, epoch: torch.Tensor) -> None:
+    """gtk_select_settle_global: the residual after the last deferred P > 1
+    step (+0.0 at the local winners in the last global list)."""
+    _lib.call("gtk_select_settle_global", P(res), P(sel.idx), P(sel.count), P(tags), P(epoch),
+              stream_of(res.device))
+
+
 def settle(res: torch.Tensor, sel: DeviceList, window: torch.Tensor) -> None:
     """gtk_select_settle: +0.0 at the last chained select's winners (the
     residual the reference keeps), and the record's pending flag cleared."""

@@ -84,7 +84,7 @@ class GTopKPipeline:
         self.chained = False  # steps leave their winners pending (settled by sync_state)
         self.deferred = False
         self._dsteps = 0  # deferred steps enqueued (the first has no previous selection)
-        if self.P == 1 and self.mode == "defer":
+        if self.mode == "defer" and (self.P == 1 or self.plan.push_slot0 is not None):
             self.dsel = [DeviceList(self.m, self.k, self.dev) for _ in range(2)]
             self.dws = [_dev.select_workspace(self.m, self.k, self.dev, slot=1 + i) for i in range(2)]
             # the next main pass starts before this finish has written the next
@@ -99,9 +99,18 @@ class GTopKPipeline:
             # one rank: the global top-k is the selection; K3 rides on K1's finish
             if self.mode == "defer":
                 prev = self.dsel[1 - parity] if self._dsteps > 0 else None
-                _dev.select_update_deferred(res_in, grad, res_out, self.k, self.dsel[parity], self.status,
-                                            self.dwin[parity], self.dws[parity], prev, self.state._w, self.lr, 1,
-                                            self.scaling, prev_ws=self.dws[1 - parity])
+                try:
+                    _dev.select_update_deferred(res_in, grad, res_out, self.k, self.dsel[parity], self.status,
+                                                self.dwin[parity], self.dws[parity], prev, self.state._w, self.lr,
+                                                1, self.scaling, prev_ws=self.dws[1 - parity])
+                except ValueError:
+                    if self._dsteps:
+                        raise
+                    # (very large k: the finish's fix list does not fit next to
+                    # its slice in shared memory) -- chained selects instead
+                    self.mode = "chain"
+                    del self.dsel, self.dws, self.dwin
+                    return self._enqueue(parity)
                 self._dsteps += 1
                 self.deferred = True
                 return
@@ -109,6 +118,31 @@ class GTopKPipeline:
             _dev.select_update(res_in, grad, res_out, self.k, self.sel, self.status, self.window,
                                self.state._w, self.lr, 1, self.scaling, chain=chain)
             self.chained = chain
+            return
+        if (self.P > 1 and self.mode == "defer" and _dev.sparse_update_fusable(self.lr, self.mom)
+                and self.plan.push_slot0 is not None):
+            # deferred P > 1 step: the selection goes to the first partner as
+            # it is written, the exchange updates w only (res = None) and lets
+            # the next step's HBM pass run beside it; the next finish settles
+            # this step's winners by membership of the global list
+            plan = self.plan
+            if plan.tags is None or plan.tags.numel() < self.m:
+                plan.tags = torch.zeros(self.m, dtype=torch.int32, device=self.dev)
+            prev = self.dsel[1 - parity] if self._dsteps > 0 else None
+            try:
+                _dev.select_push_deferred(res_in, grad, res_out, self.k, self.dsel[parity], self.status,
+                                          self.dwin[parity], self.dws[parity], prev, self.dws[1 - parity],
+                                          plan.tags, plan.push_slot0, plan.epoch)
+            except ValueError:
+                if self._dsteps:
+                    raise
+                self.mode = "plain"  # (very large k: see the P = 1 branch)
+                del self.dsel, self.dws, self.dwin
+                return self._enqueue(parity)
+            self.group.enqueue_exchange(plan, self.dsel[parity], self.status,
+                                        update=(self.state._w, None, self.lr, self.scaling), prepushed=True)
+            self._dsteps += 1
+            self.deferred = True
             return
         if self.P > 1 and _dev.sparse_update_fusable(self.lr, self.mom) and self.plan.push_slot0 is not None:
             # the selection goes to the first partner as it is written
@@ -265,7 +299,7 @@ class GTopKPipeline:
             # the same for a deferred step (the next step's finish would have
             # corrected its own view of them); idempotent if the pipeline goes
             # on -- it owns the state's buffers until then
-            _dev.settle(self.res[p], self.dsel[1 - p], self.dwin[1 - p])
+            self._settle_into(self.res[p], p)
         st._res, st._res2 = self.res[p], self.res[1 - p]
         st.iteration += self.t - getattr(self, "_synced_t", 0)
         self._synced_t = self.t
@@ -280,8 +314,15 @@ class GTopKPipeline:
         if self.chained and self.t > 0:
             _dev.settle(res, self.sel, self.window.clone())
         if self.deferred and self.t > 0:
-            _dev.settle(res, self.dsel[1 - p], self.dwin[1 - p].clone())
+            self._settle_into(res, p)
         return res
+
+    def _settle_into(self, res: torch.Tensor, p: int) -> None:
+        """+0.0 at the last deferred step's winners (P > 1: those in its global list)."""
+        if self.P == 1:
+            _dev.settle(res, self.dsel[1 - p], self.dwin[1 - p].clone())
+        else:
+            _dev.settle_global(res, self.dsel[1 - p], self.plan.tags, self.plan.epoch)
 
     def global_list(self) -> DeviceList:
         if self.plan is not None:

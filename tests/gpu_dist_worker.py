@@ -103,6 +103,21 @@ def main():
         orc.gtopk_step_all(ref2, grads[it % 2], k)
     check(np.array_equal(bits(st2.weights.cpu().numpy()), bits(ref2[r].weights)), "pipeline weights")
     check(np.array_equal(bits(st2.residual.cpu().numpy()), bits(ref2[r].residual)), "pipeline residual")
+    check(pipe.deferred, "pipeline: deferred steps (the default mode)")
+    # 3b. the non-deferred step (select_push + exchange with the residual restore)
+    os.environ["GTK_PIPE_MODE"] = "plain"
+    try:
+        st2b = opt.make_state(torch.zeros(m, device=dev), lr=0.1)
+        pipeb = GTopKPipeline(ep, st2b, k, dg)
+        pipeb.capture()
+        pipeb.run(30)
+        pipeb.check()
+        pipeb.sync_state()
+        check(not pipeb.deferred, "plain pipeline mode")
+        check(np.array_equal(bits(st2b.weights.cpu().numpy()), bits(ref2[r].weights)), "plain pipeline weights")
+        check(np.array_equal(bits(st2b.residual.cpu().numpy()), bits(ref2[r].residual)), "plain pipeline residual")
+    finally:
+        del os.environ["GTK_PIPE_MODE"]
 
     # 4. poison: a non-finite gradient on rank P-1 fails the step everywhere,
     #    state untouched

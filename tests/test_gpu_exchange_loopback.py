@@ -480,15 +480,14 @@ def test_select_push_then_prepushed_exchange(P):
 
 @pytest.mark.parametrize("P,k,grid", [(2, 1500, "auto"), (4, 1500, "auto"), (4, 25_600, "auto"),
                                       (2, 270, "auto"), (4, 3000, "grid")])
-def test_exchange_carried_band_hits_and_misses(P, k, grid, monkeypatch):
-    """Successive calls of one exchange plan: from the second call on, every
-    merge gathers a band of keys predicted from the previous call's k-th key
-    (csrc/gtk_merge.cuh predicted_band: one grid barrier instead of two).
-    The call sequence drives hits (same distribution), misses (every value
-    scaled x8: tau jumps out of the band), gather overflows (integer ties:
-    thousands of keys equal to tau) and cancellations (fewer than k union
-    entries); every call's global list is checked bitwise against the
-    oracle's tree fold, with the fused K3."""
+def test_exchange_successive_calls_carried_windows(P, k, grid, monkeypatch):
+    """Successive calls of one exchange plan: every merge step carries its
+    key window from the previous call (csrc/gtk_merge.cuh, MergeWindowRec).
+    The call sequence drives steady windows (same distribution), misses
+    (every value scaled x8: the k-th key jumps out of the window), massive
+    ties (integer gradients: thousands of keys equal to the k-th) and
+    cancellations (fewer than k union entries); every call's global list is
+    checked bitwise against the oracle's tree fold, with the fused K3."""
     import torch
 
     from oracle import gtopk_oracle as orc
@@ -526,3 +525,64 @@ def test_exchange_carried_band_hits_and_misses(P, k, grid, monkeypatch):
         ew, er = _k3_expect(w0, res0, lists[rank], final[rank], 0.01, P, 0)
         assert np.array_equal(bits(w.cpu().numpy()), bits(ew)), (P, k, call, kind)
         assert np.array_equal(bits(res.cpu().numpy()), bits(er)), (P, k, call, kind)
+
+
+@pytest.mark.parametrize("P,kind", [(2, "normal"), (4, "normal"), (2, "ties")])
+def test_deferred_p_gt_1_step_chain(P, kind):
+    """The deferred P > 1 step on rank P - 1, partners emulated by the loopback
+    inbox: gtk_select_push_deferred (winners pending, selection pushed, the
+    previous step's winners settled by membership of the previous global
+    list) then gtk_gtopk_exchange_update with res = NULL (w only).  Step by
+    step against the oracle's P-rank trajectory (optimizer.py:199-252): the
+    pushed selection, the global list, w, and the settled residual."""
+    import torch
+
+    from oracle import gtopk_oracle as orc
+
+    m, k, lr = 200_003, 400, 0.05
+    rng = np.random.default_rng(900 + P + (kind == "ties"))
+    rank = P - 1
+    scheds = schedules_for(P, "butterfly")
+    lb = Loopback(rank, P, scheds[rank], k, m, prepushed=True)
+    d = lb.d
+    dv = lb.dv
+    states = [orc.State(np.zeros(m, F32), lr) for _ in range(P)]
+    R = [torch.zeros(m, device=d), torch.empty(m, device=d)]
+    w = torch.zeros(m, device=d)
+    wins = [dv.new_window(d) for _ in range(2)]
+    wss = [dv.select_workspace(m, k, d, slot=31 + i) for i in range(2)]
+    sels = [dv.DeviceList(m, k, d) for _ in range(2)]
+    part = scheds[rank][0][0]
+    cur = 0
+    for t in range(8):
+        tag = t + 1
+        if kind == "ties":
+            grads = [rng.integers(-3, 4, m).astype(F32) for _ in range(P)]
+        else:
+            grads = [rng.standard_normal(m).astype(F32) for _ in range(P)]
+        # the oracle's step for every rank; what each rank sends at each step
+        before = [(s.weights.copy(), s.residual.copy()) for s in states]
+        (gi, gv), local = orc.gtopk_step_all(states, grads, k)
+        _sent, recv, final = simulate([(i, v) for i, v in local], k, scheds)
+        for s, got in enumerate(recv[rank]):
+            if got is not None:
+                lb.prefill(s, tag, encode_slot(k, tag, *got))
+        par = t % 2
+        lb.status.zero_()
+        dv.select_push_deferred(R[cur], torch.from_numpy(grads[rank]).to(d), R[1 - cur], k, sels[par], lb.status,
+                                wins[par], wss[par], sels[1 - par] if t else None, wss[1 - par], lb.tags,
+                                lb.inbox[part].data_ptr(), lb.epoch)
+        word = lb.call(None, w=w, res=None, lr=float(F32(lr)), local_on_dev=sels[par])
+        assert word & 0x3D == 0, (t, hex(word))
+        # the pushed selection (step 0 records written by K1's finish)
+        n, _h, si, sv_ = decode_slot(lb.sent_slot(0, tag), k, tag)
+        assert n == len(local[rank][0]) and np.array_equal(si, local[rank][0]), (P, kind, t)
+        assert np.array_equal(bits(sv_), bits(local[rank][1])), (P, kind, t)
+        ai, av = lb.acc.to_host()
+        assert np.array_equal(ai, gi) and np.array_equal(bits(av), bits(gv)), (P, kind, t)
+        assert np.array_equal(bits(w.cpu().numpy()), bits(states[rank].weights)), (P, kind, t)
+        cur = 1 - cur
+        settled = R[cur].clone()
+        dv.settle_global(settled, sels[par], lb.tags, lb.epoch)
+        assert np.array_equal(bits(settled.cpu().numpy()), bits(states[rank].residual)), (P, kind, t)
+        del before

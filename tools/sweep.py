@@ -12,6 +12,14 @@ Per config and P (= the torchrun world size, one rank per GPU):
   api_ms      : the public optimizer step (gtopk_step / topk_step / dense_step)
                 with device-resident gradients, one status read per step
                 (host syncs included), max over ranks.
+  cpu_ref     : the reference's CPU path at the same (m, rho, P) -- the oracle
+                port (numpy, one host thread per rank like run_workers), full
+                size, mean over `--cpu-steps` timed steps -- with the host's
+                core count and CPU model (rank 0 only; `--no-cpu` skips it).
+  protocol    : `--protocol`: the reference's collective benchmark
+                (cli.py:246-294: warmup 3, repeats 10, per-rank rows of bytes
+                / messages / rounds / mean wall ms / std) for configs 1 and 3
+                through bench_protocol.run_bench, CSV with the reference's header.
 Config 1 (m=1M, P=4 simulated workers) runs in-process on one GPU: 4 logical
 ranks (create_local_cluster + run_workers), the reference's own harness.
 """
@@ -48,6 +56,9 @@ def main():
     ap.add_argument("--configs", default="1,2,3,4,5")
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=1)
+    ap.add_argument("--protocol", action="store_true")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -92,6 +103,15 @@ def main():
         e1.synchronize()
         return max_over_ranks(e0.elapsed_time(e1) / steps)
 
+    from bench import cpu_model, host_cores, oracle_steps
+
+    def cpu_ref(m, rho, Pc):
+        if rank != 0 or args.no_cpu:
+            return None
+        ms, desc = oracle_steps(m, rho, Pc, args.cpu_steps, 0)
+        return {"ms": round(ms, 1), "kind": "port", "cores": min(Pc, host_cores()),
+                "host_cores": host_cores(), "cpu": cpu_model(), "sample": desc}
+
     def emit(row):
         row.update(P=P, n_gpus=world)
         rows.append(row)
@@ -122,7 +142,7 @@ def main():
         ts = gk.run_workers(eps, worker)
         row = {"config": 1, "model": "synthetic-1M", "m": m, "rho": rho, "k": k,
                "note": "P=4 logical ranks on one GPU (create_local_cluster + run_workers), host wall clock",
-               "api_ms": {"gtopk_step": round(max(ts), 4)}}
+               "api_ms": {"gtopk_step": round(max(ts), 4)}, "cpu_ref": cpu_ref(m, rho, Pl)}
         rows.append(row)
         print(json.dumps(row), flush=True)
 
@@ -169,9 +189,29 @@ def main():
                 api["dense_step"] = round(timed(lambda: opt.dense_step(st_d, ep, grads[0], P), n_api), 4)
                 del st_t, st_d
             row["api_ms"] = api
+            row["cpu_ref"] = cpu_ref(m, rho, P)
             emit(row)
             del pipe, state, grads
             torch.cuda.empty_cache()
+
+    if args.protocol:
+        from paper_1901_04359_b200 import bench_protocol
+
+        cases = []
+        if world == 1:
+            cases.append((4, 1_000_000, 0.001, None))  # config 1: P=4 in-process ranks on one GPU
+        cases.append((P, 14_700_000, 0.001, ep if world > 1 else None))  # config 3 at this job's P
+        for Pc, m, rho, e in cases:
+            rws = bench_protocol.run_bench(Pc, m=m, rho=rho, endpoint=e, with_device_ms=True)
+            if world > 1:
+                allr = [None] * world
+                dist.all_gather_object(allr, rws)
+                rws = [r for part in allr for r in part]
+            if rank == 0:
+                print(bench_protocol.BENCH_HEADER + ",device_ms", flush=True)
+                for r in rws:
+                    print(r, flush=True)
+                rows.append({"protocol": {"P": Pc, "m": m, "rho": rho, "rows": rws}})
 
     if rank == 0 and args.out:
         with open(args.out, "w") as fh:
