@@ -399,6 +399,9 @@ def run_b200(args, rank, world):
             "run": {
                 "exchange": exch,
                 "step": "K1 select + gTopKAllReduce + K3 update, CUDA-graph replay",
+                "select_mode": pipe.mode + (" (the next step's HBM pass overlaps this step's finish"
+                                            + (" and exchange" if P > 1 else "") + ")"
+                                            if pipe.mode == "defer" else ""),
                 "l2": "inputs larger than L2: 307 MB streamed by K1 per step vs 126 MB L2",
                 "residual": f"steady state: {args.precondition} untimed preconditioning steps before warmup",
                 "dense_fallback_in_timed_steps": timed_fallback,

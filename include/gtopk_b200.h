@@ -178,7 +178,8 @@ int gtk_select_update_deferred(const float* res_in, const float* grad, float* re
  * res = NULL (w updated, the residual untouched).  The previous winners are
  * corrected by membership of the previous global list: prev_tags = the
  * exchange plan's uint32[m] tags, d_epoch = its epoch counter (the previous
- * exchange's epoch when this call's finish runs).  Settle the last step with
+ * exchange's epoch when this call's finish runs).  peer_slot0 = NULL: no
+ * push (a rank whose schedule receives first).  Settle the last step with
  * gtk_select_settle_global. */
 int gtk_select_push_deferred(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
                              int32_t* sel_idx, float* sel_val, int32_t* d_count, uint32_t* d_status, void* ws,

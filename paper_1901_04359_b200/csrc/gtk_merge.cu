@@ -75,6 +75,7 @@ bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out, bool compact)
   if (lim <= 0) return false;
   const uint64_t slots = 2ull * (uint64_t)(cap < 1 ? 1 : cap);
   const int force_g = env_int("GTK_MERGE_GRID", 0), force_c = env_int("GTK_MERGE_CLUSTER", -1);
+  if (env_int("GTK_MERGE_COMPACT", 1) == 0) compact = false;
   auto cap_for = [&](int g) {
     const uint64_t per = (slots + g - 1) / g;
     uint32_t sc = kMergeSliceCap;

@@ -1332,7 +1332,8 @@ extern "C" int gtk_select_push_deferred(const float* res_in, const float* grad, 
                                         void* ws, size_t ws_bytes, uint32_t* d_window, const int32_t* prev_sel_idx,
                                         const int32_t* prev_count, const void* prev_ws, const uint32_t* prev_tags,
                                         void* peer_slot0, const uint64_t* d_epoch, void* stream) {
-  if (!res_in || !peer_slot0 || !d_epoch || (prev_sel_idx && !prev_tags)) return GTK_EINVAL;
+  // peer_slot0 = NULL: this rank receives first (tree schedule root): no push
+  if (!res_in || !d_epoch || (prev_sel_idx && !prev_tags)) return GTK_EINVAL;
   return select_impl(res_in, grad, res_out, m, k, sel_idx, sel_val, d_count, d_status, ws, ws_bytes, 0, d_window,
                      FusedUpdate{nullptr, 0.0f, 1.0f, 0}, stream, PeerPush{(uint64_t*)peer_slot0, d_epoch},
                      Deferred{true, prev_sel_idx, prev_count, prev_sel_idx ? prev_ws : nullptr, prev_tags, d_epoch});

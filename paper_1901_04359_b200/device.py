@@ -257,7 +257,7 @@ def select_update_deferred(res_in, grad: torch.Tensor, res_out: torch.Tensor, k:
 
 def select_push_deferred(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: int, out: DeviceList,
                          status: torch.Tensor, window: torch.Tensor, ws: torch.Tensor, prev: DeviceList | None,
-                         prev_ws: torch.Tensor | None, tags: torch.Tensor, peer_slot0: int,
+                         prev_ws: torch.Tensor | None, tags: torch.Tensor, peer_slot0: int | None,
                          epoch: torch.Tensor) -> None:
     """K1 for the deferred P > 1 step (gtk_select_push_deferred): winners stay
     pending in res_out, the selection goes to the exchange's first partner,
@@ -268,7 +268,7 @@ def select_push_deferred(res_in, grad: torch.Tensor, res_out: torch.Tensor, k: i
         "gtk_select_push_deferred", P(res_in), P(grad), P(res_out), m, k, P(out.idx), P(out.val), P(out.count),
         P(status), P(ws), ctypes.c_size_t(ws.numel()), P(window),
         P(prev.idx) if prev is not None else None, P(prev.count) if prev is not None else None,
-        P(prev_ws) if prev is not None else None, P(tags), ctypes.c_void_p(peer_slot0), P(epoch),
+        P(prev_ws) if prev is not None else None, P(tags), ctypes.c_void_p(peer_slot0 or 0), P(epoch),
         stream_of(grad.device),
     )
 

@@ -84,7 +84,7 @@ class GTopKPipeline:
         self.chained = False  # steps leave their winners pending (settled by sync_state)
         self.deferred = False
         self._dsteps = 0  # deferred steps enqueued (the first has no previous selection)
-        if self.mode == "defer" and (self.P == 1 or self.plan.push_slot0 is not None):
+        if self.mode == "defer":
             self.dsel = [DeviceList(self.m, self.k, self.dev) for _ in range(2)]
             self.dws = [_dev.select_workspace(self.m, self.k, self.dev, slot=1 + i) for i in range(2)]
             # the next main pass starts before this finish has written the next
@@ -119,12 +119,12 @@ class GTopKPipeline:
                                self.state._w, self.lr, 1, self.scaling, chain=chain)
             self.chained = chain
             return
-        if (self.P > 1 and self.mode == "defer" and _dev.sparse_update_fusable(self.lr, self.mom)
-                and self.plan.push_slot0 is not None):
+        if self.P > 1 and self.mode == "defer" and _dev.sparse_update_fusable(self.lr, self.mom):
             # deferred P > 1 step: the selection goes to the first partner as
-            # it is written, the exchange updates w only (res = None) and lets
-            # the next step's HBM pass run beside it; the next finish settles
-            # this step's winners by membership of the global list
+            # it is written (unless this rank receives first), the exchange
+            # updates w only (res = None) and lets the next step's HBM pass
+            # run beside it; the next finish settles this step's winners by
+            # membership of the global list
             plan = self.plan
             if plan.tags is None or plan.tags.numel() < self.m:
                 plan.tags = torch.zeros(self.m, dtype=torch.int32, device=self.dev)
@@ -140,7 +140,8 @@ class GTopKPipeline:
                 del self.dsel, self.dws, self.dwin
                 return self._enqueue(parity)
             self.group.enqueue_exchange(plan, self.dsel[parity], self.status,
-                                        update=(self.state._w, None, self.lr, self.scaling), prepushed=True)
+                                        update=(self.state._w, None, self.lr, self.scaling),
+                                        prepushed=plan.push_slot0 is not None)
             self._dsteps += 1
             self.deferred = True
             return
