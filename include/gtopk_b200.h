@@ -316,8 +316,8 @@ int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedule, int32_t
  *   res = NULL: the deferred step (gtk_select_push_deferred) -- no residual
  *   restore (the local winners stay pending for the next select's settle),
  *   the next kernel in the stream may launch at once (it is the next step's
- *   HBM pass), and the merges run on one cluster of <= 16 SMs when the union
- *   fits their shared memory, leaving the rest of the GPU to that pass. */
+ *   HBM pass), and the merges run on 32 blocks per merge round when the
+ *   union fits their shared memory, leaving the rest of the GPU to that pass. */
 int gtk_gtopk_exchange_update(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
                               void* const* peer_inbox, uint64_t* d_epoch,
                               int32_t* acc_idx, float* acc_val, int32_t* d_acc_n, int32_t k,

@@ -68,19 +68,25 @@ bool ensure_dyn_smem(const void* func, size_t bytes) {
   return true;
 }
 
-int coop_launch(const void* func, int grid, int threads, void** args, size_t smem, cudaStream_t st, bool pdl) {
+int coop_launch(const void* func, int grid, int threads, void** args, size_t smem, cudaStream_t st, bool pdl,
+                bool cooperative) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  int na = 0;
+  if (cooperative) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na++].val.cooperative = 1;
+  }
+  if (pdl && pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = (pdl && pdl_enabled()) ? 2 : 1;
+  cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelExC(&cfg, func, args);
   if (e != cudaSuccess) {
     set_last_cuda_error(e);

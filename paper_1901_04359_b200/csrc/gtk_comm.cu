@@ -29,6 +29,7 @@
 // overwritten while read, and a stale record carries another call's tag.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -476,9 +477,13 @@ static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32
                       nullptr, (MergeCtl*)(base + L.ctl), (EngineWS*)(base + L.engine),
                       (int32_t*)(base + L.u_idx), (float*)(base + L.u_val)};
   MergeGrid g;
-  // deferred (no residual): the exchange runs beside the next step's HBM pass,
-  // so it stays on at most one cluster of SMs when the union fits there
-  if (!merge_grid_for((const void*)exchange_kernel, k, &g, upd_w && !upd_res)) return GTK_ECUDA;
+  // deferred (no residual): the exchange runs beside the next step's HBM pass
+  // on 32 blocks per merge round (measured best: N = 2 32 blocks 78.1 us/step,
+  // 24: 83.3, 40: 79.8; N = 4 64 blocks 95.0, 48: 99.3, 80: 101.9, 100: 112.3)
+  int merges = 0;
+  for (int s = 0; s < nsteps; ++s) merges += schedule[4 * s + 2] ? 1 : 0;
+  const int compact_g = (upd_w && !upd_res) ? 32 * std::max(1, merges) : 0;
+  if (!merge_grid_for((const void*)exchange_kernel, k, &g, compact_g)) return GTK_ECUDA;
   a.merge.slice_cap = g.slice_cap;
   void* args[] = {&a};
   ProfScope prof(kProfExchange, (cudaStream_t)stream);

@@ -16,7 +16,7 @@ int coop_grid(const void* func, int threads, size_t smem);
 // pdl: programmatic dependent launch on the previous kernel of the stream
 // (the kernel must griddepcontrol.wait before consuming its outputs)
 int coop_launch(const void* func, int grid, int threads, void** args, size_t smem, cudaStream_t st,
-                bool pdl = false);
+                bool pdl = false, bool cooperative = true);
 // opt a kernel into > 48 KB of dynamic shared memory (once per device); false on error
 bool ensure_dyn_smem(const void* func, size_t bytes);
 // grid of a ⊤-merge kernel (merge_kernel / exchange_kernel) over lists of
@@ -28,10 +28,16 @@ struct MergeGrid {
   int G;
   uint32_t slice_cap;
   bool cluster;
+  // false: a plain launch (with PDL) instead of a cooperative one (the
+  // deferred exchange, GTK_MERGE_COMPACT_COOP=0: its few blocks are all
+  // resident before the next kernel can start, which launches only once every
+  // block has released it).  Measured equal: the next HBM pass then starts
+  // before the finish ends but loses the time to the SMs it shares
+  bool coop = true;
 };
-// compact: one cluster of up to 16 CTAs whenever the union fits their shared
-// memory (a merge that shares the GPU with an HBM pass)
-bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out, bool compact = false);
+// compact_g > 0: at most compact_g blocks whenever the union fits their
+// shared memory (a merge that shares the GPU with an HBM pass)
+bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out, int compact_g = 0);
 // launch a merge-type kernel on its MergeGrid (cluster or cooperative)
 int merge_launch(const void* func, const MergeGrid& g, void** args, size_t smem, cudaStream_t st, bool pdl);
 

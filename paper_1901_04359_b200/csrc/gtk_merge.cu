@@ -69,19 +69,45 @@ static bool cluster_fits(const void* func, int cs, size_t smem) {
   return ok;
 }
 
-bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out, bool compact) {
+bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out, int compact_g) {
   if (!ensure_dyn_smem(func, merge_smem_bytes(kMergeSliceCapMax))) return false;
   const int lim = num_sms();
   if (lim <= 0) return false;
   const uint64_t slots = 2ull * (uint64_t)(cap < 1 ? 1 : cap);
   const int force_g = env_int("GTK_MERGE_GRID", 0), force_c = env_int("GTK_MERGE_CLUSTER", -1);
-  if (env_int("GTK_MERGE_COMPACT", 1) == 0) compact = false;
+  if (env_int("GTK_MERGE_COMPACT", 1) == 0) compact_g = 0;
   auto cap_for = [&](int g) {
     const uint64_t per = (slots + g - 1) / g;
     uint32_t sc = kMergeSliceCap;
     if (per > sc) sc = (uint32_t)std::min<uint64_t>((per + 255) & ~255ull, kMergeSliceCapMax);
     return sc;
   };
+  if (compact_g > 0) {
+    // a merge sharing the GPU with an HBM pass: at most compact_g blocks of a
+    // cooperative grid (schedulable on whichever SMs are free -- a cluster
+    // needs a whole GPC free, which the running finish blocks deny: measured
+    // N = 2 16-CTA cluster 86.4 us/step vs 32-block grid 78.1).
+    // GTK_MERGE_COMPACT_G / GTK_MERGE_COMPACT_CLUSTER override (A/B)
+    const int cg = std::max(1, std::min(env_int("GTK_MERGE_COMPACT_G", compact_g), lim));
+    const bool as_cluster = env_int("GTK_MERGE_COMPACT_CLUSTER", 0) != 0 && cg <= kMergeMaxCluster;
+    const uint64_t want_c0 = slots <= (uint64_t)kMergeSoloSlots ? 1 : (slots + kMergeClusterSlots - 1) / kMergeClusterSlots;
+    const int g = (int)std::min<uint64_t>(want_c0, (uint64_t)cg);
+    if ((slots + g - 1) / g <= (uint64_t)kMergeSliceCapMax) {
+      const uint32_t sc = cap_for(g);
+      if (g == 1) {
+        *out = MergeGrid{1, sc, false};
+        return true;
+      }
+      if (as_cluster && cluster_fits(func, g, merge_smem_bytes(sc))) {
+        *out = MergeGrid{g, sc, true};
+        return true;
+      }
+      if (!as_cluster && coop_grid(func, kMergeThreads, merge_smem_bytes(sc)) >= g) {
+        *out = MergeGrid{g, sc, false, env_int("GTK_MERGE_COMPACT_COOP", 1) != 0};
+        return true;
+      }
+    }
+  }
   // cluster candidate
   const uint64_t want_c = slots <= (uint64_t)kMergeSoloSlots ? 1 : (slots + kMergeClusterSlots - 1) / kMergeClusterSlots;
   int gc = (int)std::min<uint64_t>(want_c, kMergeMaxCluster);
@@ -90,8 +116,7 @@ bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out, bool compact)
   const bool c_smem = (slots + gc - 1) / gc <= (uint64_t)kMergeSliceCapMax;
   // cluster mode only where the union spreads over <= 16 CTAs at the target density
   bool use_cluster = force_c != 0 && c_smem && (force_g > 0 ? force_g <= kMergeMaxCluster
-                                                             : (force_c == 1 || compact ||
-                                                                want_c <= (uint64_t)kMergeMaxCluster));
+                                                             : (force_c == 1 || want_c <= (uint64_t)kMergeMaxCluster));
   if (force_c == 1 && !c_smem) return false;
   if (use_cluster) {
     const uint32_t sc = cap_for(gc);
@@ -113,7 +138,7 @@ bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out, bool compact)
 }
 
 int merge_launch(const void* func, const MergeGrid& g, void** args, size_t smem, cudaStream_t st, bool pdl) {
-  if (!g.cluster) return coop_launch(func, g.G, kMergeThreads, args, smem, st, pdl);
+  if (!g.cluster) return coop_launch(func, g.G, kMergeThreads, args, smem, st, pdl, g.coop);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(g.G);
   cfg.blockDim = dim3(kMergeThreads);

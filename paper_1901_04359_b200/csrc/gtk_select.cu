@@ -46,7 +46,10 @@ constexpr int kSampleThreads = 1024;
 constexpr int kSampleChunk = kSampleThreads;                // 1024 elements per chunk (one per thread)
 constexpr int kSampleTop = 32;                               // top keys kept per sample block
 constexpr int kSampleMaxChunks = 1024;                       // sample blocks (window holds 32K keys)
-constexpr int kFinishThreads = 512;
+#ifndef GTK_FINISH_THREADS
+#define GTK_FINISH_THREADS 512
+#endif
+constexpr int kFinishThreads = GTK_FINISH_THREADS;
 constexpr int kSliceCap = 3072;                              // candidates staged per finish block (minimum)
 constexpr int kSliceCapMax = 20480;                          // ... up to 160 KB of dynamic smem at large k
 constexpr size_t kFinishDynSmemMax = 192 * 1024;             // slice + (deferred) fix list
