@@ -129,9 +129,31 @@ __global__ void scatter_add_kernel(const int32_t* idx, const float* val, const i
   }
 }
 
-__global__ void divide_kernel(float* out, uint32_t m, float Pf) {
-  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x)
-    out[e] = __fdiv_rn(out[e], Pf);
+// out /= P at the touched entries only (untouched ones are +0 and +0 / P is
+// +0): entry e of rank r divides unless an earlier rank's (ascending) list
+// holds the same index -- each index exactly once, like the reference's dense
+// division (collectives.py:164), at P x k instead of m elements
+__global__ void divide_touched_kernel(const int32_t* idx, const int32_t* d_n, int32_t P, int64_t stride, float* out,
+                                      float Pf) {
+  const uint64_t tot = (uint64_t)P * (uint64_t)stride;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < tot; q += (uint64_t)gridDim.x * blockDim.x) {
+    const int32_t r = (int32_t)(q / (uint64_t)stride);
+    const uint32_t e = (uint32_t)(q % (uint64_t)stride);
+    if (e >= (uint32_t)__ldg(d_n + r)) continue;
+    const int32_t i = __ldg(idx + (uint64_t)r * stride + e);
+    bool first = true;
+    for (int32_t s = 0; s < r && first; ++s) {
+      const int32_t* a = idx + (uint64_t)s * stride;
+      uint32_t lo = 0, hi = (uint32_t)__ldg(d_n + s);
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) < i) lo = mid + 1;
+        else hi = mid;
+      }
+      first = !(lo < (uint32_t)__ldg(d_n + s) && __ldg(a + lo) == i);
+    }
+    if (first) out[i] = __fdiv_rn(out[i], Pf);
+  }
 }
 
 __global__ void dense_sum_kernel(const float* const* srcs, int P, uint32_t m, float* out) {
@@ -220,7 +242,7 @@ extern "C" int gtk_topk_accumulate(const int32_t* idx, const float* val, const i
     GTK_CHECK_LAUNCH();
   }
   if (divide) {
-    divide_kernel<<<grid_for(m, 256), 256, 0, st>>>(out, (uint32_t)m, (float)P);
+    divide_touched_kernel<<<num_sms() * 2, 256, 0, st>>>(idx, d_n, P, stride, out, (float)P);
     GTK_CHECK_LAUNCH();
   }
   return GTK_OK;

@@ -208,21 +208,22 @@ class DistDeviceGroup:
 
     # -- TopKAllReduce baseline: NCCL allgather + rank-order accumulation -----
     def topk(self, ep: Endpoint, lst: DeviceList, divide: bool = True) -> torch.Tensor:
+        """collectives.py:148-165: every rank's list (counts, then one packed
+        all-gather of [idx | value bits] per rank), accumulated in rank order
+        by gtk_topk_accumulate (scatter per rank, division at the touched
+        entries only)."""
         W = self.world
         cnts = torch.empty(W, dtype=torch.int32, device=self.device)
         dist.all_gather_into_tensor(cnts, lst.n)
-        cap = max(int(cnts.max().item()), 1)
-        idx = torch.zeros(W * cap, dtype=torch.int32, device=self.device)
-        val = torch.zeros(W * cap, dtype=torch.float32, device=self.device)
-        mi = torch.zeros(cap, dtype=torch.int32, device=self.device)
-        mv = torch.zeros(cap, dtype=torch.float32, device=self.device)
+        cap = max(int(cnts.max().item()), 1)  # (the gather's size: one host read)
         n = min(cap, lst.cap)
-        mi[:n].copy_(lst.idx[:n])
-        mv[:n].copy_(lst.val[:n])
-        dist.all_gather_into_tensor(idx, mi)
-        dist.all_gather_into_tensor(val, mv)
+        mine = torch.empty(2 * cap, dtype=torch.int32, device=self.device)
+        mine[:n].copy_(lst.idx[:n])
+        mine[cap:cap + n].copy_(lst.val[:n].view(torch.int32))
+        allv = torch.empty(W * 2 * cap, dtype=torch.int32, device=self.device)
+        dist.all_gather_into_tensor(allv, mine)
         out = torch.empty(lst.dim, dtype=torch.float32, device=self.device)
-        _dev.topk_accumulate(idx, val, cnts, W, cap, lst.dim, out, divide=divide)
+        _dev.topk_accumulate(allv, allv[cap:].view(torch.float32), cnts, W, 2 * cap, lst.dim, out, divide=divide)
         for s in range(W - 1):
             ep.stats.add_sparse(cnts[(self.rank - s) % W:(self.rank - s) % W + 1], sent=True)
             ep.stats.add_sparse(cnts[(self.rank - s - 1) % W:(self.rank - s - 1) % W + 1], sent=False)

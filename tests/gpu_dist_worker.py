@@ -20,7 +20,8 @@ from paper_1901_04359_b200 import collectives as coll  # noqa: E402
 from paper_1901_04359_b200 import optimizer as opt  # noqa: E402
 from paper_1901_04359_b200.dist import init_dist_cluster  # noqa: E402
 from paper_1901_04359_b200.pipeline import GTopKPipeline  # noqa: E402
-from paper_1901_04359_b200.sparse import SparseVector  # noqa: E402
+from paper_1901_04359_b200.device import DeviceList  # noqa: E402
+from paper_1901_04359_b200.sparse import DeviceSparseVector, SparseVector  # noqa: E402
 from paper_1901_04359_b200.transport import TransportError  # noqa: E402
 
 F32 = np.float32
@@ -74,6 +75,19 @@ def main():
     res = coll.gtopk_allreduce(ep, SparseVector(m, *lists[r]), k, P)
     check(np.array_equal(res.global_topk.indices, want_i), "large-k idx")
     check(np.array_equal(bits(res.global_topk.values), bits(want_v)), "large-k val")
+
+    # 1b. the TopK-AllReduce baseline (NCCL count + packed all-gather, rank-order
+    #     accumulation, division at the touched entries) bitwise vs the
+    #     reference's dense accumulation (collectives.py:148-165), device lists
+    for trial in range(4):
+        m = int(rng.integers(1000, 200_000))
+        k = int(rng.integers(1, min(2000, m // 4) + 2))
+        lists = [orc.top_k_select((rng.integers(-3, 4, m) if trial % 2 else rng.standard_normal(m)).astype(F32),
+                                  k)[:2] for _ in range(P)]
+        want = orc.topk_allreduce(lists, m, P)
+        dl = DeviceList.from_host(m, *lists[r], ep.group.device, k)
+        got = coll.topk_allreduce(ep, DeviceSparseVector(dl), P).cpu().numpy()
+        check(np.array_equal(bits(got), bits(want)), f"topk_allreduce trial {trial}")
 
     # 2. full gtopk_step trajectories vs the oracle (m=270K ResNet-20 size)
     m, k, steps = 270_000, 270, 4
