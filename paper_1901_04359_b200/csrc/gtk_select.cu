@@ -1030,9 +1030,13 @@ __global__ void __launch_bounds__(kFinishThreads, GTK_FINISH_MIN_BLOCKS) select_
     }
     return;
   }
+  // the fused update skips on an error an EARLIER step left in the (sticky)
+  // status word of a pipeline, like the exchange's K3: the weights keep the
+  // last good step
+  float* const upd_w = (a.upd_w && !(__ldcg(a.d_status) & GTK_DEV_ERROR_MASK)) ? a.upd_w : nullptr;
   Sink out{a.sel_idx, a.sel_val, a.d_count, (a.chain || a.defer) ? nullptr : a.res_out, true,
            a.trace ? a.trace + 3 : nullptr,
-           a.window, wlevel, wtau, wtau2, 1u, a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling};
+           a.window, wlevel, wtau, wtau2, 1u, upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling};
   if (a.chain) out.pend_rec = a.window;
   if (a.ofs_out) {  // written by the candidate path's gather finish only (same tile partition next call)
     if (blk == 0 && threadIdx.x == 0) a.ofs_out[0] = 0u;

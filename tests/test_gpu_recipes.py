@@ -147,3 +147,35 @@ def test_graph_pipeline_steady_state_trajectory(mode, steps, monkeypatch):
     pipe.sync_state()  # the state's own residual, settled in place
     assert st._res is pipe.res[t % 2]
     assert np.array_equal(bits(st.residual.cpu().numpy()), bits(ref.residual))
+
+
+@pytest.mark.parametrize("mode", ["defer", "chain", "plain"])
+def test_pipeline_poison_keeps_last_good_weights(mode, monkeypatch):
+    """A non-finite gradient in a P = 1 graph pipeline: the failing step and
+    every later one leave the weights alone (the status word is sticky), and
+    check() raises the reference's FloatingPointError."""
+    import torch
+
+    import paper_1901_04359_b200 as gtopk
+    from oracle import gtopk_oracle as orc
+    from paper_1901_04359_b200.pipeline import GTopKPipeline
+
+    monkeypatch.setenv("GTK_PIPE_MODE", mode)
+    m, k, lr = 100_003, 100, 0.05
+    rng = np.random.default_rng(8)
+    good = rng.standard_normal(m).astype(F32)
+    bad = good.copy()
+    bad[4242] = np.nan
+    ep = gtopk.create_local_cluster(1)[0]
+    st = gtopk.make_state(torch.zeros(m, device="cuda"), lr=lr)
+    pipe = GTopKPipeline(ep, st, k, [torch.from_numpy(good).cuda(), torch.from_numpy(bad).cuda()],
+                         use_graph=False)
+    ref = orc.State(np.zeros(m, F32), lr)
+    pipe.step_eager()  # step 0: good
+    orc.gtopk_step_all([ref], [good], k)
+    for _ in range(4):  # step 1 poisoned, steps 2.. run behind it
+        pipe.step_eager()
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(st._w.cpu().numpy()), bits(ref.weights)), mode
+    with pytest.raises(FloatingPointError):
+        pipe.check()
