@@ -77,6 +77,7 @@ struct ExchangeArgs {
 
 __host__ __device__ inline size_t slot_bytes(int32_t k) { return ll_slot_bytes(k); }
 __device__ __forceinline__ uint64_t* slot_of(char* inbox, int s, uint32_t par, int32_t k) {
+  GTK_DCHECK(s >= 0 && s < kMaxSteps && par < 2u);
   return reinterpret_cast<uint64_t*>(inbox + ((size_t)s * 2 + par) * slot_bytes(k));
 }
 
@@ -291,6 +292,7 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
 #pragma unroll
         for (int u = 0; u < kK3Batch; ++u) {
           const uint32_t e = base + u * stride;
+          GTK_DCHECK(e >= gn || gi[u] >= 0);
           if (e < gn) wv[u] = a.upd_w[gi[u]];
           if (e < ln) {
             tg[u] = __ldcg(a.upd_tags + li[u]);

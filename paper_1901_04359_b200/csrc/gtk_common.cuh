@@ -12,6 +12,25 @@
 
 #include "../../include/gtopk_b200.h"
 
+// GTK_CHECKED builds (tools/checked_build.sh): every shared / global index
+// the kernels compute is asserted in range -- the bounds checks this GPU pool
+// offers in place of compute-sanitizer (a failed check prints and traps)
+#ifdef GTK_CHECKED
+#include <cstdio>
+#define GTK_DCHECK(cond)                                                                              \
+  do {                                                                                                \
+    if (!(cond)) {                                                                                    \
+      printf("GTK_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__,     \
+             (int)blockIdx.x, (int)threadIdx.x);                                                     \
+      __trap();                                                                                       \
+    }                                                                                                 \
+  } while (0)
+#else
+#define GTK_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace gtk {
 
 constexpr uint32_t kKeyMask = 0x7FFFFFFFu;

@@ -181,6 +181,7 @@ __device__ __forceinline__ void sink_count(const Sink& out, uint32_t n, uint32_t
 
 // one kept entry to the output list (+ the select's side effects)
 __device__ __forceinline__ void sink_put(const Sink& out, uint32_t p, int32_t i, float v) {
+  GTK_DCHECK(i >= 0);
   out.o_idx[p] = i;
   out.o_val[p] = v;
   if (out.zero_at) out.zero_at[i] = 0.0f;
@@ -227,6 +228,7 @@ __device__ void engine_hist(const Src& src, uint32_t s0, uint32_t s1, uint32_t l
     float v;
     if (src.get(s, key, i, v) && key >= lo && (uint64_t)key < hi) {
       const uint32_t bin = min((uint32_t)kBins, (key - lo) >> shift);
+      GTK_DCHECK(bin < (uint32_t)kHistLen);
       atomicAdd(&sm.hist[bin], 1u);
     }
   }
@@ -311,6 +313,7 @@ __device__ __forceinline__ void sink_put_batch(const Sink& out, const uint32_t (
     if (j >= n) break;
     const int32_t i = bi[j];
     const float v = bv[j];
+    GTK_DCHECK(i >= 0);
     out.o_idx[bp[j]] = i;
     out.o_val[bp[j]] = v;
     if (out.zero_at) out.zero_at[i] = 0.0f;
@@ -341,6 +344,7 @@ __device__ void engine_write(const Src& src, uint32_t s0, uint32_t s1, uint32_t 
       float v;
       const bool kept = s < s1 && src.get(s, key, i, v) && keep_fn(key, i, s - s0);
       const unsigned bal = __ballot_sync(kFull, kept);
+      GTK_DCHECK(r * NW + w < (uint32_t)NT);
       if (lane == 0) {
         sm.wcnt[r * NW + w] = __popc(bal);
         sm.wbal[r * NW + w] = bal;
@@ -416,6 +420,7 @@ __device__ void engine_gather_finish(const Src& src, uint32_t s0, uint32_t s1, u
     p0 = __shfl_sync(kFull, p0, __ffs(bal) - 1);
     if (inb) {
       const uint32_t p = p0 + __popc(bal & lanemask_lt());
+      GTK_DCHECK(p < (uint32_t)kGatherCap);
       if (p >= (uint32_t)kGatherCap) continue;  // (cannot happen: in_bin <= kGatherCap)
       if (solo) {
         sm.keys[p] = key;
@@ -431,6 +436,7 @@ __device__ void engine_gather_finish(const Src& src, uint32_t s0, uint32_t s1, u
   n_above = block_sum<NT>(n_above, sm.scan);
   uint32_t above_before = 0;
   if (!solo) {
+    GTK_DCHECK(blk < (unsigned)kMaxBlocks);
     if (threadIdx.x == 0) ws->cta_a[blk] = n_above;
     grid_sync(&ws->bar, G);
     // one round trip: the count, the (at most kGatherMax) gathered entries

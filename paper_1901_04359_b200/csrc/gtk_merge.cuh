@@ -265,6 +265,7 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
     for (uint32_t j = warp_id(); j <= jn; j += kMergeThreads / 32) {
       const uint32_t d = min(d1, d0 + (j0 + j) * kMergeSub);
       const uint32_t i = merge_path_warp(a, na, a.b_idx, nb, d);
+      GTK_DCHECK(j < (uint32_t)kMergeMaxSplits);
       if (lane_id() == 0) S.split[j] = i;
     }
     __syncthreads();
@@ -286,6 +287,7 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
       const int32_t nextB = jb < nb ? __ldcg(a.b_idx + jb) : -1;
       const float nextBv = jb < nb ? __ldcg(a.b_val + jb) : 0.0f;
       // stage A[ia, ib) and B[ja, jb): every load of the sub-chunk in flight at once
+      GTK_DCHECK(la <= (uint32_t)kMergeSub && lb <= (uint32_t)kMergeSub);
       for (uint32_t base = 0; base < la + lb; base += 4 * kMergeThreads) {
         int32_t ri[4];
         float rv[4];
@@ -326,6 +328,7 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
         }
         const uint32_t slot = sub + t + r;
         const bool valid = v != 0.0f;
+        GTK_DCHECK(slot >= d0 && slot < d1 && (!in_smem || slot - d0 < a.slice_cap));
         if (in_smem) {
           slice_idx[slot - d0] = valid ? x : -1;
           slice_val[slot - d0] = v;
@@ -346,6 +349,7 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
         const float v = S.sBv[t];
         const uint32_t slot = sub + t + r;
         const bool valid = !dup && v != 0.0f;
+        GTK_DCHECK(slot >= d0 && slot < d1 && (!in_smem || slot - d0 < a.slice_cap));
         if (in_smem) {
           slice_idx[slot - d0] = valid ? x : -1;
           slice_val[slot - d0] = v;

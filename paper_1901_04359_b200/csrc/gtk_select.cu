@@ -564,6 +564,7 @@ __device__ __forceinline__ bool main_tile(const MainArgs& a, uint32_t tile, cons
     if (didx) {
       const uint32_t bq = q == 0 ? base[0] : q == 1 ? base[1] : q == 2 ? base[2] : base[3];
       const uint32_t pos = bq + __popc(flags & ((1u << b) - 1u) & (0xFu << (4 * q)));
+      GTK_DCHECK(pos < total && (dense || pos < a.slots));
       didx[pos] = (int32_t)(tbase + ((uint64_t)q * kMainThreads + threadIdx.x) * 4 + j);
       dval[pos] = x;
     }
@@ -881,6 +882,7 @@ __device__ uint32_t deferred_fixup(const FinishArgs& a, EngineSmem<kFinishThread
     const bool keep = was || now;
     uint32_t tot;
     const uint32_t pos = n_fix + block_excl_scan<kFinishThreads>(keep ? 1u : 0u, sm.scan, &tot);
+    GTK_DCHECK(!has || (e >= 0 && (uint32_t)e < a.m));
     if (keep && pos < a.fix_cap) {
       f_idx[pos] = e;
       f_val[pos] = A;
@@ -955,6 +957,7 @@ __device__ void apply_fixes(int32_t* s_idx, float* s_val, uint32_t own_raw, cons
       np = p + lo_;
     }
     __syncthreads();
+    GTK_DCHECK(p >= own_raw || np < own_raw + n_ins);
     if (p < own_raw) {
       s_idx[np] = xi;
       s_val[np] = xv;
@@ -964,6 +967,7 @@ __device__ void apply_fixes(int32_t* s_idx, float* s_val, uint32_t own_raw, cons
   for (uint32_t q = threadIdx.x; q < n_ins; q += kFinishThreads) {
     const uint32_t f = ins[q];
     const uint32_t np = (f_flag[f] >> 2) + q;
+    GTK_DCHECK(np < own_raw + n_ins);
     s_idx[np] = f_idx[f];
     s_val[np] = f_val[f];
   }
@@ -1152,6 +1156,7 @@ __global__ void __launch_bounds__(kFinishThreads, GTK_FINISH_MIN_BLOCKS) select_
         const uint32_t inf = s_cnt[lo];
         if (inf & kOvfBit) continue;  // dense tiles are copied below
         const size_t src = (size_t)(tb + lo) * a.slots + (jj - s_dst[lo]);
+        GTK_DCHECK(jj - s_dst[lo] < a.slots && (!in_smem || jj < a.slice_cap));
         if (in_smem) {  // async: lands while the k-th key's bin is found
           cp_async4(di + jj, a.slot_idx + src);
           cp_async4(dv + jj, a.slot_val + src);
@@ -1533,7 +1538,11 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
 
 
   void* args[] = {&fa};
-  return coop_launch((const void*)select_finish_kernel, G, kFinishThreads, args, fin_smem, st, true);
+  // GTK_FINISH_COOP=0: a plain (PDL) launch -- the finish's G <= #SMs blocks
+  // are all resident once the main pass ahead of it has drained (A/B)
+  const char* fc = getenv("GTK_FINISH_COOP");
+  const bool coop = !(fc && *fc == '0');
+  return coop_launch((const void*)select_finish_kernel, G, kFinishThreads, args, fin_smem, st, true, coop);
 }
 
 extern "C" int gtk_select_main_pass(const float* res_in, const float* grad, float* res_out, int64_t m, int32_t k,
