@@ -222,6 +222,9 @@ __device__ __forceinline__ uint64_t atom_add_acq_rel_gpu_u64(uint64_t* p, uint64
   asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ void red_add_release_gpu_u64(uint64_t* p, uint64_t v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ uint64_t ld_acquire_gpu_u64(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -262,7 +265,9 @@ __device__ __forceinline__ void grid_sync(GridBarrier* b, unsigned nblocks) {
     const uint64_t old = atom_add_acq_rel_gpu_u64(word, 1ull);
     const uint32_t g = (uint32_t)(old >> 32);
     if ((uint32_t)old == nblocks - 1) {
-      atom_add_acq_rel_gpu_u64(word, (1ull << 32) - nblocks);  // count -> 0, gen -> g + 1
+      // count -> 0, gen -> g + 1: a non-returning release add -- the last
+      // arriver (the block everyone waits for) does not wait for its round trip
+      red_add_release_gpu_u64(word, (1ull << 32) - nblocks);
     } else {
       uint32_t spins = 0;
       while ((uint32_t)(ld_acquire_gpu_u64(word) >> 32) == g)

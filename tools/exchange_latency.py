@@ -25,7 +25,7 @@ import torch  # noqa: E402
 import test_gpu_exchange_loopback as lbt  # noqa: E402
 
 
-def run(P, mode, k, calls, rank=0):
+def run(P, mode, k, calls, rank=0, deferred=False):
     rng = np.random.default_rng(11 + k)
     m = max(1_000_000, 20 * k)
     lists = lbt._lists(rng, P, m, k, "normal")
@@ -67,7 +67,8 @@ def run(P, mode, k, calls, rank=0):
         # spin, with the exchange launch already queued behind it
         torch.cuda._sleep(400_000)
         e0.record()
-        rc = lb.lib.gtk_gtopk_exchange_update(*args, P_(w), P_(res), ctypes.c_float(0.01), 0, P_(lb.tags), st)
+        rc = lb.lib.gtk_gtopk_exchange_update(*args, P_(w), P_(None if deferred else res), ctypes.c_float(0.01), 0,
+                                              P_(lb.tags), st)
         e1.record()
         torch.cuda.synchronize()
         assert rc == 0, rc
@@ -101,10 +102,13 @@ def main():
     ap.add_argument("--k", type=int, nargs="+", default=[270, 25600])
     ap.add_argument("--P", type=int, nargs="+", default=[2, 4])
     ap.add_argument("--calls", type=int, default=30)
+    ap.add_argument("--deferred", action="store_true", help="res = NULL: the deferred step's exchange (compact grid)")
     a = ap.parse_args()
     for P in a.P:
         for k in a.k:
-            print(json.dumps(run(P, "butterfly", k, a.calls)), flush=True)
+            r = run(P, "butterfly", k, a.calls, deferred=a.deferred)
+            r["deferred"] = a.deferred
+            print(json.dumps(r), flush=True)
 
 
 if __name__ == "__main__":
