@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   const bool tr = a.trace && blk == 0 && threadIdx.x == 0;
   if (tr) a.trace[0] = (int64_t)globaltimer();
 
+  bool k3_fused = false;  // the final merge applied the w update (deferred steps)
   // the step whose receive writes the final global list into acc (K3's tags)
   int last_recv = -1;
   for (int s = 0; s < a.nsteps; ++s)
@@ -204,6 +205,17 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
         if (a.upd_w && s == last_recv) {  // the final global list: K3's membership tags
           m.tag = a.upd_tags;
           m.tag_val = tag;
+          if (!a.upd_res) {
+            // deferred step (no residual restore): the final merge's writer
+            // also updates w -- every LL record was read before the merge's
+            // first barrier, so the status word it checks is final
+            m.upd_w = a.upd_w;
+            m.upd_lr = a.upd_lr;
+            m.upd_Pf = (float)a.P;
+            m.upd_scaling = a.upd_scaling;
+            m.upd_skip = a.d_status;
+            k3_fused = true;
+          }
         }
         if (out_slot) {
           m.ll_body = out_slot + 2;
@@ -255,7 +267,7 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
       a.d_acc_n[1] = __ldcg(a.d_in_n + 1);
     }
   }
-  if (a.upd_w) {
+  if (a.upd_w && !k3_fused) {
     // K3 once the status is final (a failed step must leave the state
     // untouched on every rank): the global list updates w; local entries
     // whose membership tag (set by the final list's writer) is not this

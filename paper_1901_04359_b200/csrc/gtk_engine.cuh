@@ -159,7 +159,18 @@ struct Sink {
   uint32_t* pend_rec = nullptr;
   // deferred select: every block's first output position ([1 + blk]; [0] = G)
   uint32_t* blk_ofs = nullptr;
+  // the fused w update is skipped when this status word holds an error bit,
+  // read once per block after the engine's last barrier (nullable: always)
+  const uint32_t* upd_skip = nullptr;
 };
+
+// the sink a block writes with: upd_w dropped when the status word (final
+// behind the engine's last barrier) holds an error bit
+__device__ __forceinline__ Sink sink_for_write(const Sink& out) {
+  Sink o = out;
+  if (o.upd_w && o.upd_skip && (__ldcg(o.upd_skip) & GTK_DEV_ERROR_MASK)) o.upd_w = nullptr;
+  return o;
+}
 
 constexpr uint32_t kRecValid = 0x1u;    // window record word 0: lo/shift/k describe the next call's window
 constexpr uint32_t kRecPending = 0x2u;  // ... the residual still holds the last chained call's winners
@@ -553,7 +564,7 @@ __device__ void engine_gather_finish(const Src& src, uint32_t s0, uint32_t s1, u
     out.blk_ofs[1 + blk] = above_before + extra;
     if (blk == 0) out.blk_ofs[0] = G;
   }
-  engine_write<NT>(src, s0, s1, above_before + extra, keep_fn, sm, out);
+  engine_write<NT>(src, s0, s1, above_before + extra, keep_fn, sm, sink_for_write(out));
   sink_stamp(out, 3);
   if (blk == 0) {  // every block is past its last histogram read
     for (int rr = 0; rr < kRounds; ++rr)
@@ -603,7 +614,8 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       for (unsigned j = threadIdx.x; j < blk; j += NT) before += __ldcg(&ws->cta_a[j]);
       before = block_sum<NT>(before, sm.scan);
     }
-    engine_write<NT>(src, s0, s1, before, [](uint32_t, int32_t, uint32_t) { return true; }, sm, out);
+    engine_write<NT>(src, s0, s1, before, [](uint32_t, int32_t, uint32_t) { return true; }, sm,
+                     sink_for_write(out));
     if (blk == 0) {
       for (int r = 0; r < kRounds; ++r)
         for (int b = threadIdx.x; b < kHistLen; b += NT) ws->hist[r][b] = 0;
@@ -742,6 +754,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       }
       uint32_t out_pos = gt_before + min(eq_before, need);
       uint32_t eq_seen = eq_before;
+      const Sink wout = sink_for_write(out);
       for (uint32_t base = s0; base < s1; base += NT) {
         const uint32_t s = base + threadIdx.x;
         uint32_t key = 0;
@@ -756,7 +769,7 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
         if (is_eq && eq_seen + eq_rank + 1 == need && out.pend_rec) out.pend_rec[7] = (uint32_t)i;  // the last kept tie
         uint32_t k_tot;
         const uint32_t k_rank = block_excl_scan<NT>(keep ? 1u : 0u, sm.scan, &k_tot);
-        if (keep) sink_put(out, out_pos + k_rank, i, v);
+        if (keep) sink_put(wout, out_pos + k_rank, i, v);
         out_pos += k_tot;
         eq_seen += eq_tot;
       }

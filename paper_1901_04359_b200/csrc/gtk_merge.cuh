@@ -90,6 +90,7 @@ struct MergeArgs {
   uint32_t* tag;
   uint32_t tag_val;
   uint32_t slice_cap;  // slice slots staged in shared memory (behind MergeSmem)
+  const uint32_t* upd_skip = nullptr;  // the fused update skips on an error bit here (Sink::upd_skip)
   // exchange: A arrives as LL records in the inbox (a_ll[2i] = {idx, val bits}
   // tagged a_tag; a_idx / a_val unused), polled as they are read
   const uint64_t* a_ll = nullptr;
@@ -393,10 +394,11 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
   }
   merge_stamp(a, 3);  // after the histogram barrier
   const bool keep_all = n_valid <= a.k;
-  const Sink out{a.o_idx, a.o_val, a.d_no, nullptr, true, a.trace ? a.trace + 5 : nullptr,
-                 keep_all ? nullptr : rec, rec_level, rec_tau, rec_tau2, 3u,
-                 a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling, a.tag, a.tag_val,
-                 a.ll_body, a.ll_head, a.ll_tag};
+  Sink out{a.o_idx, a.o_val, a.d_no, nullptr, true, a.trace ? a.trace + 5 : nullptr,
+           keep_all ? nullptr : rec, rec_level, rec_tau, rec_tau2, 3u,
+           a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling, a.tag, a.tag_val,
+           a.ll_body, a.ll_head, a.ll_tag};
+  out.upd_skip = a.upd_skip;
   bool ok = engine_run<kMergeThreads>(src, d0, d1, keep_all ? n_valid : a.k, keep_all, win_lo, win_shift, esm.hist,
                                       true, a.ews, esm, out, G);
   merge_stamp(a, 4);  // engine done

@@ -333,9 +333,12 @@ def test_exchange_update_fused_k3(P, mode):
             assert np.all(tags[member] == tag) and not np.any(tags[~member] == tag)
 
 
-def test_exchange_poison_received_forwarded_and_k3_skipped():
+@pytest.mark.parametrize("deferred", [False, True])
+def test_exchange_poison_received_forwarded_and_k3_skipped(deferred):
     """A partner's count -1 (its K1 saw NaN/Inf): PEER_FAILED, every later
-    send of this rank carries count -1, w and the residual stay untouched."""
+    send of this rank carries count -1, w and the residual stay untouched --
+    also for the deferred step (res = NULL), whose final merge applies the w
+    update itself."""
     import torch
 
     from oracle import gtopk_oracle as orc
@@ -355,7 +358,7 @@ def test_exchange_poison_received_forwarded_and_k3_skipped():
         res0 = rng.standard_normal(m).astype(F32)
         w = torch.from_numpy(w0.copy()).cuda()
         res = torch.from_numpy(res0.copy()).cuda()
-        word = lb.call(lists[rank], w=w, res=res, lr=0.1)
+        word = lb.call(lists[rank], w=w, res=None if deferred else res, lr=0.1)
         assert word & DEV_PEER_FAILED and not word & (DEV_TIMEOUT | DEV_ABORTED)
         assert np.array_equal(w.cpu().numpy(), w0) and np.array_equal(res.cpu().numpy(), res0)
         n, _h, _i, _v = decode_slot(lb.sent_slot(1, tag), k, tag)  # the poison is forwarded
