@@ -94,6 +94,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+template <bool kSolo>
 __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   MergeSmem& S = *reinterpret_cast<MergeSmem*>(dsm);
@@ -170,6 +171,25 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
         hint_own = self_poison ? 0u : (uint32_t)__ldcg(cur_n + 1);
       }
       const uint64_t* slot = slot_of(a.inbox[a.rank], s, par, a.k);
+      auto merge_args = [&]() {
+        MergeArgs m = a.merge;
+        m.a_ll = slot + 2;
+        m.a_tag = tag;
+        m.poll = poll;
+        m.b_idx = cur_idx;
+        m.b_val = cur_val;
+        m.o_idx = a.acc_idx;
+        m.o_val = a.acc_val;
+        m.d_no = a.d_acc_n;
+        m.trace = a.trace ? a.trace + 32 + 16 * s : nullptr;
+        return m;
+      };
+      // one-CTA merge: every record this thread may read (k at most) and its
+      // own entries are loaded before the header is polled -- records already
+      // there cost no round trip of their own
+      SoloIn pre;
+      if constexpr (kSolo)
+        if (st.merge) solo_preload(merge_args(), (uint32_t)a.k, n_own, pre);
       if (threadIdx.x == 0) {
         uint32_t n, hint;
         const bool ok = ld_ll_pair(slot, tag, poll, n, hint);
@@ -192,16 +212,7 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
         pushed = true;
       }
       if (st.merge) {
-        MergeArgs m = a.merge;
-        m.a_ll = slot + 2;
-        m.a_tag = tag;
-        m.poll = poll;
-        m.b_idx = cur_idx;
-        m.b_val = cur_val;
-        m.o_idx = a.acc_idx;
-        m.o_val = a.acc_val;
-        m.d_no = a.d_acc_n;
-        m.trace = a.trace ? a.trace + 32 + 16 * s : nullptr;
+        MergeArgs m = merge_args();
         if (a.upd_w && s == last_recv) {  // the final global list: K3's membership tags
           m.tag = a.upd_tags;
           m.tag_val = tag;
@@ -222,7 +233,10 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
           m.ll_head = out_slot;
           m.ll_tag = tag;
         }
-        merge_device(m, n_in, n_own, hint_in, hint_own, G, S, wrec, wv);
+        if constexpr (kSolo)
+          merge_solo(m, min(n_in, (uint32_t)kMergeSub), min(n_own, (uint32_t)kMergeSub), hint_in, hint_own, S, pre);
+        else
+          merge_device<false>(m, n_in, n_own, hint_in, hint_own, G, S, wrec, wv);
       } else {
         const uint32_t per = (n_in + G - 1) / G;
         const uint32_t e0 = min(n_in, blk * per), e1 = min(n_in, e0 + per);
@@ -497,10 +511,11 @@ static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32
   int merges = 0;
   for (int s = 0; s < nsteps; ++s) merges += schedule[4 * s + 2] ? 1 : 0;
   const int compact_g = (upd_w && !upd_res) ? 32 * std::max(1, merges) : 0;
-  if (!merge_grid_for((const void*)exchange_kernel, k, &g, compact_g)) return GTK_ECUDA;
+  if (!merge_grid_for((const void*)exchange_kernel<false>, k, &g, compact_g)) return GTK_ECUDA;
+  const void* fn = merge_use_solo(g, k) ? (const void*)exchange_kernel<true> : (const void*)exchange_kernel<false>;
+  if (!ensure_dyn_smem(fn, merge_smem_bytes(kMergeSliceCapMax))) return GTK_ECUDA;
   a.merge.slice_cap = g.slice_cap;
   void* args[] = {&a};
   ProfScope prof(kProfExchange, (cudaStream_t)stream);
-  return merge_launch((const void*)exchange_kernel, g, args, merge_smem_bytes(g.slice_cap), (cudaStream_t)stream,
-                      true);
+  return merge_launch(fn, g, args, merge_smem_bytes(g.slice_cap), (cudaStream_t)stream, true);
 }

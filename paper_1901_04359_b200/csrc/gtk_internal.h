@@ -38,6 +38,8 @@ struct MergeGrid {
 // compact_g > 0: at most compact_g blocks whenever the union fits their
 // shared memory (a merge that shares the GPU with an HBM pass)
 bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out, int compact_g = 0);
+// a one-CTA merge of lists up to cap entries takes the merge_solo instance
+bool merge_use_solo(const MergeGrid& g, int32_t cap);
 // launch a merge-type kernel on its MergeGrid (cluster or cooperative)
 int merge_launch(const void* func, const MergeGrid& g, void** args, size_t smem, cudaStream_t st, bool pdl);
 

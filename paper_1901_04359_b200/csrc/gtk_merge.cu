@@ -13,12 +13,13 @@
 
 namespace gtk {
 
+template <bool kSolo>
 __global__ void __launch_bounds__(kMergeThreads, 1) merge_kernel(MergeArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   MergeSmem& S = *reinterpret_cast<MergeSmem*>(dsm);
   const uint32_t na = (uint32_t)__ldcg(a.d_na), nb = (uint32_t)__ldcg(a.d_nb);
   const uint32_t ha = (uint32_t)__ldcg(a.d_na + 1), hb = (uint32_t)__ldcg(a.d_nb + 1);
-  merge_device(a, na, nb, ha, hb, gridDim.x, S);
+  merge_device<kSolo>(a, na, nb, ha, hb, gridDim.x, S);
 }
 
 // Grid of a merge over two lists of <= cap entries.
@@ -137,6 +138,12 @@ bool merge_grid_for(const void* func, int32_t cap, MergeGrid* out, int compact_g
   return true;
 }
 
+bool merge_use_solo(const MergeGrid& g, int32_t cap) {
+  // GTK_MERGE_SOLO=0: the generic engine on one CTA too (A/B)
+  static const bool on = env_int("GTK_MERGE_SOLO", 1) != 0;
+  return on && g.G == 1 && !g.cluster && 2ull * (uint64_t)(cap < 1 ? 1 : cap) <= kSoloMaxSlots;
+}
+
 int merge_launch(const void* func, const MergeGrid& g, void** args, size_t smem, cudaStream_t st, bool pdl) {
   if (!g.cluster) return coop_launch(func, g.G, kMergeThreads, args, smem, st, pdl, g.coop);
   cudaLaunchConfig_t cfg = {};
@@ -164,12 +171,14 @@ int merge_launch(const void* func, const MergeGrid& g, void** args, size_t smem,
 
 int launch_merge(const MergeArgs& args, int32_t cap, cudaStream_t st) {
   MergeGrid g;
-  if (!merge_grid_for((const void*)merge_kernel, cap, &g)) return GTK_ECUDA;
+  if (!merge_grid_for((const void*)merge_kernel<false>, cap, &g)) return GTK_ECUDA;
+  const void* fn = merge_use_solo(g, cap) ? (const void*)merge_kernel<true> : (const void*)merge_kernel<false>;
+  if (!ensure_dyn_smem(fn, merge_smem_bytes(kMergeSliceCapMax))) return GTK_ECUDA;
   MergeArgs a = args;
   a.slice_cap = g.slice_cap;
   void* p[] = {&a};
   ProfScope prof(kProfMerge, st);
-  return merge_launch((const void*)merge_kernel, g, p, merge_smem_bytes(g.slice_cap), st, false);
+  return merge_launch(fn, g, p, merge_smem_bytes(g.slice_cap), st, false);
 }
 
 }  // namespace gtk

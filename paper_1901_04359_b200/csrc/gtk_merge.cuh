@@ -34,9 +34,10 @@ constexpr int kMergeMaxSplits = 65;
 constexpr int kMergeMaxCluster = 16;   // CTAs of a cluster-mode merge (non-portable size above 8)
 // cluster-mode sizing (measured, loopback exchange at P = 2: a CTA with more
 // than ~640 union slots makes its phases longer than the cluster barriers
-// save; up to ~1K slots one CTA alone beats any split)
+// save); up to 4K slots the one-CTA merge_solo beats any split (k = 1024:
+// 6.9 us vs a 4-CTA cluster's 12.7; k = 2048: 11.7 vs 12.5)
 constexpr int kMergeClusterSlots = 512;  // union slots per CTA in cluster mode
-constexpr int kMergeSoloSlots = 1024;    // unions up to this many slots: one CTA, no barriers    // sub-chunk boundaries staged per group (64 sub-chunks = 128K slots)
+constexpr int kMergeSoloSlots = 4096;    // unions up to this many slots: one CTA (merge_solo), no grid barriers
 
 struct MergeCtl {
   uint32_t n_valid;
@@ -208,6 +209,428 @@ __device__ __forceinline__ MergeWindowRec load_window_rec(const uint32_t* rec) {
   return r;
 }
 
+// ---- one-CTA merge of a small union (k <= 2K) -------------------------------
+// The whole ⊤ in one block's shared memory with a dedicated pipeline -- no
+// global workspace, no window record, ~10 block barriers in all:
+//   load   every A record (LL words, polled only if not there yet) and B entry
+//          of this thread in flight at once -- in the exchange issued before
+//          the slot header is even polled (solo_preload);
+//   union  each entry finds its union slot by one binary search in the other
+//          list (slot = own position + rank in the other list, A first on
+//          equal indices), a shared index summed once (received-then-own,
+//          collectives.py:214), exact zeros dropped (sparse.py:184-186); a
+//          2048-bin histogram of key bits 30..20 is built on the way;
+//   select the bin holding rank k; its entries (a few dozen) are gathered and
+//          ranked directly by (key desc, index asc) -- the reference's order,
+//          sparse.py:188-192; a bin with more than kSoloGather entries is
+//          refined by radix passes over key bits 19..9 and 8..0 instead (ties
+//          on the exact k-th key: lowest index first -- the union slots ARE
+//          index order, so the tie rank is a prefix count);
+//   write  kept slots compacted in slot order (already index-sorted,
+//          sparse.py:194): per-(row, warp) ballots, one 128-entry warp scan.
+// Slots are laid out in rows of kMergeThreads (slot = row * NT + thread):
+// conflict-free shared reads and coalesced output stores.
+constexpr int kSoloRows = 8;
+constexpr uint32_t kSoloMaxSlots = (uint32_t)kSoloRows * kMergeThreads;  // 4096
+constexpr int kSoloPer = kMergeSub / kMergeThreads;                     // list entries per thread (4)
+constexpr uint32_t kSoloGather = 128;  // in-bin entries ranked directly (else refined)
+static_assert(kSoloMaxSlots <= (uint32_t)kMergeSliceCap, "solo union lives in the minimum slice area");
+static_assert(kSoloRows * (kMergeThreads / 32) <= kMergeThreads, "solo row counts fit the engine's wcnt");
+static_assert(kSoloMaxSlots <= kKeptBits && kSoloGather <= (uint32_t)kGatherCap, "solo bitmap / gather");
+
+// this thread's share of both input lists, loads issued ahead of their use
+struct SoloIn {
+  uint64_t ax[kSoloPer], ay[kSoloPer];  // A: raw LL words (a_ll) or {idx, val bits}
+  int32_t bi[kSoloPer];
+  float bv[kSoloPer];
+};
+// A entries [0, na_max) (na_max >= the count still to be learnt: LL records
+// past it are loaded and ignored) and B entries [0, nb)
+static __device__ __forceinline__ void solo_preload(const MergeArgs& a, uint32_t na_max, uint32_t nb, SoloIn& in) {
+  constexpr int NT = kMergeThreads;
+  const uint32_t tid = threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < kSoloPer; ++u) {
+    const uint32_t e = u * NT + tid;
+    if (e < na_max) {
+      if (a.a_ll) {
+        ld_ll_pair_raw(a.a_ll + 2 * (size_t)e, in.ax[u], in.ay[u]);
+      } else {
+        in.ax[u] = (uint32_t)__ldcg(a.a_idx + e);
+        in.ay[u] = __float_as_uint(__ldcg(a.a_val + e));
+      }
+    }
+    if (e < nb) {
+      in.bi[u] = __ldcg(a.b_idx + e);
+      in.bv[u] = __ldcg(a.b_val + e);
+    }
+  }
+}
+
+// exclusive slot-order ranks of per-row flags (bit r of `bits` = row r of this
+// thread's slots); returns the total, positions through pos(r)
+struct SoloRanks {
+  uint32_t* cnt;  // [kSoloRows * NW] exclusive bases
+  uint32_t* bal;  // [kSoloRows * NW] ballots
+  __device__ __forceinline__ uint32_t pos(uint32_t r) const {
+    const uint32_t i = r * (kMergeThreads / 32) + warp_id();
+    return cnt[i] + __popc(bal[i] & lanemask_lt());
+  }
+};
+static __device__ __forceinline__ uint32_t solo_rank(uint32_t bits, EngineSmem<kMergeThreads>& esm,
+                                                     SoloRanks& R) {
+  constexpr int NW = kMergeThreads / 32;
+  uint32_t* cnt = esm.wcnt;
+  uint32_t* bal = esm.wbal;
+#pragma unroll
+  for (int r = 0; r < kSoloRows; ++r) {
+    const unsigned b = __ballot_sync(kFull, (bits >> r) & 1u);
+    if (lane_id() == 0) {
+      cnt[r * NW + warp_id()] = __popc(b);
+      bal[r * NW + warp_id()] = b;
+    }
+  }
+  __syncthreads();
+  if (warp_id() == 0) {  // 128 counts, 4 per lane, in (row, warp) = slot order
+    constexpr int PER = kSoloRows * NW / 32;
+    uint32_t c[PER], s = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      c[j] = cnt[lane_id() * PER + j];
+      s += c[j];
+    }
+    uint32_t x = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane_id() >= (unsigned)o) x += y;
+    }
+    uint32_t e = x - s;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      cnt[lane_id() * PER + j] = e;
+      e += c[j];
+    }
+    if (lane_id() == 31) esm.bcast[7] = x;
+  }
+  __syncthreads();
+  R.cnt = cnt;
+  R.bal = bal;
+  return esm.bcast[7];
+}
+
+// bin holding rank t (1-based from the top) of esm.hist[0, nbins), nbins <=
+// 5 * NT; every thread gets (bin, count above it, count in it) and returns the
+// histogram's total (< t: no such bin).  Two block barriers: each warp scans
+// its 5 * 32 reversed bins, the warp totals are combined by every warp from
+// shared memory.
+static __device__ __forceinline__ uint32_t solo_find(uint32_t nbins, uint32_t t, EngineSmem<kMergeThreads>& esm,
+                                                     uint32_t& bin, uint32_t& above, uint32_t& in_bin) {
+  constexpr int PER = 5, NW = kMergeThreads / 32;
+  uint32_t c[PER], sum = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {  // thread t owns reversed bins [5t, 5t + 5)
+    const uint32_t rb = threadIdx.x * PER + j;
+    c[j] = rb < nbins ? esm.hist[nbins - 1 - rb] : 0u;
+    sum += c[j];
+  }
+  uint32_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane_id() >= (unsigned)o) x += y;
+  }
+  if (lane_id() == 31) esm.scan[warp_id()] = x;
+  __syncthreads();
+  const uint32_t wt = lane_id() < (unsigned)NW ? esm.scan[lane_id()] : 0u;
+  const uint32_t wpre = __reduce_add_sync(kFull, lane_id() < warp_id() ? wt : 0u);
+  const uint32_t tot = __reduce_add_sync(kFull, wt);
+  const uint32_t pre = wpre + x - sum;
+  if (pre < t && pre + sum >= t) {
+    uint32_t acc = pre;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      if (acc < t && acc + c[j] >= t) {
+        esm.bcast[0] = nbins - 1 - (threadIdx.x * PER + j);
+        esm.bcast[1] = acc;
+        esm.bcast[2] = c[j];
+      }
+      acc += c[j];
+    }
+  }
+  __syncthreads();
+  bin = esm.bcast[0];
+  above = esm.bcast[1];
+  in_bin = esm.bcast[2];
+  return tot;
+}
+
+// a = received (plain list or LL records), b = own; na, nb <= kMergeSub,
+// na + nb <= kSoloMaxSlots <= slice_cap; `in` holds the preloaded entries;
+// hint_a / hint_b: the lists' k-th keys (the first histogram's window)
+static __device__ __forceinline__ void merge_solo(const MergeArgs& a, uint32_t na, uint32_t nb, uint32_t hint_a,
+                                                  uint32_t hint_b, MergeSmem& S, const SoloIn& in) {
+  constexpr int NT = kMergeThreads;
+  EngineSmem<NT>& esm = S.esm;
+  const uint32_t N = na + nb, tid = threadIdx.x;
+  if (N == 0) {
+    if (tid == 0) {
+      a.d_no[0] = 0;
+      a.d_no[1] = 0;
+      if (a.ll_head) st_ll_pair(a.ll_head, 0u, 0u, a.ll_tag);
+    }
+    __syncthreads();
+    return;
+  }
+  int32_t* const uI = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(&S) + kMergeSmemFixed);
+  float* const uV = reinterpret_cast<float*>(uI + a.slice_cap);
+  // the first histogram's window: a full list has all k entries >= its hint,
+  // so (cancellations aside) the union's k-th key is >= max(hint); 2048 bins
+  // over the 2 octaves above it (+ OVER) leave ~1 entry per bin -- no
+  // contended shared atomics, a tiny bin to rank
+  uint32_t lo = 0;
+  if (na >= a.k && hint_a < kInfKey) lo = max(lo, hint_a);
+  if (nb >= a.k && hint_b < kInfKey) lo = max(lo, hint_b);
+  uint32_t sh = lo ? kMergeWinShift : 20u;
+  merge_stamp(a, 0);
+  // ---- load: A records that were not there at preload time are polled now
+  int32_t ai[kSoloPer];
+  float av[kSoloPer];
+#pragma unroll
+  for (int u = 0; u < kSoloPer; ++u) {
+    if (u * NT >= max(na, nb)) break;  // (block-uniform)
+    const uint32_t e = u * NT + tid;
+    if (e < na) {
+      if (!a.a_ll || ((uint32_t)(in.ax[u] >> 32) == a.a_tag && (uint32_t)(in.ay[u] >> 32) == a.a_tag)) {
+        ai[u] = (int32_t)(uint32_t)in.ax[u];
+        av[u] = __uint_as_float((uint32_t)in.ay[u]);
+      } else {
+        a_entry(a, e, ai[u], av[u]);
+      }
+      S.sAi[e] = ai[u];
+      S.sAv[e] = av[u];
+    }
+    if (e < nb) {
+      S.sBi[e] = in.bi[u];
+      S.sBv[e] = in.bv[u];
+    }
+  }
+  for (uint32_t b = tid; b < (uint32_t)kHistLen; b += NT) esm.hist[b] = 0;
+  for (uint32_t w = tid; w < kSoloMaxSlots / 32; w += NT) esm.kept_bits[w] = 0;
+  if (tid == 0) {
+    S.s_valid = 0;
+    esm.ng = 0;
+    esm.bcast[6] = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  merge_stamp(a, 1);
+  // ---- union slots + the window histogram
+  uint32_t my_valid = 0;
+  auto count = [&](int32_t i, float v) {
+    ++my_valid;
+    const uint32_t key = merge_key_of(v);
+    if (key >= lo) {
+      atomicAdd(&esm.hist[min((uint32_t)kBins, (key - lo) >> sh)], 1u);
+      // a likely winner: its w line (the fused update) heads for L2 now
+      if (a.upd_w) prefetch_l2(a.upd_w + i);
+    }
+  };
+#pragma unroll
+  for (int u = 0; u < kSoloPer; ++u) {
+    if (u * NT >= max(na, nb)) break;  // (block-uniform)
+    const uint32_t t = u * NT + tid;
+    if (t < na) {
+      const int32_t x = ai[u];
+      const uint32_t r = lower_bound_s(S.sBi, nb, x);
+      float v = av[u];
+      if (r < nb && S.sBi[r] == x) v = add_x86(v, S.sBv[r]);
+      const bool valid = v != 0.0f;
+      GTK_DCHECK(t + r < N);
+      uI[t + r] = valid ? x : -1;
+      uV[t + r] = v;
+      if (valid) count(x, v);
+    }
+    if (t < nb) {
+      const int32_t x = in.bi[u];
+      const uint32_t r = upper_bound_s(S.sAi, na, x);
+      const bool valid = !(r > 0 && S.sAi[r - 1] == x) && in.bv[u] != 0.0f;
+      GTK_DCHECK(t + r < N);
+      uI[t + r] = valid ? x : -1;
+      uV[t + r] = in.bv[u];
+      if (valid) count(x, in.bv[u]);
+    }
+  }
+  my_valid = warp_sum(my_valid);
+  if (lane_id() == 0 && my_valid) atomicAdd(&S.s_valid, my_valid);
+  __syncthreads();
+  merge_stamp(a, 2);
+  const uint32_t n_valid = S.s_valid;
+  const bool keep_all = n_valid <= a.k;
+  // ---- the k-th key's bin [blo, bhi): kept(key) = key >= bhi, or key in the
+  // bin and (mode) the whole bin / its gathered rank / its index-order tie
+  // rank says so.  A bin too crowded to rank is refined 2^11-fold.
+  enum { kWhole, kBitmap, kTies };
+  int mode = kWhole;
+  uint64_t blo = 0, bhi = 0;
+  uint32_t t = a.k;
+  if (!keep_all) {
+    uint64_t hi = 0x80000000ull;
+#pragma unroll 1
+    for (int r = 0; r < 5; ++r) {
+      if (r > 0) {  // rebuild over [lo, hi) (a refinement or the full range)
+        for (uint32_t b = tid; b < (uint32_t)kHistLen; b += NT) esm.hist[b] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kSoloRows; ++q) {
+    if (q * NT >= N) break;  // (block-uniform: rows past the union)
+          const uint32_t s = q * NT + tid;
+          if (s < N && uI[s] >= 0) {
+            const uint32_t key = merge_key_of(uV[s]);
+            if (key >= lo && (uint64_t)key < hi) atomicAdd(&esm.hist[min((uint32_t)kBins, (key - lo) >> sh)], 1u);
+          }
+        }
+        __syncthreads();
+      }
+      uint32_t bin, above, in_bin;
+      if (solo_find(kHistLen, t, esm, bin, above, in_bin) < t) {
+        // the window missed (cancellation on shared indices): the full range
+        GTK_DCHECK(lo != 0);
+        lo = 0;
+        sh = 20;
+        continue;
+      }
+      if (r == 0) merge_stamp(a, 5);
+      if (a.trace && tid == 0 && r == 0) {  // diagnostics: the k-th key's bin
+        a.trace[10] = bin;
+        a.trace[11] = in_bin;
+        a.trace[12] = lo;
+      }
+      blo = (uint64_t)lo + ((uint64_t)bin << sh);
+      bhi = bin < (uint32_t)kBins ? min((uint64_t)(blo + (1ull << sh)), hi) : hi;
+      t -= above;
+      if (in_bin == t) break;  // every entry of the bin is kept
+      if (in_bin <= kSoloGather) {
+        // gather the bin and rank it directly: (key desc, index asc)
+        mode = kBitmap;
+#pragma unroll
+        for (int q = 0; q < kSoloRows; ++q) {
+    if (q * NT >= N) break;  // (block-uniform: rows past the union)
+          const uint32_t s = q * NT + tid;
+          if (s < N && uI[s] >= 0) {
+            const uint32_t key = merge_key_of(uV[s]);
+            if (key >= blo && key < bhi) {
+              const uint32_t p = atomicAdd(&esm.ng, 1u);
+              esm.keys[p] = key;
+              esm.gidx[p] = uI[s];
+              esm.gblk[p] = s;
+            }
+          }
+        }
+        __syncthreads();
+        merge_stamp(a, 6);
+        const uint32_t ng = esm.ng;
+        for (uint32_t j = tid; j < ng; j += NT) {
+          const uint32_t kj = esm.keys[j];
+          const int32_t ij = esm.gidx[j];
+          uint32_t rank = 0;
+          for (uint32_t q0 = 0; q0 < ng; q0 += 8) {  // 8 independent loads in flight
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const uint32_t q = q0 + u;
+              if (q < ng) {
+                const uint32_t kq = esm.keys[q];
+                const int32_t iq = esm.gidx[q];
+                rank += (kq > kj) | ((kq == kj) & (iq < ij));
+              }
+            }
+          }
+          if (rank < t) atomicOr(&esm.kept_bits[esm.gblk[j] >> 5], 1u << (esm.gblk[j] & 31));
+        }
+        __syncthreads();
+        merge_stamp(a, 7);
+        break;
+      }
+      if (bhi - blo == 1) {  // one exact key: t of its in_bin entries, lowest index first
+        mode = kTies;
+        break;
+      }
+      lo = (uint32_t)blo;
+      hi = bhi;
+      sh = ceil_log2_u64((bhi - blo + kBins - 1) / kBins);
+    }
+  }
+  merge_stamp(a, 3);
+  // ---- kept flags in slot order
+  uint32_t eq_bits = 0, kbits = 0;
+#pragma unroll
+  for (int q = 0; q < kSoloRows; ++q) {
+    if (q * NT >= N) break;  // (block-uniform: rows past the union)
+    const uint32_t s = q * NT + tid;
+    if (s < N && uI[s] >= 0) {
+      const uint32_t key = merge_key_of(uV[s]);
+      bool kept = keep_all || key >= bhi;
+      if (!kept && key >= blo) {
+        if (mode == kWhole) kept = true;
+        else if (mode == kBitmap) kept = (esm.kept_bits[s >> 5] >> (s & 31)) & 1u;
+        else eq_bits |= 1u << q;
+      }
+      if (kept) kbits |= 1u << q;
+    }
+  }
+  if (mode == kTies) {  // t entries of key == blo, lowest slots first
+    SoloRanks E;
+    solo_rank(eq_bits, esm, E);
+#pragma unroll
+    for (int q = 0; q < kSoloRows; ++q)
+      if (((eq_bits >> q) & 1u) && E.pos(q) < t) kbits |= 1u << q;
+    __syncthreads();  // esm.wcnt / wbal reused below
+  }
+  // the fused update's w loads go out before the compaction's barriers
+  Sink out{a.o_idx, a.o_val, a.d_no, nullptr, true, nullptr, nullptr, 2u, 0u, 0u, 3u,
+           a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling, a.tag, a.tag_val, a.ll_body, a.ll_head, a.ll_tag};
+  out.upd_skip = a.upd_skip;
+  const Sink wout = sink_for_write(out);
+  float wv[kSoloRows];
+  if (wout.upd_w) {
+#pragma unroll
+    for (int q = 0; q < kSoloRows; ++q)
+      if (q * NT < N && ((kbits >> q) & 1u)) wv[q] = wout.upd_w[uI[q * NT + tid]];
+  }
+  // the hint: the k-th key = the smallest kept key
+  uint32_t kmin = 0xFFFFFFFFu;
+#pragma unroll
+  for (int q = 0; q < kSoloRows; ++q)
+    if (q * NT < N && ((kbits >> q) & 1u)) kmin = min(kmin, merge_key_of(uV[q * NT + tid]));
+  kmin = __reduce_min_sync(kFull, kmin);
+  if (lane_id() == 0 && kmin != 0xFFFFFFFFu) atomicMin(&esm.bcast[6], kmin);
+  SoloRanks R;
+  const uint32_t n_out = solo_rank(kbits, esm, R);  // (its barriers publish bcast[6])
+  GTK_DCHECK(n_out == (keep_all ? n_valid : a.k));
+  // ---- write (+ the fused side effects of the exchange's final merge)
+#pragma unroll
+  for (int q = 0; q < kSoloRows; ++q) {
+    if (q * NT >= N) break;  // (block-uniform: rows past the union)
+    if ((kbits >> q) & 1u) {
+      const uint32_t p = R.pos(q);
+      const int32_t i = uI[q * NT + tid];
+      const float v = uV[q * NT + tid];
+      wout.o_idx[p] = i;
+      wout.o_val[p] = v;
+      if (wout.upd_w)
+        wout.upd_w[i] = __fsub_rn(wv[q], __fmul_rn(wout.upd_lr, scale_u(v, wout.upd_Pf, wout.upd_scaling)));
+      if (wout.tag) wout.tag[i] = wout.tag_val;
+      if (wout.ll_body) st_ll_pair(wout.ll_body + 2 * (size_t)p, (uint32_t)i, __float_as_uint(v), wout.ll_tag);
+    }
+  }
+  if (tid == 0) sink_count(out, n_out, keep_all ? 0u : esm.bcast[6]);
+  merge_stamp(a, 4);
+  __syncthreads();  // callers may reuse the inputs / shared memory right after
+}
+
+// kSolo: the instance for one-CTA grids of lists up to kSoloMaxSlots / 2
+// entries (merge_solo only -- its own register allocation); the host picks it
+// with merge_use_solo
+template <bool kSolo = false>
 static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t na, uint32_t nb, uint32_t hint_a,
                                                     uint32_t hint_b, unsigned G, MergeSmem& S,
                                                     uint32_t* rec = nullptr, MergeWindowRec rv = {}) {
@@ -221,6 +644,16 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
       if (a.ll_head) st_ll_pair(a.ll_head, 0u, 0u, a.ll_tag);
     }
     grid_sync(&a.ews->bar, G);  // callers may reuse the inputs right after
+    return;
+  }
+  if constexpr (kSolo) {
+    // (the host guarantees na, nb <= kMergeSub: lists of <= cap <= kSoloMaxSlots / 2)
+    GTK_DCHECK(G == 1 && na <= (uint32_t)kMergeSub && nb <= (uint32_t)kMergeSub && N <= a.slice_cap);
+    na = min(na, (uint32_t)kMergeSub);
+    nb = min(nb, (uint32_t)kMergeSub);
+    SoloIn in;
+    solo_preload(a, na, nb, in);
+    merge_solo(a, na, nb, hint_a, hint_b, S, in);
     return;
   }
   uint32_t win_lo = 0;
