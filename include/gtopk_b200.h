@@ -247,6 +247,20 @@ int gtk_densify(const int32_t* idx, const float* val, const int32_t* d_n, int64_
 int gtk_topk_accumulate(const int32_t* idx, const float* val, const int32_t* d_n, int32_t P,
                         int64_t stride, int64_t m, float* out, int32_t divide, void* stream);
 
+/* optimizer.py:232-241 (measure_divergence) terms: pruned[i] = total[g_idx[i]] -
+ * g_val[i] for the global list's entries (the reference's masked sum minus
+ * densify(global) at the mask), and *d_shared = |{global indices} ∩ {naive
+ * indices}| (_mask_divergence, optimizer.py:192-196).  Both lists index-sorted. */
+int gtk_divergence_terms(const int32_t* g_idx, const float* g_val, const int32_t* d_gn, const int32_t* n_idx,
+                         const int32_t* d_nn, const float* total, int64_t m, float* pruned, uint32_t* d_shared,
+                         void* stream);
+
+/* The step's single host round trip (optimizer.py:246-252 builds the
+ * StepReport and raises from it): h_out[0] = *d_status, h_out[1] = *d_count
+ * (h_out: pinned host memory), then *d_status = 0 when reset; synchronises
+ * the stream. */
+int gtk_status_read(const int32_t* d_status, const int32_t* d_count, int32_t* h_out, int32_t reset, void* stream);
+
 /* rank-ordered dense sum of P device vectors (in-process dense baseline;
  * optimizer.py:108-115 summation order). srcs: device array of P pointers. */
 int gtk_dense_sum(const float* const* srcs, int32_t P, int64_t m, float* out, void* stream);

@@ -59,6 +59,8 @@ EXPORTS = (
     "gtk_densify",
     "gtk_topk_accumulate",
     "gtk_dense_sum",
+    "gtk_divergence_terms",
+    "gtk_status_read",
     "gtk_exchange_inbox_bytes",
     "gtk_dev_alloc",
     "gtk_dev_free",
@@ -116,6 +118,8 @@ _SIGS = {
     "gtk_densify": ([_P, _P, _P, _I64, _P, _P], _I32),
     "gtk_topk_accumulate": ([_P, _P, _P, _I32, _I64, _I64, _P, _I32, _P], _I32),
     "gtk_dense_sum": ([_P, _I32, _I64, _P, _P], _I32),
+    "gtk_divergence_terms": ([_P, _P, _P, _P, _P, _P, _I64, _P, _P, _P], _I32),
+    "gtk_status_read": ([_P, _P, _P, _I32, _P], _I32),
     "gtk_exchange_inbox_bytes": ([_I32, _I32, ctypes.POINTER(_SZ)], _I32),
     "gtk_dev_alloc": ([_SZ, ctypes.POINTER(_P)], _I32),
     "gtk_dev_free": ([_P], _I32),

@@ -248,6 +248,60 @@ extern "C" int gtk_topk_accumulate(const int32_t* idx, const float* val, const i
   return GTK_OK;
 }
 
+// measure_divergence (optimizer.py:232-241): for every global entry i the
+// pruned mass total[g_idx[i]] - g_val[i] (the reference's masked sum minus
+// densify(global) at the mask, optimizer.py:238-240), and the number of global
+// indices also in the naive list (|shared| of _mask_divergence, :192-196):
+// one binary search per entry in the index-sorted naive list, warp-aggregated
+__global__ void divergence_kernel(const int32_t* g_idx, const float* g_val, const int32_t* d_gn,
+                                  const int32_t* n_idx, const int32_t* d_nn, const float* total, float* pruned,
+                                  uint32_t* d_shared) {
+  const uint32_t gn = (uint32_t)__ldg(d_gn), nn = (uint32_t)__ldg(d_nn);
+  for (uint32_t base = blockIdx.x * blockDim.x; base < gn; base += gridDim.x * blockDim.x) {
+    const uint32_t e = base + threadIdx.x;
+    bool hit = false;
+    if (e < gn) {
+      const int32_t i = g_idx[e];
+      pruned[e] = __fsub_rn(total[i], g_val[e]);
+      uint32_t lo = 0, hi = nn;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (n_idx[mid] < i) lo = mid + 1;
+        else hi = mid;
+      }
+      hit = lo < nn && n_idx[lo] == i;
+    }
+    const unsigned bal = __ballot_sync(0xFFFFFFFFu, hit);
+    if ((threadIdx.x & 31) == 0 && bal) atomicAdd(d_shared, (uint32_t)__popc(bal));
+  }
+}
+
+extern "C" int gtk_divergence_terms(const int32_t* g_idx, const float* g_val, const int32_t* d_gn,
+                                    const int32_t* n_idx, const int32_t* d_nn, const float* total, int64_t m,
+                                    float* pruned, uint32_t* d_shared, void* stream) {
+  if (!g_idx || !g_val || !d_gn || !n_idx || !d_nn || !total || !pruned || !d_shared || m < 1 ||
+      m >= (int64_t(1) << 31))
+    return GTK_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  GTK_CUDA(cudaMemsetAsync(d_shared, 0, sizeof(uint32_t), st));
+  divergence_kernel<<<num_sms() * 2, 256, 0, st>>>(g_idx, g_val, d_gn, n_idx, d_nn, total, pruned, d_shared);
+  GTK_CHECK_LAUNCH();
+  return GTK_OK;
+}
+
+// the step's one host round trip: status word and count -> pinned host pair
+// (then, with reset, the status word back to 0 for the next step), synchronised
+extern "C" int gtk_status_read(const int32_t* d_status, const int32_t* d_count, int32_t* h_out, int32_t reset,
+                               void* stream) {
+  if (!d_status || !d_count || !h_out) return GTK_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  GTK_CUDA(cudaMemcpyAsync(h_out, d_status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  GTK_CUDA(cudaMemcpyAsync(h_out + 1, d_count, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  if (reset) GTK_CUDA(cudaMemsetAsync(const_cast<int32_t*>(d_status), 0, sizeof(int32_t), st));
+  GTK_CUDA(cudaStreamSynchronize(st));
+  return GTK_OK;
+}
+
 extern "C" int gtk_dense_sum(const float* const* srcs, int32_t P, int64_t m, float* out, void* stream) {
   if (!srcs || !out || P < 1 || m < 1 || m >= (int64_t(1) << 31)) return GTK_EINVAL;
   dense_sum_kernel<<<grid_for(m, 256), 256, 0, (cudaStream_t)stream>>>(srcs, P, (uint32_t)m, out);

@@ -40,7 +40,10 @@ def P(t) -> ctypes.c_void_p:
 
 
 def stream_of(device: torch.device) -> ctypes.c_void_p:
-    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    """torch's current stream on `device` as a raw cudaStream_t (the direct
+    binding: torch.cuda.current_stream() costs ~10 us of Python per call)."""
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(idx))
 
 
 class DeviceList:
@@ -332,6 +335,26 @@ def dense_sum(srcs, m: int, out: torch.Tensor) -> None:
     _lib.call("gtk_dense_sum", P(ptrs), len(srcs), m, P(out), stream_of(out.device))
     # keep the pointer table alive until the kernel has consumed it
     torch.cuda.current_stream(out.device).synchronize()
+
+
+def divergence_terms(glist: DeviceList, naive: DeviceList, total: torch.Tensor):
+    """gtk_divergence_terms: (pruned mass per global entry [device f32, gn],
+    |shared indices| [device u32 as int32]) of optimizer.py:232-241."""
+    dev = total.device
+    pruned = torch.empty(glist.cap, dtype=torch.float32, device=dev)
+    shared = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.call("gtk_divergence_terms", P(glist.idx), P(glist.val), P(glist.count), P(naive.idx), P(naive.count),
+              P(total), total.numel(), P(pruned), P(shared), stream_of(dev))
+    return pruned, shared
+
+
+def read_status(status: torch.Tensor, count: torch.Tensor, host: torch.Tensor, reset: bool) -> tuple[int, int]:
+    """gtk_status_read: (status word, count) in one D2H round trip into the
+    pinned `host` pair, the status word zeroed behind it when `reset`."""
+    _lib.call("gtk_status_read", P(status), P(count), ctypes.c_void_p(host.data_ptr()), int(reset),
+              stream_of(status.device))
+    h = host.numpy()
+    return int(h[0]), int(h[1])
 
 
 def raise_status(word: int) -> None:

@@ -269,14 +269,29 @@ def _scaling_code(state: OptimizerState) -> int:
 
 
 class _Timer:
+    """Phase events of a step (StepReport's t_compress / t_communicate),
+    created once per state and recorded on the stream looked up once."""
+
     def __init__(self):
         self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        self.stream = None
+
+    def start(self, dev):
+        self.stream = torch.cuda.current_stream(dev)
+        return self
 
     def mark(self, i):
-        self.ev[i].record()
+        self.ev[i].record(self.stream)
 
     def ms(self, i, j):
         return self.ev[i].elapsed_time(self.ev[j])
+
+
+def _timer(state) -> _Timer:
+    tm = state._bufs.get("timer")
+    if tm is None:
+        tm = state._bufs["timer"] = _Timer()
+    return tm.start(state._dev)
 
 
 def _select_checked(state, g, k, sel: DeviceList, status, fused_update: bool = False) -> None:
@@ -300,10 +315,25 @@ def _select_checked(state, g, k, sel: DeviceList, status, fused_update: bool = F
         _dev.select(state._res, g, state._res2, k, sel, status[0:1], window=win)
 
 
-def _finish(status, count_src) -> tuple[int, int]:
-    """One small D2H: (status word, count)."""
-    status[1:2].copy_(count_src)
-    word, cnt = (int(x) for x in status.cpu().tolist())
+def _begin(state) -> torch.Tensor:
+    """The step's device status word, zero (it is left zeroed by the previous
+    step's _finish; anything else re-zeroes it)."""
+    status = state._status()
+    if not state._bufs.get("status_clean", False):
+        status.zero_()
+    state._bufs["status_clean"] = False
+    return status
+
+
+def _finish(state, count_src) -> tuple[int, int]:
+    """The step's one host round trip (gtk_status_read): (status word, count),
+    the status word re-zeroed for the next step."""
+    host = state._bufs.get("status_host")
+    if host is None:
+        host = state._bufs["status_host"] = torch.zeros(2, dtype=torch.int32, pin_memory=True)
+    word, cnt = _dev.read_status(state._status(), count_src, host, reset=True)
+    state._bufs["status_clean"] = True
+    state._bufs["last_status"] = word  # (diagnostics: e.g. the dense-fallback bit)
     return word, cnt
 
 
@@ -314,10 +344,9 @@ def gtopk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float =
         raise ValueError("P must match the cluster size")
     dev, g = _setup(state, ep, grad)
     state._ensure_velocity()
-    status = state._status()
-    status.zero_()
+    status = _begin(state)
     sel = state._list("sel", k)
-    tm = _Timer()
+    tm = _timer(state)
     tm.mark(0)
     if P == 1 and not measure_divergence and _dev.sparse_update_fusable(state.lr, state.momentum):
         # one rank: gtopk_allreduce is the identity (collectives.py:188-219), no
@@ -325,7 +354,7 @@ def gtopk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float =
         _select_checked(state, g, k, sel, status, fused_update=True)
         tm.mark(1)
         tm.mark(2)
-        word, gnnz = _finish(status, sel.n)
+        word, gnnz = _finish(state, sel.n)
         _dev.raise_status(word)
         state._commit(swap_residual=True)
         state._pending = (sel, state._window)  # this step's winners, pending in the new residual
@@ -357,7 +386,7 @@ def gtopk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float =
     if not fused_k3:
         _dev.scatter_update(state._w, state._res2, state._vel, glist, sel, state.m, float(np.float32(state.lr)),
                             float(np.float32(state.momentum)), P, _scaling_code(state), skip=status[0:1])
-    word, gnnz = _finish(status, glist.n)
+    word, gnnz = _finish(state, glist.n)
     _dev.raise_status(word)
     state._commit(swap_residual=True)
     return StepReport(loss=loss, t_compute_ms=t_compute_ms, t_compress_ms=tm.ms(0, 1),
@@ -372,10 +401,9 @@ def topk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float = 
         raise ValueError("P must match the cluster size")
     dev, g = _setup(state, ep, grad)
     state._ensure_velocity()
-    status = state._status()
-    status.zero_()
+    status = _begin(state)
     sel = state._list("sel", k)
-    tm = _Timer()
+    tm = _timer(state)
     tm.mark(0)
     _select_checked(state, g, k, sel, status)
     tm.mark(1)
@@ -384,7 +412,7 @@ def topk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float = 
     averaged = _coll.topk_allreduce(ep, DeviceSparseVector(sel), P)
     tm.mark(2)
     _dense_update(state, averaged)
-    word, nnz = _finish(status, sel.n)
+    word, nnz = _finish(state, sel.n)
     _dev.raise_status(word)
     state._commit(swap_residual=True)
     return StepReport(loss=loss, t_compute_ms=t_compute_ms, t_compress_ms=tm.ms(0, 1),
@@ -434,17 +462,20 @@ def _naive_global_select(total: torch.Tensor, k: int, dev) -> DeviceList:
 def _divergence(ep, sel: DeviceList, glist: DeviceList, k: int, m: int):
     """optimizer.py:232-241: reference (allgather) selection vs tree result:
     mask divergence and the |mass| pruned mid-tree at indices that still
-    landed in the global mask."""
+    landed in the global mask.  The intersection and the pruned terms come
+    from one kernel (gtk_divergence_terms); the lost mass is then summed over
+    the dense m-vector exactly as the reference does (np.abs(pruned).sum():
+    numpy's pairwise order over all m slots, zeros included), so it matches
+    bitwise -- a diagnostics-only host reduction of k D2H'd values."""
     dev = sel.device
     total = _coll.rank_order_sparse_sum(ep, DeviceSparseVector(sel))
     naive = _naive_global_select(total, k, dev)
-    gi, gv = glist.to_host()
-    ni, _nv = naive.to_host()
-    sa, sb = set(gi.tolist()), set(ni.tolist())
-    divergence = 1.0 - len(sa & sb) / max(len(sa), len(sb), 1)
-    t = total.cpu().numpy()
-    pruned = t[gi.astype(np.int64)] - gv  # masked total minus densify(global)
-    lost_mass = float(np.abs(pruned.astype(FLOAT)).sum())
+    pruned, shared = _dev.divergence_terms(glist, naive, total)
+    gn, nn, n_shared = (int(x) for x in torch.cat([glist.count[:1], naive.count[:1], shared]).cpu().tolist())
+    divergence = 1.0 - n_shared / max(gn, nn, 1)
+    dense = np.zeros(m, dtype=FLOAT)
+    dense[glist.idx[:gn].cpu().numpy().astype(np.int64)] = pruned[:gn].cpu().numpy()
+    lost_mass = float(np.abs(dense).sum())
     return lost_mass, divergence
 
 
@@ -456,10 +487,9 @@ def gtopk_naive_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: f
         raise ValueError("P must match the cluster size")
     dev, g = _setup(state, ep, grad)
     state._ensure_velocity()
-    status = state._status()
-    status.zero_()
+    status = _begin(state)
     sel = state._list("sel", k)
-    tm = _Timer()
+    tm = _timer(state)
     tm.mark(0)
     _select_checked(state, g, k, sel, status)
     tm.mark(1)
@@ -479,7 +509,7 @@ def gtopk_naive_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: f
     scaling = 1 if state.update_scaling == "average" else 2
     _dev.scatter_update(state._w, state._res2, state._vel, gsel, sel, state.m, float(np.float32(state.lr)),
                         float(np.float32(state.momentum)), P, scaling, skip=status[0:1])
-    word, nnz = _finish(status, gsel.n)
+    word, nnz = _finish(state, gsel.n)
     _dev.raise_status(word)
     state._commit(swap_residual=True)
     return StepReport(loss=loss, t_compute_ms=t_compute_ms, t_compress_ms=tm.ms(0, 1),

@@ -363,6 +363,44 @@ def test_divergence_and_lost_mass(gk, opt):
     assert outs[0][1].residual[6] == 0.0 and outs[1][1].residual[6] == 0.0
 
 
+def test_divergence_lost_mass_bitwise(gk, opt):
+    """measure_divergence at a real size, bitwise against the reference's own
+    formulas (optimizer.py:232-241) on the oracle's selections: the mass is
+    numpy's sum over all m slots (zeros included), the divergence the set
+    arithmetic of _mask_divergence."""
+    from oracle import gtopk_oracle as orc
+
+    P, m, k = 4, 200_003, 1500
+    rng = np.random.default_rng(23)
+    grads = [rng.standard_normal(m).astype(np.float32) for _ in range(P)]
+    # correlated coordinates, so the tree prunes mass that lands in the mask
+    hot = rng.choice(m, 400, replace=False)
+    for g in grads:
+        g[hot] += np.float32(2.5)
+    sels = [orc.top_k_select(g, k)[:2] for g in grads]
+    total = np.zeros(m, dtype=np.float32)
+    for i, v in sels:  # rank order (optimizer.py:176-183)
+        total[i.astype(np.int64)] += v
+    gi, gv = orc.tree_fold(sels, k)
+    ni, nv, _ = orc.top_k_select(total, k)
+    ni = ni[nv != 0]
+    mask = np.zeros(m, dtype=bool)
+    mask[gi.astype(np.int64)] = True
+    want_mass = float(np.abs(np.where(mask, total, np.float32(0)) - orc.densify(gi, gv, m)).sum())
+    sa, sb = set(gi.tolist()), set(ni.tolist())
+    want_div = 1.0 - len(sa & sb) / max(len(sa), len(sb), 1)
+
+    def w(ep):
+        st = opt.make_state(zeros(m), lr=1.0)
+        return opt.gtopk_step(st, ep, grads[ep.rank], k, P, measure_divergence=True)
+
+    reps = gk.run_workers(gk.create_local_cluster(P), w)
+    assert want_mass > 0.0 and 0.0 < want_div < 1.0
+    for rep in reps:
+        assert rep.lost_mass == want_mass
+        assert rep.divergence == want_div
+
+
 def test_extra_residual_identity_and_replicas(gk, opt):
     from oracle import gtopk_oracle as orc
 

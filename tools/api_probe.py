@@ -25,7 +25,7 @@ t0 = time.perf_counter()
 n = 100
 for i in range(n):
     opt.gtopk_step(st, ep, grads[i % 2], k, 1)
-    fb += bool(int(st._status()[0].item()) & 0x2)
+    fb += bool(st._bufs.get("last_status", 0) & 0x2)
 torch.cuda.synchronize()
 print(f"gtopk_step m={m} k={k}: {(time.perf_counter() - t0) / n * 1e3:.3f} ms per call, dense fallbacks {fb}/{n}")
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -35,3 +35,15 @@ for i in range(n):
 e1.record()
 e1.synchronize()
 print(f"  device-event span per call: {e0.elapsed_time(e1) / n:.3f} ms")
+
+if os.environ.get("API_PROFILE"):
+    import cProfile
+    import pstats
+
+    pr = cProfile.Profile()
+    pr.enable()
+    for i in range(200):
+        opt.gtopk_step(st, ep, grads[i % 2], k, 1)
+    pr.disable()
+    torch.cuda.synchronize()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(25)
