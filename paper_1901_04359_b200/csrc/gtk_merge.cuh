@@ -209,6 +209,47 @@ __device__ __forceinline__ MergeWindowRec load_window_rec(const uint32_t* rec) {
   return r;
 }
 
+// Union slots [s_lo, s_hi) of the merged sequence of the staged sA[0, la) and
+// sB[0, lb) (index-sorted; A first on equal indices) for one thread: one
+// merge-path search for the thread's first slot, then a sequential merge --
+// ~log2(la + lb) + (s_hi - s_lo) dependent shared loads instead of one binary
+// search per entry.  A shared index is summed once (received-then-own,
+// collectives.py:214) in A's slot; B's copy leaves an empty slot.  prevA /
+// (nextB, nextBv): the A entry before sA[0] and the B entry after sB[lb - 1]
+// (-1: none).  emit(slot, idx, val, valid).
+template <class Emit>
+static __device__ __forceinline__ void union_by_path(const int32_t* sAi, const float* sAv, uint32_t la,
+                                                     const int32_t* sBi, const float* sBv, uint32_t lb,
+                                                     uint32_t s_lo, uint32_t s_hi, int32_t prevA, int32_t nextB,
+                                                     float nextBv, Emit&& emit) {
+  uint32_t lo = s_lo > lb ? s_lo - lb : 0u, hi = min(s_lo, la);
+  while (lo < hi) {  // # A entries among the first s_lo merged ones
+    const uint32_t mid = (lo + hi) >> 1;
+    if (sAi[mid] <= sBi[s_lo - 1 - mid]) lo = mid + 1;
+    else hi = mid;
+  }
+  uint32_t i = lo, j = s_lo - lo;
+  for (uint32_t sl = s_lo; sl < s_hi; ++sl) {
+    if (i < la && (j >= lb || sAi[i] <= sBi[j])) {
+      const int32_t x = sAi[i];
+      float v = sAv[i];
+      if (j < lb) {
+        if (sBi[j] == x) v = add_x86(v, sBv[j]);
+      } else if (nextB == x) {
+        v = add_x86(v, nextBv);
+      }
+      emit(sl, x, v, v != 0.0f);
+      ++i;
+    } else {
+      const int32_t x = sBi[j];
+      const float v = sBv[j];
+      const bool dup = i > 0 ? (sAi[i - 1] == x) : (prevA == x);
+      emit(sl, x, v, !dup && v != 0.0f);
+      ++j;
+    }
+  }
+}
+
 // ---- one-CTA merge of a small union (k <= 2K) -------------------------------
 // The whole ⊤ in one block's shared memory with a dedicated pipeline -- no
 // global workspace, no window record, ~10 block barriers in all:
@@ -435,30 +476,15 @@ static __device__ __forceinline__ void merge_solo(const MergeArgs& a, uint32_t n
       if (a.upd_w) prefetch_l2(a.upd_w + i);
     }
   };
-#pragma unroll
-  for (int u = 0; u < kSoloPer; ++u) {
-    if (u * NT >= max(na, nb)) break;  // (block-uniform)
-    const uint32_t t = u * NT + tid;
-    if (t < na) {
-      const int32_t x = ai[u];
-      const uint32_t r = lower_bound_s(S.sBi, nb, x);
-      float v = av[u];
-      if (r < nb && S.sBi[r] == x) v = add_x86(v, S.sBv[r]);
-      const bool valid = v != 0.0f;
-      GTK_DCHECK(t + r < N);
-      uI[t + r] = valid ? x : -1;
-      uV[t + r] = v;
-      if (valid) count(x, v);
-    }
-    if (t < nb) {
-      const int32_t x = in.bi[u];
-      const uint32_t r = upper_bound_s(S.sAi, na, x);
-      const bool valid = !(r > 0 && S.sAi[r - 1] == x) && in.bv[u] != 0.0f;
-      GTK_DCHECK(t + r < N);
-      uI[t + r] = valid ? x : -1;
-      uV[t + r] = in.bv[u];
-      if (valid) count(x, in.bv[u]);
-    }
+  {
+    const uint32_t per = (N + NT - 1) / NT, s_lo = min(N, tid * per), s_hi = min(N, s_lo + per);
+    union_by_path(S.sAi, S.sAv, na, S.sBi, S.sBv, nb, s_lo, s_hi, -1, -1, 0.0f,
+                  [&](uint32_t sl, int32_t x, float v, bool valid) {
+                    GTK_DCHECK(sl < N);
+                    uI[sl] = valid ? x : -1;
+                    uV[sl] = v;
+                    if (valid) count(x, v);
+                  });
   }
   my_valid = warp_sum(my_valid);
   if (lane_id() == 0 && my_valid) atomicAdd(&S.s_valid, my_valid);
@@ -751,51 +777,27 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
         prevA = ((uint32_t)(pax >> 32) == a.a_tag && (uint32_t)(pay >> 32) == a.a_tag) ? (int32_t)(uint32_t)pax
                                                                                         : a_index(a, ia - 1);
       __syncthreads();
-      for (uint32_t t = threadIdx.x; t < la; t += kMergeThreads) {
-        const int32_t x = S.sAi[t];
-        const uint32_t r = lower_bound_s(S.sBi, lb, x);
-        float v = S.sAv[t];
-        if (r < lb) {
-          if (S.sBi[r] == x) v = add_x86(v, S.sBv[r]);
-        } else if (nextB == x) {
-          v = add_x86(v, nextBv);
-        }
-        const uint32_t slot = sub + t + r;
-        const bool valid = v != 0.0f;
-        GTK_DCHECK(slot >= d0 && slot < d1 && (!in_smem || slot - d0 < a.slice_cap));
-        if (in_smem) {
-          slice_idx[slot - d0] = valid ? x : -1;
-          slice_val[slot - d0] = v;
-        } else {
-          a.u_idx[slot] = valid ? x : -1;
-          a.u_val[slot] = v;
-        }
-        if (valid) {
-          ++my_valid;
-          const uint32_t key = merge_key_of(v);
-          if (key >= win_lo) atomicAdd(&esm.hist[min((uint32_t)kBins, (key - win_lo) >> win_shift)], 1u);
-        }
-      }
-      for (uint32_t t = threadIdx.x; t < lb; t += kMergeThreads) {
-        const int32_t x = S.sBi[t];
-        const uint32_t r = upper_bound_s(S.sAi, la, x);
-        const bool dup = r > 0 ? (S.sAi[r - 1] == x) : (prevA == x);
-        const float v = S.sBv[t];
-        const uint32_t slot = sub + t + r;
-        const bool valid = !dup && v != 0.0f;
-        GTK_DCHECK(slot >= d0 && slot < d1 && (!in_smem || slot - d0 < a.slice_cap));
-        if (in_smem) {
-          slice_idx[slot - d0] = valid ? x : -1;
-          slice_val[slot - d0] = v;
-        } else {
-          a.u_idx[slot] = valid ? x : -1;
-          a.u_val[slot] = v;
-        }
-        if (valid) {
-          ++my_valid;
-          const uint32_t key = merge_key_of(v);
-          if (key >= win_lo) atomicAdd(&esm.hist[min((uint32_t)kBins, (key - win_lo) >> win_shift)], 1u);
-        }
+      {
+        const uint32_t L = la + lb, per = (L + kMergeThreads - 1) / kMergeThreads;
+        const uint32_t s_lo = min(L, threadIdx.x * per), s_hi = min(L, s_lo + per);
+        union_by_path(S.sAi, S.sAv, la, S.sBi, S.sBv, lb, s_lo, s_hi, prevA, nextB, nextBv,
+                      [&](uint32_t sl, int32_t x, float v, bool valid) {
+                        const uint32_t slot = sub + sl;
+                        GTK_DCHECK(slot >= d0 && slot < d1 && (!in_smem || slot - d0 < a.slice_cap));
+                        if (in_smem) {
+                          slice_idx[slot - d0] = valid ? x : -1;
+                          slice_val[slot - d0] = v;
+                        } else {
+                          a.u_idx[slot] = valid ? x : -1;
+                          a.u_val[slot] = v;
+                        }
+                        if (valid) {
+                          ++my_valid;
+                          const uint32_t key = merge_key_of(v);
+                          if (key >= win_lo)
+                            atomicAdd(&esm.hist[min((uint32_t)kBins, (key - win_lo) >> win_shift)], 1u);
+                        }
+                      });
       }
       __syncthreads();
     }
