@@ -364,9 +364,14 @@ def run_b200(args, rank, world):
         opt.gtopk_step(st2, ep, pinned[i % 2], k, P)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_fallbacks = 0
     e0.record()
     for i in range(args.steps):
         rep = opt.gtopk_step(st2, ep, pinned[i % 2], k, P)
+        e2e_fallbacks += bool(st2._bufs.get("last_status", 0) & 0x2)  # (host int: no device work)
+        if os.environ.get("GTK_E2E_DEBUG") and i < 8:
+            print(f"e2e step {i}: status 0x{st2._bufs.get('last_status', 0):x} "
+                  f"window {st2._window.cpu().numpy().tolist()}", file=sys.stderr, flush=True)
     e1.record()
     e1.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
@@ -421,7 +426,7 @@ def run_b200(args, rank, world):
                 "nvlink_floor_us_per_round": round(16 * k / 900e3, 3),
                 "note": "per round: push + partner flag + merge (+ K3 after the last round); latency-bound"},
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": 4 * m,
-                    "d2h_bytes_per_step": 8},
+                    "d2h_bytes_per_step": 8, "dense_fallback_steps": e2e_fallbacks},
             "gpu_launches": gpu_launches,
             "kernels_per_step": pipe.kernels_per_step,
             "clocks": clocks,

@@ -1241,6 +1241,11 @@ __global__ void __launch_bounds__(kFinishThreads, GTK_FINISH_MIN_BLOCKS) select_
   dout.prev_tau = dout.prev_tau2 = 0u;
   engine_run<kFinishThreads>(dsrc, s0, s1, a.k, false, 0u, 20u, nullptr, false, a.ews, sm, dout, G);
   if (blk == 0) reset_select_counters(a, G);
+  // the record's k-th-key estimate: the exact k-th key (this thread wrote it
+  // as the count's hint) instead of the edge of its 2^20-key bin -- a coarse
+  // estimate would read as a jump of the k-th key two calls later and push
+  // that window's lower edge far down (overflow, another fallback, ...)
+  if (a.window && blk == 0 && threadIdx.x == 0) a.window[4] = (uint32_t)a.d_count[1];
 }
 
 }  // namespace gtk

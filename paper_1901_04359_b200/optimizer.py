@@ -308,8 +308,17 @@ def _select_checked(state, g, k, sel: DeviceList, status, fused_update: bool = F
         state._settle()
         win = state._window = _dev.new_window(g.device)  # this residual's key window (K1 hint)
     if fused_update:
+        # chained (no sampling kernel, the window carried in `win`) once a
+        # window is established; the first step and every step after an exact
+        # dense fallback run the sampled form instead -- a window recorded by
+        # the dense pass (2^20-key bins) can admit millions of keys of a
+        # flat-topped residual, overflow again and never recover
+        chain = not state._bufs.get("window_cold", True)
+        if not chain:
+            state._settle()
         _dev.select_update(state._res, g, state._res2, k, sel, status[0:1], win, state._w,
-                           float(np.float32(state.lr)), 1, _scaling_code(state), chain=True)
+                           float(np.float32(state.lr)), 1, _scaling_code(state), chain=chain)
+        state._bufs["chained"] = chain
     else:
         state._settle()
         _dev.select(state._res, g, state._res2, k, sel, status[0:1], window=win)
@@ -355,9 +364,12 @@ def gtopk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float =
         tm.mark(1)
         tm.mark(2)
         word, gnnz = _finish(state, sel.n)
+        state._bufs["window_cold"] = bool(word & (_lib.DEV_FALLBACK | _lib.DEV_ERROR_MASK))
         _dev.raise_status(word)
         state._commit(swap_residual=True)
-        state._pending = (sel, state._window)  # this step's winners, pending in the new residual
+        # a chained step's winners stay pending in the new residual (settled on
+        # the fly by the next chained step); the sampled form zeroed them
+        state._pending = (sel, state._window) if state._bufs["chained"] else None
         return StepReport(loss=loss, t_compute_ms=t_compute_ms, t_compress_ms=tm.ms(0, 1),
                           t_communicate_ms=tm.ms(1, 2), selected_k=gnnz)
     _select_checked(state, g, k, sel, status)

@@ -210,6 +210,37 @@ def test_pipeline_steady_state_no_fallback(gk):
     assert int(pipe.status.item()) & 0x2 == 0, "steady-state select used the dense fallback"
 
 
+def test_public_step_after_steady_state_no_fallback(gk):
+    """The public gtopk_step continuing a steady-state (flat-topped) residual
+    -- bench.py's e2e order: the pipeline's residual, then the API with its
+    own, fresh key window.  Its first step runs the sampled select (no carried
+    window yet); every later step stays on the fast chained path.  (A window
+    recorded by the exact dense pass -- 2^20-key bins -- used to admit the
+    flat top's millions of keys, overflow and fall back on every call.)"""
+    import torch
+
+    from paper_1901_04359_b200 import optimizer as opt
+    from paper_1901_04359_b200.pipeline import GTopKPipeline
+
+    d = torch.device("cuda", 0)
+    m, k = 2_000_000, 2000
+    gen = torch.Generator(device=d).manual_seed(6)
+    grads = [torch.randn(m, device=d, generator=gen) for _ in range(2)]
+    ep = gk.create_local_cluster(1)[0]
+    st = opt.make_state(torch.zeros(m, device=d), lr=0.01)
+    pipe = GTopKPipeline(ep, st, k, grads)
+    pipe.capture()
+    pipe.run(4000)
+    pipe.check()
+    pipe.sync_state()
+    falls = []
+    for i in range(40):
+        rep = opt.gtopk_step(st, ep, grads[i % 2], k, 1)
+        assert rep.selected_k == k
+        falls.append(bool(st._bufs["last_status"] & 0x2))
+    assert not any(falls[1:]), falls
+
+
 def test_top_op_golden(gk):
     z = load_golden("top_op.npz")
     for c in range(int(z["n"])):

@@ -91,7 +91,7 @@ def run(P, mode, k, calls, rank=0, deferred=False):
         mb = 32 + 16 * s
         names = ["m.start", "m.path", "m.slots", "m.hist_bar", "m.engine_end", "bin", "gather_bar", "ranked",
                  "written"]
-        if os.environ.get("GTK_MERGE_SOLO", "1") != "0" and k <= 2048 and not trace[mb + 7]:
+        if os.environ.get("GTK_MERGE_SOLO", "1") != "0" and k <= 2048 and os.environ.get("GTK_MERGE_GRID", "1") == "1":
             # one-CTA merge_solo stamps: start, loaded, union, selected, written,
             # bin found, gathered, ranked; diagnostics [10..12] = bin, in_bin, above
             names = ["m.start", "m.loaded", "m.union", "m.selected", "m.written", "s.bin", "s.gathered", "s.ranked"]

@@ -46,3 +46,15 @@ t0 = time.perf_counter()
 for i in range(30):
     pinned[i % 2].is_pinned()
 print("is_pinned: %.1f us" % ((time.perf_counter() - t0) / 30 * 1e6))
+
+# the same with bench.py's nvidia-smi clock sampler running beside it
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import bench  # noqa: E402
+
+smp = bench.ClockSampler(0)
+smp.start()
+time.sleep(0.5)
+print("gtopk_step pinned grads, sampler on: %.3f ms (wall %.3f)" % ev_time(lambda i: opt.gtopk_step(st, ep, pinned[i % 2], k, 1)))
+print("h2d copy_, sampler on: %.3f ms (wall %.3f)" % ev_time(lambda i: buf.copy_(pinned[i % 2], non_blocking=True)))
+print("gtopk_step device grads, sampler on: %.3f ms (wall %.3f)" % ev_time(lambda i: opt.gtopk_step(st, ep, dev_g[i % 2], k, 1)))
+smp.stop(0, 1e18)
