@@ -258,7 +258,8 @@ __device__ void engine_hist(const Src& src, uint32_t s0, uint32_t s1, uint32_t l
 template <int NT>
 __device__ bool engine_find_bin(const uint32_t* hist, bool in_smem, uint32_t t, EngineSmem<NT>& sm,
                                 uint32_t& bin, uint32_t& above, uint32_t& in_bin, uint32_t t2 = 0,
-                                uint32_t t3 = 0, uint32_t* bin2 = nullptr, uint32_t* bin3 = nullptr) {
+                                uint32_t t3 = 0, uint32_t* bin2 = nullptr, uint32_t* bin3 = nullptr,
+                                uint32_t* above2 = nullptr) {
   constexpr int PER = (kHistLen + NT - 1) / NT;
   // thread t owns reversed positions [t*PER, t*PER+PER): rb = 0 is OVER (bin 2048)
   uint32_t c[PER];
@@ -289,7 +290,10 @@ __device__ bool engine_find_bin(const uint32_t* hist, bool in_smem, uint32_t t, 
     uint32_t acc = pre;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-      if (acc < t2 && acc + c[j] >= t2) sm.bcast[5] = kBins - (threadIdx.x * PER + j);
+      if (acc < t2 && acc + c[j] >= t2) {
+        sm.bcast[5] = kBins - (threadIdx.x * PER + j);
+        sm.bcast[3] = acc;  // (entries above rank t2's bin)
+      }
       if (acc < t3 && acc + c[j] >= t3) sm.bcast[6] = kBins - (threadIdx.x * PER + j);
       acc += c[j];
     }
@@ -300,6 +304,7 @@ __device__ bool engine_find_bin(const uint32_t* hist, bool in_smem, uint32_t t, 
   in_bin = sm.bcast[2];
   if (bin2) *bin2 = sm.bcast[5];
   if (bin3) *bin3 = sm.bcast[6];
+  if (above2) *above2 = sm.bcast[3];
   __syncthreads();
   return tot >= t && bin != 0xFFFFFFFFu;
 }
@@ -629,6 +634,13 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
   uint32_t t = kt;
   const uint32_t* hist = hist0;
   bool hsm = hist0_smem;
+  // a select's window recorded with no k-th-key history (the exact dense
+  // pass): when the next window's lower rank t2 lies in the k-th key's bin,
+  // its edge is refined with every refinement round (t2r = its rank inside
+  // the current range; 0 = not tracked) -- one 2^20-key bin of a flat-topped
+  // residual can hold millions of keys, and a window opening at its edge
+  // overflows on every later call
+  uint32_t t2r = 0;
   for (int r = 0; r < kRounds; ++r) {
     if (hist == nullptr) {
       engine_hist<NT>(src, s0, s1, lo, hi, shift, solo ? nullptr : ws->hist[r], sm);
@@ -643,10 +655,12 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
       // accumulated residual moves slowly from step to step, so next time
       // about that many candidates pass lo' (a miss costs one exact dense
       // fallback and raises L)
-      uint32_t b2, b3;
+      uint32_t b2, b3, a2 = 0;
       const uint64_t t2w = (uint64_t)kt + (((uint64_t)kt << out.window_level) >> out.window_rank_shift);
       const uint32_t t2 = (uint32_t)min(t2w, (uint64_t)0xFFFFFFFFu), t3 = max(1u, kt / 2);
-      if (!engine_find_bin<NT>(hist, hsm, t, sm, bin, above, in_bin, t2, t3, &b2, &b3)) return false;
+      if (!engine_find_bin<NT>(hist, hsm, t, sm, bin, above, in_bin, t2, t3, &b2, &b3, &a2)) return false;
+      if (out.window_rank_shift == 1 && out.prev_tau == 0u && out.prev_tau2 == 0u && b2 == bin && t2 > a2)
+        t2r = t2 - a2;
       if (blk == 0 && threadIdx.x == 0) {
         uint64_t lo_n = lo, hi_n = hi;
         if (b2 != 0xFFFFFFFFu) lo_n = (uint64_t)lo + ((uint64_t)b2 << shift);
@@ -697,6 +711,20 @@ __device__ bool engine_run(const Src& src, uint32_t s0, uint32_t s1, uint32_t kt
         out.next_window[5] = p1;
         out.next_window[0] = kRecValid | (out.window_level << 8);
       }
+    } else if (t2r != 0) {
+      uint32_t b2, a2 = 0;
+      if (!engine_find_bin<NT>(hist, hsm, t, sm, bin, above, in_bin, t2r, 0u, &b2, nullptr, &a2)) return false;
+      if (b2 != 0xFFFFFFFFu && b2 < (uint32_t)kBins && blk == 0 && threadIdx.x == 0) {
+        // raise the recorded lower edge to rank t2's (finer) bin, same upper end
+        const uint64_t lo_r = (uint64_t)lo + ((uint64_t)b2 << shift);
+        const uint64_t lo_w = out.next_window[1], hi_w = lo_w + ((uint64_t)kBins << out.next_window[2]);
+        if (lo_r > lo_w && lo_r < hi_w) {
+          out.next_window[1] = (uint32_t)lo_r;
+          const uint64_t width = hi_w - lo_r;
+          out.next_window[2] = width <= (uint64_t)kBins ? 0u : ceil_log2_u64((width + kBins - 1) / kBins);
+        }
+      }
+      t2r = (b2 == bin && t2r > a2) ? t2r - a2 : 0u;
     } else if (!engine_find_bin<NT>(hist, hsm, t, sm, bin, above, in_bin)) {
       return false;
     }

@@ -241,6 +241,42 @@ def test_public_step_after_steady_state_no_fallback(gk):
     assert not any(falls[1:]), falls
 
 
+def test_dense_fallback_window_recovers(gk, dev):
+    """Chained selects on a steady-state (flat-topped) residual starting from
+    an empty key window: the first call takes the exact dense fallback, whose
+    recorded window (edge refined inside the k-th key's 2^20-key bin) keeps
+    every later call on the fast path -- no fallback loop."""
+    import torch
+
+    from paper_1901_04359_b200 import optimizer as opt
+    from paper_1901_04359_b200.pipeline import GTopKPipeline
+
+    d = torch.device("cuda", 0)
+    m, k = 25_600_000, 25_600  # the headline size: ~10K steps grow the flat top (0.6 s of pipeline)
+    gen = torch.Generator(device=d).manual_seed(7)
+    grads = [torch.randn(m, device=d, generator=gen) for _ in range(2)]
+    ep = gk.create_local_cluster(1)[0]
+    st = opt.make_state(torch.zeros(m, device=d), lr=0.01)
+    pipe = GTopKPipeline(ep, st, k, grads)
+    pipe.capture()
+    pipe.run(10_000)
+    pipe.check()
+    pipe.sync_state()
+    R = [st._res, st._res2]
+    w = st._w
+    win = dev.new_window(d)
+    sel = dev.DeviceList(m, k, d)
+    status = torch.zeros(1, dtype=torch.int32, device=d)
+    falls = []
+    for i in range(12):
+        status.zero_()
+        dev.select_update(R[i % 2], grads[i % 2], R[1 - i % 2], k, sel, status, win, w, 0.01, 1, 0, chain=True)
+        word = int(status.item())
+        assert word & 0x3D == 0, hex(word)
+        falls.append(bool(word & 0x2))
+    assert falls[0] and not any(falls[1:]), falls
+
+
 def test_top_op_golden(gk):
     z = load_golden("top_op.npz")
     for c in range(int(z["n"])):
