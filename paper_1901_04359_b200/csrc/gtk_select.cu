@@ -823,21 +823,38 @@ constexpr uint32_t kFixWas = 1u, kFixNow = 2u;  // fix-list flags: a candidate b
 // after the copy.  Returns the fix-list length (*n_ins: new candidates);
 // raises the overflow flag (exact dense fallback over the corrected res_out)
 // if the lists do not fit.
+// The words the correction starts from, loaded right after griddepcontrol.wait
+// in one round trip together with the non-finite check (they are independent:
+// loading them inside deferred_fixup put two more dependent round trips ahead
+// of the next pass's release)
+struct FixupPre {
+  uint32_t lo, shift, n_prev, ep32, ofs0, ofs_b;
+};
+__device__ __forceinline__ FixupPre fixup_preload(const FinishArgs& a) {
+  FixupPre p;
+  p.lo = __ldcg(&a.ctl->lo);
+  p.shift = __ldcg(&a.ctl->shift);
+  p.n_prev = (uint32_t)max(__ldcg(a.prev_count), 0);
+  p.ep32 = a.prev_epoch ? (uint32_t)__ldcg((const unsigned long long*)a.prev_epoch) : 0u;
+  p.ofs0 = a.prev_ofs ? __ldcg(a.prev_ofs) : 0u;
+  const uint32_t b = blockIdx.x + threadIdx.x;  // (threads 0 / 1: my range's ends)
+  p.ofs_b = (a.prev_ofs && threadIdx.x < 2 && b < gridDim.x) ? __ldcg(a.prev_ofs + 1 + b) : 0xFFFFFFFFu;
+  return p;
+}
+
 __device__ uint32_t deferred_fixup(const FinishArgs& a, EngineSmem<kFinishThreads>& sm, int32_t* f_idx, float* f_val,
-                                   uint32_t* f_flag, uint32_t t0, uint32_t t1, uint32_t* n_ins_out) {
-  const uint32_t lo = __ldcg(&a.ctl->lo), shift = __ldcg(&a.ctl->shift);
-  const uint32_t n_prev = min((uint32_t)max(__ldcg(a.prev_count), 0), a.m);
-  const uint32_t ep32 = a.prev_epoch ? (uint32_t)__ldcg((const unsigned long long*)a.prev_epoch) : 0u;
+                                   uint32_t* f_flag, uint32_t t0, uint32_t t1, uint32_t* n_ins_out,
+                                   const FixupPre& pre) {
+  const uint32_t lo = pre.lo, shift = pre.shift;
+  const uint32_t n_prev = min(pre.n_prev, a.m);
+  const uint32_t ep32 = pre.ep32;
   const int32_t E0 = (int32_t)min((uint64_t)t0 * kTile, (uint64_t)a.m);
   const int32_t E1 = (int32_t)min((uint64_t)t1 * kTile, (uint64_t)a.m);
   // my range of the previous selection: its finish recorded every block's
   // first output position (same tile partition), else two warp searches
-  const bool have_ofs = a.prev_ofs && __ldcg(a.prev_ofs) == gridDim.x;
+  const bool have_ofs = a.prev_ofs && pre.ofs0 == gridDim.x;
   if (have_ofs) {
-    if (threadIdx.x < 2) {
-      const uint32_t b = blockIdx.x + threadIdx.x;
-      sm.bcast[threadIdx.x] = b < gridDim.x ? min(__ldcg(a.prev_ofs + 1 + b), n_prev) : n_prev;
-    }
+    if (threadIdx.x < 2) sm.bcast[threadIdx.x] = min(pre.ofs_b, n_prev);  // (past the last block: n_prev)
   } else if (warp_id() < 2) {
     const uint32_t j = lower_bound_warp(a.prev_idx, n_prev, warp_id() == 0 ? E0 : E1);
     if (lane_id() == 0) sm.bcast[warp_id()] = j;
@@ -1012,6 +1029,8 @@ __global__ void __launch_bounds__(kFinishThreads, GTK_FINISH_MIN_BLOCKS) select_
   const uint32_t wlevel = (a.window && blk == 0) ? min(kMaxWindowLevel, max(kMinWindowLevel, __ldcg(a.window) >> 8)) : kMinWindowLevel;
   const bool wsame = a.window && blk == 0 && __ldcg(a.window + 3) == a.k;
   const uint32_t wtau = wsame ? __ldcg(a.window + 4) : 0u, wtau2 = wsame ? __ldcg(a.window + 5) : 0u;
+  FixupPre fpre{};
+  if (fixing) fpre = fixup_preload(a);
   if (const uint32_t bad = __ldcg(&a.ctl->nonfinite)) {
     grid_sync(&a.ews->bar, G);  // every block has read the counters
     if (blk == 0) {
@@ -1064,7 +1083,7 @@ __global__ void __launch_bounds__(kFinishThreads, GTK_FINISH_MIN_BLOCKS) select_
   uint32_t* f_flag = reinterpret_cast<uint32_t*>(f_val + a.fix_cap);
   uint32_t n_fix = 0, n_ins = 0;
   if (fixing) {
-    n_fix = deferred_fixup(a, sm, f_idx, f_val, f_flag, t0, t1, &n_ins);
+    n_fix = deferred_fixup(a, sm, f_idx, f_val, f_flag, t0, t1, &n_ins, fpre);
     if (a.trace && blk == 0 && threadIdx.x == 0) {  // diagnostics (block 0's fix list)
       a.trace[14] = n_fix;
       a.trace[15] = n_ins;
