@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
         m.o_val = a.acc_val;
         m.d_no = a.d_acc_n;
         m.trace = a.trace ? a.trace + 32 + 16 * s : nullptr;
+        m.trace_arrive = a.trace ? a.trace + 104 + 2 * s : nullptr;
         return m;
       };
       // one-CTA merge: every record this thread may read (k at most) and its

@@ -101,6 +101,9 @@ struct MergeArgs {
   uint64_t* ll_body = nullptr;
   uint64_t* ll_head = nullptr;
   uint32_t ll_tag = 0;
+  // diagnostics (nullable): [0] latest block arrival at the histogram
+  // barrier (atomicMax of %globaltimer), [1] block 0's arrival
+  int64_t* trace_arrive = nullptr;
 };
 
 // entry i of A (plain list or polled LL records)
@@ -817,6 +820,11 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
       if (c) atomicAdd(&a.ews->hist[0][b], c);
     }
     if (threadIdx.x == 0 && S.s_valid) atomicAdd(&a.ctl->n_valid, S.s_valid);
+    if (a.trace_arrive && threadIdx.x == 0) {
+      const uint64_t tnow = globaltimer_ns();
+      atomicMax((unsigned long long*)a.trace_arrive, (unsigned long long)tnow);
+      if (blk == 0) a.trace_arrive[1] = (int64_t)tnow;
+    }
     grid_sync(&a.ews->bar, G);
     // the global histogram -> shared memory by async copies, landing while
     // the valid count is read: the engine's bin search then needs no second

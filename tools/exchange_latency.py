@@ -97,6 +97,9 @@ def run(P, mode, k, calls, rank=0, deferred=False):
             names = ["m.start", "m.loaded", "m.union", "m.selected", "m.written", "s.bin", "s.gathered", "s.ranked"]
             phases[f"s{s}"]["diag"] = trace[mb + 10:mb + 13]
         phases[f"s{s}"].update({n: us(trace[mb + i]) for i, n in enumerate(names) if trace[mb + i]})
+        if s < 4 and trace[104 + 2 * s]:  # histogram-barrier arrivals: the latest block, block 0
+            phases[f"s{s}"]["arr.last"] = us(trace[104 + 2 * s])
+            phases[f"s{s}"]["arr.blk0"] = us(trace[105 + 2 * s])
     return {"P": P, "mode": mode, "k": k, "us_median": round(statistics.median(times), 2),
             "us_min": round(min(times), 2), "grid": os.environ.get("GTK_MERGE_GRID", "auto"),
             "cluster": os.environ.get("GTK_MERGE_CLUSTER", "auto"), "phases": phases}
