@@ -117,7 +117,10 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   // and forward the poison, so every rank fails the step and K3 is skipped.
   const bool self_poison = (__ldcg(a.d_status) & GTK_DEV_NONFINITE) != 0;
   const bool tr = a.trace && blk == 0 && threadIdx.x == 0;
-  if (tr) a.trace[0] = (int64_t)globaltimer();
+  if (tr) {
+    a.trace[0] = (int64_t)globaltimer();
+    a.trace[120] = (int64_t)clock64();  // (with [121]: the SM clock over the call)
+  }
 
   bool k3_fused = false;  // the final merge applied the w update (deferred steps)
   // the step whose receive writes the final global list into acc (K3's tags)
@@ -337,7 +340,10 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   }
   if (blk == 0 && threadIdx.x == 0) {
     *a.d_epoch = epoch;
-    if (tr) a.trace[1] = (int64_t)globaltimer();
+    if (tr) {
+      a.trace[1] = (int64_t)globaltimer();
+      a.trace[121] = (int64_t)clock64();
+    }
   }
 }
 

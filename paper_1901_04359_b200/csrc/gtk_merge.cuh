@@ -701,6 +701,7 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
       }
     }
   }
+#ifndef GTK_MERGE_TRACE_FINE
   if (a.trace && blk == 0 && threadIdx.x == 0) {  // window used (diagnostics)
     a.trace[14] = win_lo;
     a.trace[15] = win_shift;
@@ -708,6 +709,7 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
     a.trace[11] = rec_tau;
     a.trace[12] = rec_tau2;
   }
+#endif
   for (int b = threadIdx.x; b < kHistLen; b += kMergeThreads) esm.hist[b] = 0;
   if (threadIdx.x == 0) S.s_valid = 0;
   if (blk == 0 && threadIdx.x < kRounds) a.ews->gather_n[threadIdx.x] = 0;  // read only after a barrier
@@ -780,6 +782,9 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
         prevA = ((uint32_t)(pax >> 32) == a.a_tag && (uint32_t)(pay >> 32) == a.a_tag) ? (int32_t)(uint32_t)pax
                                                                                         : a_index(a, ia - 1);
       __syncthreads();
+#ifdef GTK_MERGE_TRACE_FINE
+      if (j == 0) merge_stamp(a, 10);  // (diagnostic build: first sub-chunk staged)
+#endif
       {
         const uint32_t L = la + lb, per = (L + kMergeThreads - 1) / kMergeThreads;
         const uint32_t s_lo = min(L, threadIdx.x * per), s_hi = min(L, s_lo + per);
@@ -803,6 +808,10 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
                       });
       }
       __syncthreads();
+#ifdef GTK_MERGE_TRACE_FINE
+      if (j == 0) merge_stamp(a, 11);  // (first sub-chunk's union done)
+      if (j + 1 == nsub) merge_stamp(a, 12);
+#endif
     }
   }
   my_valid = warp_sum(my_valid);

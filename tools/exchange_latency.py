@@ -86,6 +86,8 @@ def run(P, mode, k, calls, rank=0, deferred=False):
     t0 = trace[0]
     us = lambda v: round((v - t0) / 1e3, 2) if v else None  # noqa: E731
     phases = {"end": us(trace[1])}
+    if trace[121] and trace[1] > t0:  # SM clock of block 0's SM over the call
+        phases["sm_mhz"] = round((trace[121] - trace[120]) / ((trace[1] - t0) / 1e3), 1)
     for s in range(lb.nsteps):
         phases[f"s{s}"] = {"hdr": us(trace[3 + 4 * s]), "merge": us(trace[4 + 4 * s]), "bar": us(trace[5 + 4 * s])}
         mb = 32 + 16 * s
@@ -97,6 +99,9 @@ def run(P, mode, k, calls, rank=0, deferred=False):
             names = ["m.start", "m.loaded", "m.union", "m.selected", "m.written", "s.bin", "s.gathered", "s.ranked"]
             phases[f"s{s}"]["diag"] = trace[mb + 10:mb + 13]
         phases[f"s{s}"].update({n: us(trace[mb + i]) for i, n in enumerate(names) if trace[mb + i]})
+        if os.environ.get("GTK_TRACE_FINE"):  # a GTK_MERGE_TRACE_FINE build: staged / union 0 / union last
+            phases[f"s{s}"].update({n: us(trace[mb + 10 + i]) for i, n in enumerate(["f.staged0", "f.union0",
+                                                                                      "f.union_last"])})
         if s < 4 and trace[104 + 2 * s]:  # histogram-barrier arrivals: the latest block, block 0
             phases[f"s{s}"]["arr.last"] = us(trace[104 + 2 * s])
             phases[f"s{s}"]["arr.blk0"] = us(trace[105 + 2 * s])
