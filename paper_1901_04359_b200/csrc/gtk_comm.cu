@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(kMergeThreads) exchange_kernel(ExchangeArgs a)
   if (deferred) pdl_launch_dependents();
   pdl_wait();  // launched programmatically behind the select
   if (!deferred) pdl_launch_dependents();
+  grid_sync_begin(&a.merge.ews->bar);
   // every block reads the counter before anyone advances it (block 0 does so
   // after the final grid barrier)
   const uint64_t epoch = __ldcg((const unsigned long long*)a.d_epoch) + 1;

@@ -198,10 +198,22 @@ __device__ __forceinline__ bool ld_ll_pair(const uint64_t* p, uint32_t tag, cons
   return true;
 }
 
-// one 64-bit word: arrival count (low half) and generation (high half)
-struct __align__(8) GridBarrier {
-  uint32_t count;
-  uint32_t gen;
+// Grid barrier over three rotating arrival counters: barrier instance i of a
+// launch sends its arrivals (red.release, no return trip) to ctr[i % 3] and
+// polls it (ld.acquire) until all G blocks are in; block 0, once past
+// instance i, clears ctr[(i + 2) % 3] -- the counter of instance i - 1, which
+// every block has stopped polling, and of instance i + 2, which nobody can
+// reach before block 0's next (release) arrival -- and records i + 1 in
+// `next`, where the next launch on this barrier starts (read by every block
+// at its start, grid_sync_begin; block 0 writes it only after every block has
+// arrived, i.e. started).  Invariant between launches: ctr[next] =
+// ctr[next + 1] = 0.  Measured (tools/probe/lat_probe.cu, 100 blocks): 2.3K
+// cycles per barrier vs 3.4K for a {count, generation} word whose last
+// arriver bumps the generation behind its returning acq_rel arrival.
+// (GTK_GRID_BAR_GEN=1 builds that protocol instead, for A/B.)
+struct __align__(16) GridBarrier {
+  uint32_t ctr[3];
+  uint32_t next;
 };
 
 __device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v) {
@@ -230,15 +242,15 @@ __device__ __forceinline__ uint64_t ld_acquire_gpu_u64(const uint64_t* p) {
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void red_add_release_gpu_u32(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
-// Thread 0 arrives with one acq_rel atomic on the {count, gen} word
-// (cumulative over the block's writes through the preceding bar.sync): the
-// returned word carries both the generation and the arrival rank, so arrival
-// is a single round trip.  The last arriver resets the count and advances the
-// generation with one more release add; the others acquire the new
-// generation; bar.sync then extends the ordering to the whole block.
-// Cross-block data is read with ld.global.cg.
-//
 // A grid that is one thread-block cluster (cluster-mode merges) synchronises
 // with barrier.cluster instead: release/acquire at cluster scope orders the
 // blocks' global-memory writes too, and no global word is touched.
@@ -250,6 +262,33 @@ __device__ __forceinline__ uint32_t cluster_ncta() {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+
+// a grid barrier that has not completed after kGridSyncTrapNs (a peer block
+// that can never arrive) traps: the launch fails with an error instead of
+// spinning forever
+constexpr uint64_t kGridSyncTrapNs = 20ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ uint64_t grid_sync_now() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void grid_sync_check_stall(uint64_t& t0) {
+  const uint64_t now = grid_sync_now();
+  if (t0 == 0) t0 = now;
+  else if (now - t0 > kGridSyncTrapNs) __trap();
+}
+
+// this block's next barrier instance (mod 3), thread 0 only
+__device__ __forceinline__ uint32_t& grid_sync_inst() {
+  __shared__ uint32_t s_inst;
+  return s_inst;
+}
+// every kernel that may call grid_sync with G > 1 calls this first (after its
+// griddepcontrol.wait: the previous launch on the barrier must be complete)
+__device__ __forceinline__ void grid_sync_begin(const GridBarrier* b) {
+  if (threadIdx.x == 0) grid_sync_inst() = __ldcg(&b->next) % 3u;
+}
+
 __device__ __forceinline__ void grid_sync(GridBarrier* b, unsigned nblocks) {
   if (nblocks == 1) {
     __syncthreads();
@@ -261,18 +300,35 @@ __device__ __forceinline__ void grid_sync(GridBarrier* b, unsigned nblocks) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    uint64_t* word = reinterpret_cast<uint64_t*>(b);
+#if defined(GTK_GRID_BAR_GEN) && GTK_GRID_BAR_GEN
+    // {count, generation} in ctr[0..1]: the last arriver (known from its
+    // returning acq_rel arrival) resets the count and advances the generation
+    uint64_t* word = reinterpret_cast<uint64_t*>(b->ctr);
     const uint64_t old = atom_add_acq_rel_gpu_u64(word, 1ull);
     const uint32_t g = (uint32_t)(old >> 32);
     if ((uint32_t)old == nblocks - 1) {
-      // count -> 0, gen -> g + 1: a non-returning release add -- the last
-      // arriver (the block everyone waits for) does not wait for its round trip
       red_add_release_gpu_u64(word, (1ull << 32) - nblocks);
     } else {
-      uint32_t spins = 0;
-      while ((uint32_t)(ld_acquire_gpu_u64(word) >> 32) == g)
-        if (++spins > 64) __nanosleep(20);
+      uint64_t t0 = 0;
+      for (uint32_t spins = 1; (uint32_t)(ld_acquire_gpu_u64(word) >> 32) == g; ++spins)
+        if ((spins & 1023u) == 0) grid_sync_check_stall(t0);
     }
+#else
+    uint32_t& inst = grid_sync_inst();
+    const uint32_t i = inst;
+    GTK_DCHECK(i < 3u);
+    uint32_t* c = &b->ctr[i];
+    red_add_release_gpu_u32(c, 1u);
+    uint64_t t0 = 0;
+    for (uint32_t spins = 1; ld_acquire_gpu_u32(c) < nblocks; ++spins)
+      if ((spins & 1023u) == 0) grid_sync_check_stall(t0);
+    const uint32_t nx = i == 2u ? 0u : i + 1u;
+    inst = nx;
+    if (blockIdx.x == 0) {
+      b->ctr[nx == 2u ? 0u : nx + 1u] = 0u;  // ctr[(i + 2) % 3]
+      b->next = nx;
+    }
+#endif
   }
   __syncthreads();
 }

@@ -17,6 +17,7 @@ template <bool kSolo>
 __global__ void __launch_bounds__(kMergeThreads, 1) merge_kernel(MergeArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   MergeSmem& S = *reinterpret_cast<MergeSmem*>(dsm);
+  grid_sync_begin(&a.ews->bar);
   const uint32_t na = (uint32_t)__ldcg(a.d_na), nb = (uint32_t)__ldcg(a.d_nb);
   const uint32_t ha = (uint32_t)__ldcg(a.d_na + 1), hb = (uint32_t)__ldcg(a.d_nb + 1);
   merge_device<kSolo>(a, na, nb, ha, hb, gridDim.x, S);

@@ -1021,6 +1021,7 @@ __global__ void __launch_bounds__(kFinishThreads, GTK_FINISH_MIN_BLOCKS) select_
   float* s_val = reinterpret_cast<float*>(s_dyn + sizeof(int32_t) * a.slice_cap);
   const unsigned G = gridDim.x, blk = blockIdx.x;
   pdl_wait();  // launched programmatically behind the main pass
+  grid_sync_begin(&a.ews->bar);
   // (a deferred call with a previous selection releases the next call's main
   // pass once that selection is corrected in res_out, below)
   const bool fixing = a.defer && a.prev_idx != nullptr;

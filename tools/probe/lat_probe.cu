@@ -83,6 +83,46 @@ __global__ void gridbar_kernel(Bar* bar, long long* out, int reps) {
   if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = (clock64() - t0) / reps;
 }
 
+// {count, gen} barrier variants (the repo's protocol = mode 0):
+//   0: atom.add.acq_rel arrival; last: red.release gen bump; others: ld.acquire poll (+ nanosleep after 64 spins)
+//   1: as 0 without the nanosleep
+//   2: as 1, the last arriver bumps gen with red.relaxed (its acq_rel arrival already ordered everything)
+//   3: atom.add.release arrival; last: fence.acquire + red.relaxed bump; others: ld.acquire poll
+template <int kMode>
+__global__ void genbar_kernel(Bar* bar, long long* out, int reps) {
+  __syncthreads();
+  long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint64_t* word = reinterpret_cast<uint64_t*>(bar);
+      uint64_t old;
+      if (kMode == 3)
+        asm volatile("atom.add.release.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(word), "l"(1ull) : "memory");
+      else
+        asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(word), "l"(1ull) : "memory");
+      const unsigned g = (unsigned)(old >> 32);
+      if ((unsigned)old == gridDim.x - 1) {
+        if (kMode <= 1) {
+          asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(word), "l"((1ull << 32) - gridDim.x) : "memory");
+        } else {
+          if (kMode == 3) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(word), "l"((1ull << 32) - gridDim.x) : "memory");
+        }
+      } else {
+        uint64_t v;
+        unsigned spins = 0;
+        do {
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(word) : "memory");
+          if (kMode == 0 && ++spins > 64) __nanosleep(20);
+        } while ((unsigned)(v >> 32) == g);
+      }
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = (clock64() - t0) / reps;
+}
+
 // barrier variants over a monotonic arrival counter (zeroed before the launch):
 // barrier r completes when the counter reaches G * (r + 1)
 //   mode 1: red.release arrival, ld.acquire poll
@@ -179,6 +219,18 @@ int main() {
     cudaMemcpy(h, out, 8, cudaMemcpyDeviceToHost);
     printf("gridbar G=%3d  cycles per barrier %lld\n", G, h[0]);
   }
+  auto gen_run = [&](auto kern, int mode) {
+    for (int G : {2, 32, 100}) {
+      cudaMemset(bar, 0, sizeof(Bar));
+      kern<<<G, 512>>>(bar, out, 200);
+      cudaMemcpy(h, out, 8, cudaMemcpyDeviceToHost);
+      printf("genbar mode %d G=%3d  cycles per barrier %lld\n", mode, G, h[0]);
+    }
+  };
+  gen_run(genbar_kernel<0>, 0);
+  gen_run(genbar_kernel<1>, 1);
+  gen_run(genbar_kernel<2>, 2);
+  gen_run(genbar_kernel<3>, 3);
   unsigned* ctr;
   cudaMalloc(&ctr, 4096);
   auto ctr_run = [&](auto kern, int mode) {
