@@ -908,18 +908,26 @@ __device__ uint32_t deferred_fixup(const FinishArgs& a, EngineSmem<kFinishThread
     n_fix += tot;
     n_ins += block_sum<kFinishThreads>((now && !was) ? 1u : 0u, sm.scan);
   }
-  for (int b = threadIdx.x; b < kHistLen; b += kFinishThreads) {  // (block_sum above synced sm.hist)
+  *n_ins_out = n_ins;
+  return n_fix;  // (the histogram moves stay in sm.hist for deferred_fixup_publish)
+}
+
+// The fixup's effects on this finish's own bookkeeping -- the histogram moves
+// (sm.hist), the new candidates of my tile range, the overflow flag -- after
+// the next pass has been released: it reads none of them (it works in the
+// other select workspace), and the grid barrier that follows orders them
+// before this finish reads them.
+__device__ void deferred_fixup_publish(const FinishArgs& a, EngineSmem<kFinishThreads>& sm, uint32_t n_fix,
+                                       uint32_t n_ins) {
+  for (int b = threadIdx.x; b < kHistLen; b += kFinishThreads) {  // (block_sum in the fixup synced sm.hist)
     const uint32_t dlt = sm.hist[b];
     if (dlt) atomicAdd(a.ews->hist[0] + b, dlt);  // (mod 2^32: negative moves wrap)
   }
-  const uint32_t own_raw = __ldcg(a.group_cnt + blockIdx.x);
   if (threadIdx.x == 0) {
     if (n_ins) atomicAdd(a.group_cnt + blockIdx.x, n_ins);
     if (n_fix > a.fix_cap || n_ins > (uint32_t)kGatherCap)
       atomicOr(&a.ctl->overflow, 1u);  // lists too long: exact dense fallback (res_out is corrected)
   }
-  *n_ins_out = n_ins;
-  return min(n_fix, a.fix_cap);
 }
 
 // The fix list applied to the staged slice (index order, own_raw entries):
@@ -1089,9 +1097,16 @@ __global__ void __launch_bounds__(kFinishThreads, GTK_FINISH_MIN_BLOCKS) select_
       a.trace[14] = n_fix;
       a.trace[15] = n_ins;
     }
+#ifdef GTK_FIXUP_PUBLISH_EARLY  // (A/B: the round-2 order, bookkeeping ahead of the release)
+    deferred_fixup_publish(a, sm, n_fix, n_ins);
+#endif
     __threadfence();  // res_out corrections visible before the next main pass is released
     __syncthreads();
     pdl_launch_dependents();
+#ifndef GTK_FIXUP_PUBLISH_EARLY
+    deferred_fixup_publish(a, sm, n_fix, n_ins);
+#endif
+    n_fix = min(n_fix, a.fix_cap);
     grid_sync(&a.ews->bar, G);
     finish_stamp(a, 20);  // (diagnostics: fixup + barrier done)
   }
