@@ -41,6 +41,15 @@ constexpr int kMainThreads = 256;
 constexpr int kMainVec = 4;                                  // float4 per thread per array
 constexpr int kTile = kMainThreads * kMainVec * 4;          // 4096 elements
 constexpr int kMainTilesPerBlock = 2;                      // tiles loaded up front by one main-pass block
+// main pass loads: 0 = float4 register loads (default), 1 = bulk copies (TMA)
+// of the block's tiles into 64 KB of shared memory on one mbarrier.  The bulk
+// form frees ~24 registers per thread but measured slower on the same box
+// (profiles/r2_main_tma_ab.txt: main pass alone 53.0 -> 54.2 us, N = 1 step
+// 61.9 -> 65.1 us, N = 2 75.1 -> 79.4): kept as an A/B switch
+#ifndef GTK_MAIN_TMA
+#define GTK_MAIN_TMA 0
+#endif
+constexpr size_t kMainStageBytes = GTK_MAIN_TMA ? (size_t)kMainTilesPerBlock * 2 * kTile * sizeof(float) : 0;
 constexpr int kMainDenseHist = 48;                          // candidates per tile above which the histogram goes via smem
 constexpr int kSampleThreads = 1024;
 constexpr int kSampleChunk = kSampleThreads;                // 1024 elements per chunk (one per thread)
@@ -615,6 +624,27 @@ __global__ void __launch_bounds__(kMainThreads, 3) select_main_kernel(MainArgs a
   if (a.trace && blk == 0 && threadIdx.x == 0) a.trace[0] = (int64_t)globaltimer_ns();
   const uint32_t t0 = blk < a.n2 ? 2 * blk : a.n2 + blk;
   const uint32_t ntile = blk < a.n2 ? 2u : 1u;
+#if GTK_MAIN_TMA
+  // the full tiles' gradient and residual by the bulk-copy engine into shared
+  // memory (64 KB per block in flight without a register each: a block that
+  // shares its SM with a finish or exchange block still streams at depth),
+  // one mbarrier for all of them
+  extern __shared__ __align__(128) float4 s_stage[];  // [tile][grad | res][kTile / 4]
+  __shared__ __align__(8) uint64_t s_mbar;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_mbar, 1);
+    uint32_t bytes = 0;
+    for (uint32_t u = 0; u < ntile; ++u)
+      if ((uint64_t)(t0 + u + 1) * kTile <= a.m) bytes += (a.res ? 2u : 1u) * kTile * 4u;
+    mbar_arrive_expect_tx(&s_mbar, bytes);
+    for (uint32_t u = 0; u < ntile; ++u) {
+      const uint64_t tbase = (uint64_t)(t0 + u) * kTile;
+      if (tbase + kTile > a.m) break;
+      bulk_g2s_stream(s_stage + (2 * u) * (kTile / 4), a.grad + tbase, kTile * 4u, &s_mbar);
+      if (a.res) bulk_g2s_stream(s_stage + (2 * u + 1) * (kTile / 4), a.res + tbase, kTile * 4u, &s_mbar);
+    }
+  }
+#else
   float4 gv[kMainTilesPerBlock][kMainVec], rv[kMainTilesPerBlock][kMainVec];
 #pragma unroll
   for (int u = 0; u < kMainTilesPerBlock; ++u) {
@@ -628,6 +658,7 @@ __global__ void __launch_bounds__(kMainThreads, 3) select_main_kernel(MainArgs a
       }
     }
   }
+#endif
   // the dense-tile histogram, cleared while the loads are in flight (the
   // first tile's barrier orders it before any use)
   for (int b = threadIdx.x; b < kHistLen; b += kMainThreads) s_hist[b] = 0u;
@@ -665,6 +696,10 @@ __global__ void __launch_bounds__(kMainThreads, 3) select_main_kernel(MainArgs a
     shift = __ldcg(&a.ctl->shift);
   }
   bool any_dense = false;
+#if GTK_MAIN_TMA
+  __syncthreads();  // (the mbarrier's initialisation before anyone waits on it)
+  mbar_wait_parity(&s_mbar, 0);
+#endif
 #pragma unroll
   for (int u = 0; u < kMainTilesPerBlock; ++u) {
     const uint32_t tile = t0 + u;
@@ -675,9 +710,17 @@ __global__ void __launch_bounds__(kMainThreads, 3) select_main_kernel(MainArgs a
     if (full) {
 #pragma unroll
       for (int q = 0; q < kMainVec; ++q) {
+#if GTK_MAIN_TMA
+        float4 x = s_stage[(2 * u) * (kTile / 4) + q * kMainThreads + threadIdx.x];
+#else
         float4 x = gv[u][q];
+#endif
         if (a.res) {
+#if GTK_MAIN_TMA
+          float4 r = s_stage[(2 * u + 1) * (kTile / 4) + q * kMainThreads + threadIdx.x];
+#else
           float4 r = rv[u][q];
+#endif
           // (chained: one max-key test per 4 elements; a pending winner is in
           // ~k/m of them)
           if (kChain && pend &&
@@ -1289,8 +1332,16 @@ using namespace gtk;
 
 // main-pass grid: two tiles per block, except that about one wave of resident
 // blocks at the end of the grid takes one tile each (a shorter drain)
+static bool main_smem_ready() {
+  if (kMainStageBytes == 0) return true;
+  return ensure_dyn_smem((const void*)select_main_kernel<kMainPlain>, kMainStageBytes) &&
+         ensure_dyn_smem((const void*)select_main_kernel<kMainChain>, kMainStageBytes) &&
+         ensure_dyn_smem((const void*)select_main_kernel<kMainDefer>, kMainStageBytes);
+}
+
 static uint32_t main_grid(uint32_t ntiles, uint32_t* n2) {
-  const int slots = coop_grid((const void*)select_main_kernel<kMainPlain>, kMainThreads, 0);  // resident blocks, all SMs
+  if (!main_smem_ready()) return 0;
+  const int slots = coop_grid((const void*)select_main_kernel<kMainPlain>, kMainThreads, kMainStageBytes);  // resident blocks, all SMs
   if (slots <= 0) return 0;
   uint32_t n1 = std::min<uint32_t>(ntiles, (uint32_t)slots);
   uint32_t two = (ntiles - n1) / 2;
@@ -1524,7 +1575,7 @@ static int select_impl(const float* res_in, const float* grad, float* res_out, i
     ma.trace = trace_buffer() ? trace_buffer() + 112 : nullptr;
     auto* mk = defer ? select_main_kernel<kMainDefer>
                      : (chain ? select_main_kernel<kMainChain> : select_main_kernel<kMainPlain>);
-    GTK_CUDA(launch_pdl(mk, dim3(gmain), dim3(kMainThreads), 0, st, ma));
+    GTK_CUDA(launch_pdl(mk, dim3(gmain), dim3(kMainThreads), kMainStageBytes, st, ma));
     GTK_CHECK_LAUNCH();
   }
 
@@ -1607,7 +1658,7 @@ extern "C" int gtk_select_main_pass(const float* res_in, const float* grad, floa
   const uint32_t gmain = main_grid(L.ntiles, &ma.n2);
   if (gmain == 0) return GTK_ECUDA;
   for (int r = 0; r < reps; ++r) {
-    select_main_kernel<kMainPlain><<<gmain, kMainThreads, 0, st>>>(ma);
+    select_main_kernel<kMainPlain><<<gmain, kMainThreads, kMainStageBytes, st>>>(ma);
     GTK_CHECK_LAUNCH();
   }
   // the repeated passes accumulated histogram / counter state: clear it
