@@ -4,7 +4,7 @@
 # of the deferred main pass / finish in their steady state, of the exchange kernel
 # (loopback, k = 25.6K and 270) and of the standalone merge, plus timelines.
 set -u
-OUT=gpurun_out/prof_r2
+OUT=${OUT:-gpurun_out/prof_r2}
 mkdir -p $OUT
 python bench.py --steps 200 --warmup 20 > $OUT/bench_n1.json 2> $OUT/bench_n1.err
 # launch list: 300 preconditioning steps (2 launches each) + capture, then the timed steps
