@@ -424,7 +424,7 @@ def run_b200(args, rank, world):
                                  if stage.get("exchange") else None),
                 # k LL records of 16 B (idx|tag, value|tag) per round over 900 GB/s NVLink 5
                 "nvlink_floor_us_per_round": round(16 * k / 900e3, 3),
-                "note": "per round: push + partner flag + merge (+ K3 after the last round); latency-bound"},
+                "note": "per round: LL records pushed by the partner + merge (+ K3 after the last round); latency-bound"},
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": 4 * m,
                     "d2h_bytes_per_step": 8, "dense_fallback_steps": e2e_fallbacks},
             "gpu_launches": gpu_launches,

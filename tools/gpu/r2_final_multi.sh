@@ -1,7 +1,7 @@
 # four GPUs: the multi-GPU suite, N = 2 / 4 bench lines (default deferred and the
 # non-deferred step), sweeps with the reference-protocol rows, N = 2 timeline
 nvidia-smi -L
-OUT=gpurun_out/final_multi
+OUT=${OUT:-gpurun_out/final_multi}
 mkdir -p $OUT
 python -m pytest tests/test_gpu_dist.py -q 2>&1 | tail -3 > $OUT/dist.txt
 for n in 2 4; do
