@@ -664,3 +664,35 @@ def test_deferred_select_update_trajectory(dev, kind):
         dev.settle(settled, sels[par], wins[par].clone())
         assert np.array_equal(settled.cpu().numpy().view(np.uint32), ref.residual.view(np.uint32)), (kind, t)
         prev = (gi, gv)
+
+
+def test_grid_barrier_across_launches_of_varying_grids(gk, monkeypatch):
+    """The rotating-counter grid barrier (gtk_common.cuh grid_sync) keeps its
+    between-launch invariant on one shared merge workspace while consecutive
+    launches use different grid sizes (GTK_MERGE_GRID, read per call) and
+    different numbers of barrier instances: keep-all unions (1 barrier),
+    windowed selects (2), and window misses through cancellation (the
+    full-range retry: 5).  Every result is checked against the oracle; a
+    broken invariant shows as a hang (the barrier traps after 20 s) or a
+    wrong list."""
+    from oracle import gtopk_oracle as orc
+
+    rng = np.random.default_rng(77)
+    m, k = 200_000, 20_000
+    grids = ["100", "37", "2", "64", "1", "148", "3", "100"]
+    for rep in range(3):
+        for j, g in enumerate(grids):
+            monkeypatch.setenv("GTK_MERGE_GRID", g)
+            monkeypatch.setenv("GTK_MERGE_CLUSTER", "0")
+            kind = (rep + j) % 3
+            ga = rng.standard_normal(m).astype(F32)
+            gb = rng.standard_normal(m).astype(F32)
+            if kind == 1:
+                gb[: m // 3] = -ga[: m // 3]  # cancellation on a third of the shared indices
+            ai, av, _ = orc.top_k_select(ga, k)
+            bi, bv, _ = orc.top_k_select(gb, k)
+            kk = 3 * k if kind == 2 else k  # kind 2: the union holds <= kk entries (keep-all)
+            wi, wv = orc.top_op(ai, av, bi, bv, kk)
+            o = gk.top_op(gk.SparseVector(m, ai, av), gk.SparseVector(m, bi, bv), kk)
+            assert np.array_equal(o.indices, wi), (rep, g, kind)
+            assert np.array_equal(o.values.view(np.uint32), wv.view(np.uint32)), (rep, g, kind)
