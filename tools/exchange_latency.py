@@ -25,7 +25,7 @@ import torch  # noqa: E402
 import test_gpu_exchange_loopback as lbt  # noqa: E402
 
 
-def run(P, mode, k, calls, rank=0, deferred=False):
+def run(P, mode, k, calls, rank=0, deferred=False, thrash_mb=0):
     rng = np.random.default_rng(11 + k)
     m = max(1_000_000, 20 * k)
     lists = lbt._lists(rng, P, m, k, "normal")
@@ -40,6 +40,7 @@ def run(P, mode, k, calls, rank=0, deferred=False):
     # every call's inbox words, built once (tag = call number)
     words = {}
     tr = torch.zeros(256, dtype=torch.int64, device=d)
+    thrash = torch.zeros(thrash_mb * 262144, device=d) if thrash_mb else None
     times = []
     trace = None
     for call in range(calls):
@@ -65,6 +66,8 @@ def run(P, mode, k, calls, rank=0, deferred=False):
         st = lb.dv.stream_of(d)  # torch's current stream: the events below see the kernel
         # the GPU is kept busy (SM clocks up) and the start event lands after the
         # spin, with the exchange launch already queued behind it
+        if thrash is not None:
+            thrash.add_(1.0)  # stream a buffer larger than L2 through it (evicts the kernel's code lines)
         torch.cuda._sleep(400_000)
         e0.record()
         rc = lb.lib.gtk_gtopk_exchange_update(*args, P_(w), P_(None if deferred else res), ctypes.c_float(0.01), 0,
@@ -115,11 +118,12 @@ def main():
     ap.add_argument("--k", type=int, nargs="+", default=[270, 25600])
     ap.add_argument("--P", type=int, nargs="+", default=[2, 4])
     ap.add_argument("--calls", type=int, default=30)
+    ap.add_argument("--thrash-mb", type=int, default=0, help="stream this many MB through L2 before each call")
     ap.add_argument("--deferred", action="store_true", help="res = NULL: the deferred step's exchange (compact grid)")
     a = ap.parse_args()
     for P in a.P:
         for k in a.k:
-            r = run(P, "butterfly", k, a.calls, deferred=a.deferred)
+            r = run(P, "butterfly", k, a.calls, deferred=a.deferred, thrash_mb=a.thrash_mb)
             r["deferred"] = a.deferred
             print(json.dumps(r), flush=True)
 
