@@ -851,25 +851,36 @@ static __device__ __forceinline__ void merge_device(const MergeArgs& a, uint32_t
            a.upd_w, a.upd_lr, a.upd_Pf, a.upd_scaling, a.tag, a.tag_val,
            a.ll_body, a.ll_head, a.ll_tag};
   out.upd_skip = a.upd_skip;
-  bool ok = engine_run<kMergeThreads>(src, d0, d1, keep_all ? n_valid : a.k, keep_all, win_lo, win_shift, esm.hist,
-                                      true, a.ews, esm, out, G);
-  merge_stamp(a, 4);  // engine done
-  if (a.trace && rec && blk == 0 && threadIdx.x == 0) a.trace[13] = __ldcg(rec + 1);
-  if (!ok) {  // the window missed (hint: cancellation; carried: a shift): full key range
-    if (rec && blk == 0 && threadIdx.x == 0) {
-      rec[0] = min(4u, rec_level + 1) << 8;  // invalid, wider margin next time
-      rec[4] = rec[5] = 0u;
-    }
-    if (!solo) {
-      grid_sync(&a.ews->bar, G);
-      if (blk == 0) {
-        for (int r = 0; r < kRounds; ++r)
-          for (int b = threadIdx.x; b < kHistLen; b += kMergeThreads) a.ews->hist[r][b] = 0;
-        if (threadIdx.x < kRounds) a.ews->gather_n[threadIdx.x] = 0;
+  // one engine call site for both attempts (the window, then -- if it missed
+  // through cancellation or a shifted carried window -- the full key range):
+  // a single inlined copy of the engine keeps the kernel's code compact (its
+  // phases run once per call; instruction fetch is a large share of its stalls)
+  bool ok = false;
+#pragma unroll 1
+  for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+    const bool first = attempt == 0;
+    if (!first) {
+      if (rec && blk == 0 && threadIdx.x == 0) {
+        rec[0] = min(4u, rec_level + 1) << 8;  // invalid, wider margin next time
+        rec[4] = rec[5] = 0u;
       }
-      grid_sync(&a.ews->bar, G);
+      if (!solo) {
+        grid_sync(&a.ews->bar, G);
+        if (blk == 0) {
+          for (int r = 0; r < kRounds; ++r)
+            for (int b = threadIdx.x; b < kHistLen; b += kMergeThreads) a.ews->hist[r][b] = 0;
+          if (threadIdx.x < kRounds) a.ews->gather_n[threadIdx.x] = 0;
+        }
+        grid_sync(&a.ews->bar, G);
+      }
     }
-    engine_run<kMergeThreads>(src, d0, d1, a.k, false, 0u, 20u, nullptr, false, a.ews, esm, out, G);
+    const bool ka = first && keep_all;
+    ok = engine_run<kMergeThreads>(src, d0, d1, ka ? n_valid : a.k, ka, first ? win_lo : 0u, first ? win_shift : 20u,
+                                   first ? esm.hist : nullptr, first, a.ews, esm, out, G);
+    if (first) {
+      merge_stamp(a, 4);  // engine done
+      if (a.trace && rec && blk == 0 && threadIdx.x == 0) a.trace[13] = __ldcg(rec + 1);
+    }
   }
   // every block read n_valid before the engine's first barrier
   if (!solo && blk == 0 && threadIdx.x == 0) a.ctl->n_valid = 0;
