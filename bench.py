@@ -32,6 +32,7 @@ from __future__ import annotations
 import argparse
 import ctypes
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -309,9 +310,13 @@ def run_b200(args, rank, world):
     dbg = bool(os.environ.get("GTK_PROF_DEBUG"))
     if dbg:
         print(f"[rank {rank}] after timed loop: status=0x{int(pipe.status.item()):x}", flush=True)
-    # keep the GPU busy until the clock sampler has seen it under load
-    soak_end = time.monotonic() + 0.5
-    while time.monotonic() < soak_end:
+    # keep the GPU busy until the clock sampler has seen it under load: ~0.5 s
+    # of pipeline steps -- the SAME number on every rank (each step is a
+    # collective; a wall-clock loop let ranks run different counts, and the
+    # extra steps' exchanges then waited out their peers' timeouts)
+    n_soak = max(1, int(math.ceil(500.0 / max(elapsed / args.steps * 20, 1e-3))))
+    n_soak = int(max_over_ranks(n_soak))
+    for _ in range(n_soak):
         pipe.run(20)
         torch.cuda.synchronize(dev)
     t_clk1 = time.monotonic()
@@ -455,6 +460,10 @@ def main():
                     help="untimed steps that build the residual up to its steady state")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if os.environ.get("GTK_HANG_DUMP"):  # diagnostics: every thread's Python stack after N s, to stderr
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(os.environ["GTK_HANG_DUMP"]), exit=False)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":

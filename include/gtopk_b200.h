@@ -330,7 +330,7 @@ int gtk_gtopk_exchange(int32_t rank, int32_t P, const int32_t* schedule, int32_t
  *   res = NULL: the deferred step (gtk_select_push_deferred) -- no residual
  *   restore (the local winners stay pending for the next select's settle),
  *   the next kernel in the stream may launch at once (it is the next step's
- *   HBM pass), and the merges run on 32 blocks per merge round when the
+ *   HBM pass), and the merges run on 32 blocks (+24 per further merge round) when the
  *   union fits their shared memory, leaving the rest of the GPU to that pass. */
 int gtk_gtopk_exchange_update(int32_t rank, int32_t P, const int32_t* schedule, int32_t nsteps,
                               void* const* peer_inbox, uint64_t* d_epoch,

@@ -514,11 +514,14 @@ static int exchange_impl(int32_t rank, int32_t P, const int32_t* schedule, int32
                       (int32_t*)(base + L.u_idx), (float*)(base + L.u_val)};
   MergeGrid g;
   // deferred (no residual): the exchange runs beside the next step's HBM pass
-  // on 32 blocks per merge round (measured best: N = 2 32 blocks 78.1 us/step,
-  // 24: 83.3, 40: 79.8; N = 4 64 blocks 95.0, 48: 99.3, 80: 101.9, 100: 112.3)
+  // on 32 blocks for one merge round and 24 more per further round (measured
+  // with the rotating-counter grid barrier, profiles/r2_compact_grid_sweep.txt:
+  // N = 2 32 blocks 75.3 us/step, 24: 77.9, 40: 76.5, 16: 83.5; N = 4 56 blocks
+  // 87.7, 48: 89.3, 64: 90.6, 40: 92.6, 32: 98.7, 80: 97.9 -- the earlier
+  // {count, generation} barrier's slower rounds wanted 64 at N = 4)
   int merges = 0;
   for (int s = 0; s < nsteps; ++s) merges += schedule[4 * s + 2] ? 1 : 0;
-  const int compact_g = (upd_w && !upd_res) ? 32 * std::max(1, merges) : 0;
+  const int compact_g = (upd_w && !upd_res) ? 32 + 24 * (std::max(1, merges) - 1) : 0;
   if (!merge_grid_for((const void*)exchange_kernel<false>, k, &g, compact_g)) return GTK_ECUDA;
   const void* fn = merge_use_solo(g, k) ? (const void*)exchange_kernel<true> : (const void*)exchange_kernel<false>;
   if (!ensure_dyn_smem(fn, merge_smem_bytes(kMergeSliceCapMax))) return GTK_ECUDA;
