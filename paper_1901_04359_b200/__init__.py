@@ -8,8 +8,10 @@ running as hand-written sm_100a kernels behind a C ABI (libgtopk_b200.so).
 
 Every hot-path name of the reference's top level is exported here.  The
 collective and optimizer names are resolved on first use (they import
-torch); the reference's `cost_model` / `models` re-exports and its TCP mesh
-are outside this package's scope.
+torch); the reference's TCP mesh (`ClusterConfig`, `connect_tcp_cluster`) is
+`tcp.py`, with the collectives staged through host bytes onto this host's
+GPU.  The reference's `cost_model` / `models` re-exports are outside this
+package's scope.
 """
 
 from .sparse import (
@@ -36,6 +38,7 @@ from .transport import (
     encode_sparse,
     run_workers,
 )
+from .tcp import ClusterConfig, TcpEndpoint, connect_tcp_cluster, load_hosts_file
 
 __version__ = "1.1.0"
 
@@ -67,7 +70,8 @@ __all__ = sorted(
         "FLOAT", "INDEX", "DeviceSparseVector", "IndexMask", "SparseVector", "as_dense", "densify",
         "k_from_density", "masked_extract", "top_k_select", "top_op", "DEFAULT_TIMEOUT", "Endpoint",
         "ProtocolError", "TransportError", "TransportStats", "create_local_cluster", "decode_sparse",
-        "encode_sparse", "run_workers",
+        "encode_sparse", "run_workers", "ClusterConfig", "TcpEndpoint", "connect_tcp_cluster",
+        "load_hosts_file",
     ]
     + list(_LAZY)
 )
