@@ -446,6 +446,10 @@ def dense_step(state: OptimizerState, ep, grad, P: int, *, loss: float = 0.0,
     if rank_order_sum:
         # allgather + rank-order accumulation (optimizer.py:108-115)
         total = _coll.rank_order_dense_sum(ep, g)
+    elif ep.world_size == 1:
+        # one rank: the ring allreduce is the identity (collectives.py:97-98
+        # returns a copy); the update only reads it, so no copy is made
+        total = g
     else:
         total = _coll.dense_ring_allreduce(ep, g)
     t_comm = (time.perf_counter() - t0) * 1e3
