@@ -127,3 +127,33 @@ def test_tcp_gtopk_step_trajectory_vs_oracle(P, momentum):
     for r in range(P):
         assert np.array_equal(bits(outs[r][0]), bits(ref[r].weights)), r
         assert np.array_equal(bits(outs[r][1]), bits(ref[r].residual)), r
+
+
+def test_tcp_local_backend_equivalence_bitwise():
+    """reference pkg/tests/test_transport.py:255-298: identical inputs through
+    the in-process and the TCP backends give identical results for every
+    collective -- and identical byte / message accounting."""
+    import paper_1901_04359_b200 as gk
+    from paper_1901_04359_b200 import collectives as coll
+
+    rng = np.random.default_rng(21)
+    P, m, k = 3, 24, 3
+    sparse_in = sparse_lists(rng, P, m, k)
+    dense_in = [rng.standard_normal(m).astype(F32) for _ in range(P)]
+
+    def all_collectives(ep):
+        r = ep.rank
+        out = (coll.gtopk_allreduce(ep, sparse_in[r], k, P), coll.topk_allreduce(ep, sparse_in[r], P),
+               coll.dense_ring_allreduce(ep, dense_in[r]))
+        st = ep.stats
+        return out, (st.bytes_sent, st.bytes_recv, st.msgs_sent, st.msgs_recv)
+
+    local = gk.run_workers(gk.create_local_cluster(P), all_collectives)
+    over_tcp = run(tcp_mesh(P), all_collectives)
+    for r in range(P):
+        (g_t, t_t, d_t), s_t = over_tcp[r]
+        (g_l, t_l, d_l), s_l = local[r]
+        assert g_t.global_topk == g_l.global_topk
+        assert np.array_equal(bits(t_t), bits(t_l))
+        assert np.array_equal(bits(d_t), bits(d_l))
+        assert s_t == s_l, (r, s_t, s_l)

@@ -293,3 +293,31 @@ def test_mixed_mesh_with_reference_ranks():
     finally:
         for ep in eps:
             ep.close()
+
+
+def test_duplicate_announcement_is_protocol_error():
+    """reference pkg/tests/test_transport.py:232-253."""
+    from paper_1901_04359_b200.transport import ProtocolError
+
+    ports = free_ports(3)
+    cfg = tcp.ClusterConfig(3, "tcp", [("127.0.0.1", p) for p in ports], 5.0)
+    err = {}
+
+    def node0():
+        try:
+            tcp.connect_tcp_cluster(cfg, 0)
+        except Exception as exc:  # noqa: BLE001
+            err["exc"] = exc
+
+    t = threading.Thread(target=node0)
+    t.start()
+    time.sleep(0.2)
+    socks = []
+    for _ in range(2):  # two sockets both claim rank 1
+        s = socket.create_connection(("127.0.0.1", ports[0]), timeout=5)
+        s.sendall(struct.pack("<I", 1))
+        socks.append(s)
+    t.join(10)
+    for s in socks:
+        s.close()
+    assert isinstance(err.get("exc"), ProtocolError)
