@@ -265,6 +265,11 @@ int gtk_status_read(const int32_t* d_status, const int32_t* d_count, int32_t* h_
  * optimizer.py:108-115 summation order). srcs: device array of P pointers. */
 int gtk_dense_sum(const float* const* srcs, int32_t P, int64_t m, float* out, void* stream);
 
+/* dense sum of P device vectors in the reference's ring reduce-scatter order
+ * (collectives.py:88-128: chunk c = e / ceil(m/P) summed from rank c on),
+ * bitwise the ring allreduce's result (in-process dense baseline). */
+int gtk_dense_ring_sum(const float* const* srcs, int32_t P, int64_t m, float* out, void* stream);
+
 /* ------------------------------------------------------------------------
  * gTopKAllReduce exchange (collectives.py:188-219) over NVLink peer memory.
  * One persistent cooperative kernel per rank runs every round of the

@@ -59,6 +59,7 @@ EXPORTS = (
     "gtk_densify",
     "gtk_topk_accumulate",
     "gtk_dense_sum",
+    "gtk_dense_ring_sum",
     "gtk_divergence_terms",
     "gtk_status_read",
     "gtk_exchange_inbox_bytes",
@@ -118,6 +119,7 @@ _SIGS = {
     "gtk_densify": ([_P, _P, _P, _I64, _P, _P], _I32),
     "gtk_topk_accumulate": ([_P, _P, _P, _I32, _I64, _I64, _P, _I32, _P], _I32),
     "gtk_dense_sum": ([_P, _I32, _I64, _P, _P], _I32),
+    "gtk_dense_ring_sum": ([_P, _I32, _I64, _P, _P], _I32),
     "gtk_divergence_terms": ([_P, _P, _P, _P, _P, _P, _I64, _P, _P, _P], _I32),
     "gtk_status_read": ([_P, _P, _P, _I32, _P], _I32),
     "gtk_exchange_inbox_bytes": ([_I32, _I32, ctypes.POINTER(_SZ)], _I32),

@@ -334,7 +334,9 @@ def rank_order_sparse_sum(ep: Endpoint, local):
 
 
 def _local_dense_leader(ops, ring_stats=True):
-    """Rank-ordered sum of every rank's dense vector (one kernel).  Accounting:
+    """Sum of every rank's dense vector in one kernel: in the ring's order
+    (bitwise the reference's dense_ring_allreduce) or, with ring_stats=False,
+    in rank order from +0 (the rank-order sum).  Accounting:
     the ring allreduce's 2(P-1) chunk messages (collectives.py:101-126), or
     with ring_stats=False the allgather of whole vectors (optimizer.py:108-115)."""
     P = len(ops)
@@ -345,7 +347,7 @@ def _local_dense_leader(ops, ring_stats=True):
                 f"ring chunk size mismatch: got {4 * (-(-g.numel() // P))} bytes, expected {4 * (-(-m // P))}"
             )
     out = torch.empty(m, dtype=torch.float32, device=ops[0][1].device)
-    _dev.dense_sum([g for _ep, g in ops], m, out)
+    _dev.dense_sum([g for _ep, g in ops], m, out, ring=ring_stats)
     msgs, nbytes = (2 * (P - 1), 4 * -(-m // P)) if ring_stats else (P - 1, 4 * m)
     for ep_r, _g in ops:
         ep_r.stats.msgs_sent += msgs

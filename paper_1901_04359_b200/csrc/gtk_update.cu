@@ -192,6 +192,21 @@ __global__ void dense_sum_kernel(const float* const* srcs, int P, uint32_t m, fl
   }
 }
 
+// the reference's ring reduce-scatter order (collectives.py:119-122): element
+// e lies in chunk c = e / chunk, whose sum starts at rank c's value and takes
+// ranks c+1, c+2, ... (mod P) in turn -- bitwise the ring's result
+__global__ void dense_ring_sum_kernel(const float* const* srcs, int P, uint32_t m, uint32_t chunk, float* out) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+    const int c = (int)(e / chunk);
+    float acc = srcs[c][e];
+    for (int j = 1; j < P; ++j) {
+      const int r = c + j < P ? c + j : c + j - P;
+      acc = __fadd_rn(acc, srcs[r][e]);
+    }
+    out[e] = acc;
+  }
+}
+
 static int grid_for(uint64_t n, int threads) {
   uint64_t g = (n + threads - 1) / threads;
   const uint64_t cap = (uint64_t)num_sms() * 16;
@@ -330,6 +345,15 @@ extern "C" int gtk_status_read(const int32_t* d_status, const int32_t* d_count, 
   GTK_CUDA(cudaMemcpyAsync(h_out + 1, d_count, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   if (reset) GTK_CUDA(cudaMemsetAsync(const_cast<int32_t*>(d_status), 0, sizeof(int32_t), st));
   GTK_CUDA(cudaStreamSynchronize(st));
+  return GTK_OK;
+}
+
+extern "C" int gtk_dense_ring_sum(const float* const* srcs, int32_t P, int64_t m, float* out, void* stream) {
+  if (!srcs || !out || P < 1 || m < 1 || m >= (int64_t(1) << 31)) return GTK_EINVAL;
+  const int64_t chunk = (m + P - 1) / P;
+  dense_ring_sum_kernel<<<grid_for(m, 256), 256, 0, (cudaStream_t)stream>>>(srcs, P, (uint32_t)m, (uint32_t)chunk,
+                                                                             out);
+  GTK_CHECK_LAUNCH();
   return GTK_OK;
 }
 

@@ -330,9 +330,12 @@ def topk_accumulate(idx: torch.Tensor, val: torch.Tensor, counts: torch.Tensor, 
     )
 
 
-def dense_sum(srcs, m: int, out: torch.Tensor) -> None:
+def dense_sum(srcs, m: int, out: torch.Tensor, ring: bool = False) -> None:
+    """Sum of the P vectors: in rank order from +0 (ring=False,
+    optimizer.py:108-115) or in the ring allreduce's order (ring=True,
+    collectives.py:119-122)."""
     ptrs = torch.tensor([t.data_ptr() for t in srcs], dtype=torch.int64, device=out.device)
-    _lib.call("gtk_dense_sum", P(ptrs), len(srcs), m, P(out), stream_of(out.device))
+    _lib.call("gtk_dense_ring_sum" if ring else "gtk_dense_sum", P(ptrs), len(srcs), m, P(out), stream_of(out.device))
     # keep the pointer table alive until the kernel has consumed it
     torch.cuda.current_stream(out.device).synchronize()
 

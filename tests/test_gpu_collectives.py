@@ -216,9 +216,12 @@ def test_dense_allreduce(gk, coll):
         ins = [rng.standard_normal(m).astype(F32) for _ in range(4)]
         want = np.sum(np.stack(ins), axis=0, dtype=np.float64)
         outs = gk.run_workers(gk.create_local_cluster(4), lambda ep: coll.dense_ring_allreduce(ep, ins[ep.rank]))
-        for o in outs:
+        from oracle import gtopk_oracle as orc
+
+        ring = orc.dense_ring_allreduce(ins)  # the reference's ring order, simulated
+        for r, o in enumerate(outs):
             np.testing.assert_allclose(o, want, rtol=1e-4, atol=1e-5)
-            assert np.array_equal(bits(o), bits(outs[0]))
+            assert np.array_equal(bits(o), bits(ring[r]))  # bitwise the ring's sum
     with pytest.raises(ProtocolError):
         gk.run_workers(gk.create_local_cluster(2, timeout=5),
                        lambda ep: coll.dense_ring_allreduce(ep, np.ones([8, 12][ep.rank], F32)))
