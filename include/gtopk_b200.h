@@ -247,6 +247,15 @@ int gtk_densify(const int32_t* idx, const float* val, const int32_t* d_n, int64_
 int gtk_topk_accumulate(const int32_t* idx, const float* val, const int32_t* d_n, int32_t P,
                         int64_t stride, int64_t m, float* out, int32_t divide, void* stream);
 
+/* the topk baseline's sparse update at momentum 0 (optimizer.py:145-173 with
+ * _apply_update :92-99): the P lists (same layout as gtk_topk_accumulate)
+ * summed in rank order into `acc` (f32[m], all +0 on entry, all +0 again on
+ * return), then w[i] -= lr * (acc[i] / P if divide else acc[i]) at each
+ * touched index once -- bitwise the dense average + dense update, at P x k
+ * instead of m elements. */
+int gtk_topk_apply(const int32_t* idx, const float* val, const int32_t* d_n, int32_t P, int64_t stride, int64_t m,
+                   float* acc, float* w, float lr, int32_t divide, void* stream);
+
 /* optimizer.py:232-241 (measure_divergence) terms: pruned[i] = total[g_idx[i]] -
  * g_val[i] for the global list's entries (the reference's masked sum minus
  * densify(global) at the mask), and *d_shared = |{global indices} ∩ {naive

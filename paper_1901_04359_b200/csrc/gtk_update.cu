@@ -157,10 +157,28 @@ __global__ void scatter_add_kernel(const int32_t* idx, const float* val, const i
   }
 }
 
+// entry e of rank r is an index's first occurrence unless an earlier rank's
+// (ascending) list holds the same index: each touched index is handled by
+// exactly one thread
+__device__ __forceinline__ bool first_occurrence(const int32_t* idx, const int32_t* d_n, int32_t r, int64_t stride,
+                                                 int32_t i) {
+  for (int32_t s = 0; s < r; ++s) {
+    const int32_t* a = idx + (uint64_t)s * stride;
+    const uint32_t n = (uint32_t)__ldg(d_n + s);
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(a + mid) < i) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < n && __ldg(a + lo) == i) return false;
+  }
+  return true;
+}
+
 // out /= P at the touched entries only (untouched ones are +0 and +0 / P is
-// +0): entry e of rank r divides unless an earlier rank's (ascending) list
-// holds the same index -- each index exactly once, like the reference's dense
-// division (collectives.py:164), at P x k instead of m elements
+// +0): each index exactly once, like the reference's dense division
+// (collectives.py:164), at P x k instead of m elements
 __global__ void divide_touched_kernel(const int32_t* idx, const int32_t* d_n, int32_t P, int64_t stride, float* out,
                                       float Pf) {
   const uint64_t tot = (uint64_t)P * (uint64_t)stride;
@@ -169,18 +187,28 @@ __global__ void divide_touched_kernel(const int32_t* idx, const int32_t* d_n, in
     const uint32_t e = (uint32_t)(q % (uint64_t)stride);
     if (e >= (uint32_t)__ldg(d_n + r)) continue;
     const int32_t i = __ldg(idx + (uint64_t)r * stride + e);
-    bool first = true;
-    for (int32_t s = 0; s < r && first; ++s) {
-      const int32_t* a = idx + (uint64_t)s * stride;
-      uint32_t lo = 0, hi = (uint32_t)__ldg(d_n + s);
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(a + mid) < i) lo = mid + 1;
-        else hi = mid;
-      }
-      first = !(lo < (uint32_t)__ldg(d_n + s) && __ldg(a + lo) == i);
-    }
-    if (first) out[i] = __fdiv_rn(out[i], Pf);
+    if (first_occurrence(idx, d_n, r, stride, i)) out[i] = __fdiv_rn(out[i], Pf);
+  }
+}
+
+// the topk baseline's update at momentum 0 (optimizer.py:92-99 with the
+// averaged vector of collectives.py:158-165): w -= lr * (sum / P) at the
+// touched entries only -- untouched entries would subtract lr * +0, which
+// leaves every w bitwise unchanged -- and the rank-ordered sums in `acc` are
+// reset to +0 for the next call
+__global__ void apply_touched_kernel(const int32_t* idx, const int32_t* d_n, int32_t P, int64_t stride, float* acc,
+                                     float* w, float lr, float Pf, int divide) {
+  const uint64_t tot = (uint64_t)P * (uint64_t)stride;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < tot; q += (uint64_t)gridDim.x * blockDim.x) {
+    const int32_t r = (int32_t)(q / (uint64_t)stride);
+    const uint32_t e = (uint32_t)(q % (uint64_t)stride);
+    if (e >= (uint32_t)__ldg(d_n + r)) continue;
+    const int32_t i = __ldg(idx + (uint64_t)r * stride + e);
+    if (!first_occurrence(idx, d_n, r, stride, i)) continue;
+    float u = acc[i];
+    if (divide) u = __fdiv_rn(u, Pf);
+    w[i] = __fsub_rn(w[i], __fmul_rn(lr, u));
+    acc[i] = 0.0f;
   }
 }
 
@@ -291,6 +319,20 @@ extern "C" int gtk_topk_accumulate(const int32_t* idx, const float* val, const i
     divide_touched_kernel<<<num_sms() * 2, 256, 0, st>>>(idx, d_n, P, stride, out, (float)P);
     GTK_CHECK_LAUNCH();
   }
+  return GTK_OK;
+}
+
+extern "C" int gtk_topk_apply(const int32_t* idx, const float* val, const int32_t* d_n, int32_t P, int64_t stride,
+                              int64_t m, float* acc, float* w, float lr, int32_t divide, void* stream) {
+  if (!idx || !val || !d_n || !acc || !w || P < 1 || m < 1 || m >= (int64_t(1) << 31) || stride < 0)
+    return GTK_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int r = 0; r < P; ++r) {  // rank order 0..P-1 (collectives.py:162-163), into the all-+0 acc
+    scatter_add_kernel<<<num_sms() * 2, 256, 0, st>>>(idx + r * stride, val + r * stride, d_n + r, acc);
+    GTK_CHECK_LAUNCH();
+  }
+  apply_touched_kernel<<<num_sms() * 2, 256, 0, st>>>(idx, d_n, P, stride, acc, w, lr, (float)P, divide);
+  GTK_CHECK_LAUNCH();
   return GTK_OK;
 }
 

@@ -330,6 +330,15 @@ def topk_accumulate(idx: torch.Tensor, val: torch.Tensor, counts: torch.Tensor, 
     )
 
 
+def topk_apply(idx: torch.Tensor, val: torch.Tensor, counts: torch.Tensor, P_: int, stride: int, m: int,
+               acc: torch.Tensor, w: torch.Tensor, lr: float, divide: bool = True) -> None:
+    """gtk_topk_apply: the topk baseline's momentum-0 update from the P
+    gathered lists, at the touched entries only (acc: all-+0 f32[m] scratch,
+    left all +0)."""
+    _lib.call("gtk_topk_apply", P(idx), P(val), P(counts), P_, stride, m, P(acc), P(w), ctypes.c_float(lr),
+              1 if divide else 0, stream_of(w.device))
+
+
 def dense_sum(srcs, m: int, out: torch.Tensor, ring: bool = False) -> None:
     """Sum of the P vectors: in rank order from +0 (ring=False,
     optimizer.py:108-115) or in the ring allreduce's order (ring=True,

@@ -207,7 +207,7 @@ class DistDeviceGroup:
             _dev.scatter_update(w, res, None, plan.acc, lst, lst.dim, lr, 0.0, self.world, scaling, skip=status)
 
     # -- TopKAllReduce baseline: NCCL allgather + rank-order accumulation -----
-    def topk(self, ep: Endpoint, lst: DeviceList, divide: bool = True) -> torch.Tensor:
+    def topk(self, ep: Endpoint, lst: DeviceList, divide: bool = True, apply=None):
         """collectives.py:148-165: every rank's list (counts, then one packed
         all-gather of [idx | value bits] per rank), accumulated in rank order
         by gtk_topk_accumulate (scatter per rank, division at the touched
@@ -222,8 +222,13 @@ class DistDeviceGroup:
         mine[cap:cap + n].copy_(lst.val[:n].view(torch.int32))
         allv = torch.empty(W * 2 * cap, dtype=torch.int32, device=self.device)
         dist.all_gather_into_tensor(allv, mine)
-        out = torch.empty(lst.dim, dtype=torch.float32, device=self.device)
-        _dev.topk_accumulate(allv, allv[cap:].view(torch.float32), cnts, W, 2 * cap, lst.dim, out, divide=divide)
+        out = None
+        if apply is not None:  # (w, lr, acc): topk_step's momentum-0 update, touched entries only
+            w, lr, acc = apply
+            _dev.topk_apply(allv, allv[cap:].view(torch.float32), cnts, W, 2 * cap, lst.dim, acc, w, lr, divide)
+        else:
+            out = torch.empty(lst.dim, dtype=torch.float32, device=self.device)
+            _dev.topk_accumulate(allv, allv[cap:].view(torch.float32), cnts, W, 2 * cap, lst.dim, out, divide=divide)
         for s in range(W - 1):
             ep.stats.add_sparse(cnts[(self.rank - s) % W:(self.rank - s) % W + 1], sent=True)
             ep.stats.add_sparse(cnts[(self.rank - s - 1) % W:(self.rank - s - 1) % W + 1], sent=False)

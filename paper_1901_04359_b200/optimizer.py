@@ -421,9 +421,25 @@ def topk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float = 
     tm.mark(1)
     word = int(status[0].item())
     _dev.raise_status(word)
-    averaged = _coll.topk_allreduce(ep, DeviceSparseVector(sel), P)
-    tm.mark(2)
-    _dense_update(state, averaged)
+    if _dev.sparse_update_fusable(state.lr, state.momentum) and (P == 1 or hasattr(ep.group, "topk")):
+        # momentum 0, finite lr >= +0: the update touches only the gathered
+        # lists' indices (w - lr * +0 leaves every other weight bitwise unchanged), so the
+        # rank-ordered sums go to a persistent all-+0 scratch and the update
+        # runs at those entries (gtk_topk_apply) -- no m-wide memset / apply
+        acc = state._bufs.pop("topk_acc", None)
+        if acc is None or acc.numel() != state.m or acc.device != dev:
+            acc = torch.zeros(state.m, dtype=torch.float32, device=dev)
+        lr = float(np.float32(state.lr))
+        if P == 1:
+            _dev.topk_apply(sel.idx, sel.val, sel.n, 1, sel.cap, state.m, acc, state._w, lr, divide=True)
+        else:
+            ep.group.topk(ep, sel, divide=True, apply=(state._w, lr, acc))
+        state._bufs["topk_acc"] = acc  # (dropped above if the collective raised)
+        tm.mark(2)
+    else:
+        averaged = _coll.topk_allreduce(ep, DeviceSparseVector(sel), P)
+        tm.mark(2)
+        _dense_update(state, averaged)
     word, nnz = _finish(state, sel.n)
     _dev.raise_status(word)
     state._commit(swap_residual=True)

@@ -500,7 +500,7 @@ class HostStagedGroup:
         return blocks
 
     # -- TopKAllReduce: allgather + rank-order accumulation (collectives.py:148-165)
-    def topk(self, ep, lst, divide: bool = True):
+    def topk(self, ep, lst, divide: bool = True, apply=None):
         import torch
 
         from . import device as _dev
@@ -521,9 +521,13 @@ class HostStagedGroup:
             val[q, : s.nnz] = s.values
             cnt[q] = s.nnz
         d = self.device
+        ti, tv, tc = torch.from_numpy(idx).to(d), torch.from_numpy(val).to(d), torch.from_numpy(cnt).to(d)
+        if apply is not None:  # (w, lr, acc): topk_step's momentum-0 update, touched entries only
+            w, lr, acc = apply
+            _dev.topk_apply(ti, tv, tc, P, cap, lst.dim, acc, w, lr, divide)
+            return None
         out = torch.empty(lst.dim, dtype=torch.float32, device=d)
-        _dev.topk_accumulate(torch.from_numpy(idx).to(d), torch.from_numpy(val).to(d), torch.from_numpy(cnt).to(d),
-                             P, cap, lst.dim, out, divide=divide)
+        _dev.topk_accumulate(ti, tv, tc, P, cap, lst.dim, out, divide=divide)
         return out
 
     # -- dense ring allreduce (collectives.py:88-128): chunk adds on the GPU ----

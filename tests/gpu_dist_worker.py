@@ -103,6 +103,18 @@ def main():
     check(np.array_equal(bits(st.residual), bits(ref[r].residual)), "step residual")
     check(rep.selected_k == k, "selected_k")
 
+    # 2b. topk_step trajectories (momentum 0: the touched-entry update,
+    # gtk_topk_apply; momentum 0.9: the dense update) vs the oracle
+    for mom in (0.0, 0.9):
+        stt = opt.make_state(np.zeros(m, F32), lr=0.1, momentum=mom)
+        for it in range(steps):
+            opt.topk_step(stt, ep, grads[it][r], k, P)
+        reft = [orc.State(np.zeros(m, F32), 0.1, mom) for _ in range(P)]
+        for it in range(steps):
+            orc.topk_step_all(reft, grads[it], k)
+        check(np.array_equal(bits(stt.weights), bits(reft[r].weights)), f"topk_step weights mom={mom}")
+        check(np.array_equal(bits(stt.residual), bits(reft[r].residual)), f"topk_step residual mom={mom}")
+
     # 3. the CUDA-graph pipeline gives the same trajectory
     dev = ep.group.device
     dg = [torch.from_numpy(grads[0][r]).to(dev), torch.from_numpy(grads[1][r]).to(dev)]

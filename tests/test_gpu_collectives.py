@@ -476,3 +476,27 @@ def test_baseline_configs_vs_oracle(gk, opt, cfg):
     for r in range(P):
         assert np.array_equal(bits(outs[r][0]), bits(ref[r].weights)), (name, r)
         assert np.array_equal(bits(outs[r][1]), bits(ref[r].residual)), (name, r)
+
+
+def test_topk_step_touched_update_bitwise(gk, opt):
+    """topk_step at P = 1, momentum 0 (gtk_topk_apply: the update at the
+    selected entries only) against the oracle's dense average + dense update,
+    with -0.0 / inf / NaN weights that a dense w - lr * +0 leaves unchanged;
+    8 steps, weights and residual bitwise."""
+    from oracle import gtopk_oracle as orc
+
+    m, k, steps = 100_003, 97, 8
+    rng = np.random.default_rng(12)
+    w0 = rng.standard_normal(m).astype(F32)
+    w0[::7] = F32(-0.0)
+    w0[5::11] = np.inf
+    w0[3::13] = np.nan
+    grads = [rng.standard_normal(m).astype(F32) for _ in range(steps)]
+    (ep,) = gk.create_local_cluster(1)
+    st = opt.make_state(w0, lr=0.25)
+    ref = [orc.State(w0, 0.25)]
+    for it in range(steps):
+        opt.topk_step(st, ep, grads[it], k, 1)
+        orc.topk_step_all(ref, [grads[it]], k)
+    assert np.array_equal(bits(st.weights), bits(ref[0].weights))
+    assert np.array_equal(bits(st.residual), bits(ref[0].residual))

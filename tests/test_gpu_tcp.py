@@ -157,3 +157,30 @@ def test_tcp_local_backend_equivalence_bitwise():
         assert np.array_equal(bits(t_t), bits(t_l))
         assert np.array_equal(bits(d_t), bits(d_l))
         assert s_t == s_l, (r, s_t, s_l)
+
+
+@pytest.mark.parametrize("P,momentum", [(3, 0.0), (2, 0.9)])
+def test_tcp_topk_step_trajectory_vs_oracle(P, momentum):
+    """topk_step over the TCP mesh: momentum 0 takes the touched-entry update
+    (gtk_topk_apply), momentum 0.9 the dense one; 4 steps bitwise."""
+    from oracle import gtopk_oracle as orc
+    from paper_1901_04359_b200 import optimizer as opt
+
+    m, k, steps = 30_000, 60, 4
+    rng = np.random.default_rng(8)
+    grads = [[rng.standard_normal(m).astype(F32) for _ in range(P)] for _ in range(steps)]
+    w0 = rng.standard_normal(m).astype(F32)
+
+    def worker(ep):
+        st = opt.make_state(w0, lr=0.05, momentum=momentum)
+        for it in range(steps):
+            opt.topk_step(st, ep, grads[it][ep.rank], k, P)
+        return st.weights.copy(), st.residual.copy()
+
+    outs = run(tcp_mesh(P), worker)
+    ref = [orc.State(w0, 0.05, momentum) for _ in range(P)]
+    for it in range(steps):
+        orc.topk_step_all(ref, grads[it], k)
+    for r in range(P):
+        assert np.array_equal(bits(outs[r][0]), bits(ref[r].weights)), r
+        assert np.array_equal(bits(outs[r][1]), bits(ref[r].residual)), r
