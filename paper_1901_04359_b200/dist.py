@@ -268,9 +268,14 @@ class DistDeviceGroup:
         return out
 
     def _check_dims(self, m: int) -> None:
-        ms = [torch.zeros(1, dtype=torch.int64) for _ in range(self.world)]
-        dist.all_gather(ms, torch.tensor([m], dtype=torch.int64), group=self.gloo)
-        if any(int(x) != m for x in ms):
+        """ProtocolError on every rank when the ranks' vector lengths differ
+        (collectives.py:113-117) -- checked before the size-dependent
+        collective by one 2-element NCCL max-reduction of (m, -m), the same
+        size on every rank (in place of a gloo all-gather of m)."""
+        t = torch.tensor([m, -m], dtype=torch.int64).to(self.device, non_blocking=True)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        hi, neg_lo = t.tolist()
+        if hi != m or -neg_lo != m:
             from .transport import ProtocolError
 
             raise ProtocolError("ring chunk size mismatch across ranks")

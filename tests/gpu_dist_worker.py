@@ -115,6 +115,18 @@ def main():
         check(np.array_equal(bits(stt.weights), bits(reft[r].weights)), f"topk_step weights mom={mom}")
         check(np.array_equal(bits(stt.residual), bits(reft[r].residual)), f"topk_step residual mom={mom}")
 
+    # 2c. mismatched dense lengths raise ProtocolError on every rank
+    # (collectives.py:113-117), and the group stays usable
+    from paper_1901_04359_b200.transport import ProtocolError
+
+    try:
+        coll.dense_ring_allreduce(ep, np.ones(8 + r, F32))
+        check(False, "dense length mismatch: no ProtocolError")
+    except ProtocolError:
+        pass
+    ok = coll.dense_ring_allreduce(ep, np.full(9, r + 1.0, F32))
+    check(np.array_equal(ok, np.full(9, P * (P + 1) / 2, F32)), "dense allreduce after a mismatch")
+
     # 3. the CUDA-graph pipeline gives the same trajectory
     dev = ep.group.device
     dg = [torch.from_numpy(grads[0][r]).to(dev), torch.from_numpy(grads[1][r]).to(dev)]
