@@ -213,6 +213,26 @@ class DistDeviceGroup:
         by gtk_topk_accumulate (scatter per rank, division at the touched
         entries only)."""
         W = self.world
+        if apply is not None:
+            # topk_step (w, lr, acc): every rank's list has the same capacity
+            # (k), so one all-gather of [count | idx | value bits] per rank
+            # carries the counts too -- no host read of the sizes -- and the
+            # momentum-0 update runs at the touched entries only.  (Callers
+            # pass the same k on every rank, like every step of the job.)
+            w, lr, acc = apply
+            cap = lst.cap
+            stride = 2 * cap + 1
+            mine = torch.empty(stride, dtype=torch.int32, device=self.device)
+            mine[0:1].copy_(lst.n)
+            mine[1:1 + cap].copy_(lst.idx)
+            mine[1 + cap:].copy_(lst.val.view(torch.int32))
+            allv = torch.empty(W * stride, dtype=torch.int32, device=self.device)
+            dist.all_gather_into_tensor(allv, mine)
+            cnts = allv.view(W, stride)[:, 0].contiguous()
+            _dev.topk_apply(allv[1:], allv[1 + cap:].view(torch.float32), cnts, W, stride, lst.dim, acc, w, lr,
+                            divide)
+            self._topk_stats(ep, cnts)
+            return None
         cnts = torch.empty(W, dtype=torch.int32, device=self.device)
         dist.all_gather_into_tensor(cnts, lst.n)
         cap = max(int(cnts.max().item()), 1)  # (the gather's size: one host read)
@@ -222,17 +242,17 @@ class DistDeviceGroup:
         mine[cap:cap + n].copy_(lst.val[:n].view(torch.int32))
         allv = torch.empty(W * 2 * cap, dtype=torch.int32, device=self.device)
         dist.all_gather_into_tensor(allv, mine)
-        out = None
-        if apply is not None:  # (w, lr, acc): topk_step's momentum-0 update, touched entries only
-            w, lr, acc = apply
-            _dev.topk_apply(allv, allv[cap:].view(torch.float32), cnts, W, 2 * cap, lst.dim, acc, w, lr, divide)
-        else:
-            out = torch.empty(lst.dim, dtype=torch.float32, device=self.device)
-            _dev.topk_accumulate(allv, allv[cap:].view(torch.float32), cnts, W, 2 * cap, lst.dim, out, divide=divide)
+        out = torch.empty(lst.dim, dtype=torch.float32, device=self.device)
+        _dev.topk_accumulate(allv, allv[cap:].view(torch.float32), cnts, W, 2 * cap, lst.dim, out, divide=divide)
+        self._topk_stats(ep, cnts)
+        return out
+
+    def _topk_stats(self, ep: Endpoint, cnts: torch.Tensor) -> None:
+        """Ring-allgather accounting of the reference (collectives.py:140-144)."""
+        W = self.world
         for s in range(W - 1):
             ep.stats.add_sparse(cnts[(self.rank - s) % W:(self.rank - s) % W + 1], sent=True)
             ep.stats.add_sparse(cnts[(self.rank - s - 1) % W:(self.rank - s - 1) % W + 1], sent=False)
-        return out
 
     # -- dense baseline: NCCL allreduce (sum) -----------------------------------
     def dense(self, ep: Endpoint, g: torch.Tensor) -> torch.Tensor:
