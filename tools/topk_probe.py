@@ -51,5 +51,15 @@ res["topk_step"] = timed(lambda: opt.topk_step(state, ep, g, k, ep.world_size), 
 res["gtopk_step"] = timed(lambda: opt.gtopk_step(state, ep, g, k, ep.world_size), 20)
 if ep.rank == 0:
     print({a: round(b, 4) for a, b in res.items()}, flush=True)
+if os.environ.get("TOPK_PROFILE"):
+    from torch.profiler import ProfilerActivity, profile
+
+    with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+        for _ in range(5):
+            opt.topk_step(state, ep, g, k, ep.world_size)
+        torch.cuda.synchronize()
+    if ep.rank == 0:
+        print(prof.key_averages().table(sort_by="self_cpu_time_total", row_limit=25), flush=True)
+        print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=12), flush=True)
 ep.close()
 dist.destroy_process_group()
