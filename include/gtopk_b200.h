@@ -252,9 +252,13 @@ int gtk_topk_accumulate(const int32_t* idx, const float* val, const int32_t* d_n
  * summed in rank order into `acc` (f32[m], all +0 on entry, all +0 again on
  * return), then w[i] -= lr * (acc[i] / P if divide else acc[i]) at each
  * touched index once -- bitwise the dense average + dense update, at P x k
- * instead of m elements. */
+ * instead of m elements.  d_status (NULL = none): the P ranks' status words,
+ * status_stride int32 apart; if any carries an error bit nothing is added or
+ * applied and d_local_status (this rank's word, may be NULL) gets
+ * GTK_DEV_PEER_FAILED unless it already holds an error. */
 int gtk_topk_apply(const int32_t* idx, const float* val, const int32_t* d_n, int32_t P, int64_t stride, int64_t m,
-                   float* acc, float* w, float lr, int32_t divide, void* stream);
+                   float* acc, float* w, float lr, int32_t divide, const int32_t* d_status, int64_t status_stride,
+                   int32_t* d_local_status, void* stream);
 
 /* optimizer.py:232-241 (measure_divergence) terms: pruned[i] = total[g_idx[i]] -
  * g_val[i] for the global list's entries (the reference's masked sum minus

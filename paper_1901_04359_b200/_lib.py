@@ -119,7 +119,7 @@ _SIGS = {
     "gtk_dense_apply": ([_P, _P, _P, _I64, _F, _F, _I32, _P], _I32),
     "gtk_densify": ([_P, _P, _P, _I64, _P, _P], _I32),
     "gtk_topk_accumulate": ([_P, _P, _P, _I32, _I64, _I64, _P, _I32, _P], _I32),
-    "gtk_topk_apply": ([_P, _P, _P, _I32, _I64, _I64, _P, _P, _F, _I32, _P], _I32),
+    "gtk_topk_apply": ([_P, _P, _P, _I32, _I64, _I64, _P, _P, _F, _I32, _P, _I64, _P, _P], _I32),
     "gtk_dense_sum": ([_P, _I32, _I64, _P, _P], _I32),
     "gtk_dense_ring_sum": ([_P, _I32, _I64, _P, _P], _I32),
     "gtk_divergence_terms": ([_P, _P, _P, _P, _P, _P, _I64, _P, _P, _P], _I32),

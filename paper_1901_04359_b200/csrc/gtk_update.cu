@@ -196,8 +196,35 @@ __global__ void divide_touched_kernel(const int32_t* idx, const int32_t* d_n, in
 // touched entries only -- untouched entries would subtract lr * +0, which
 // leaves every w bitwise unchanged -- and the rank-ordered sums in `acc` are
 // reset to +0 for the next call
+// any of the P status words (stride `sstride`) carries an error bit: the
+// step is void on every rank (nothing is added or applied)
+__device__ __forceinline__ bool any_rank_failed(const int32_t* d_st, int32_t P, int64_t sstride) {
+  if (!d_st) return false;
+  for (int32_t r = 0; r < P; ++r)
+    if (__ldcg(d_st + (uint64_t)r * sstride) & GTK_DEV_ERROR_MASK) return true;
+  return false;
+}
+
+__global__ void scatter_add_guarded_kernel(const int32_t* idx, const float* val, const int32_t* d_n, float* out,
+                                           const int32_t* d_st, int32_t P, int64_t sstride) {
+  if (any_rank_failed(d_st, P, sstride)) return;
+  const uint32_t n = (uint32_t)__ldg(d_n);
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int32_t i = __ldg(idx + e);
+    out[i] = __fadd_rn(out[i], __ldg(val + e));
+  }
+}
+
 __global__ void apply_touched_kernel(const int32_t* idx, const int32_t* d_n, int32_t P, int64_t stride, float* acc,
-                                     float* w, float lr, float Pf, int divide) {
+                                     float* w, float lr, float Pf, int divide, const int32_t* d_st, int64_t sstride,
+                                     int32_t* d_local) {
+  if (any_rank_failed(d_st, P, sstride)) {
+    // a healthy rank learns that a peer's selection failed (the failing
+    // rank's own word already carries its error)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && d_local && !(*d_local & GTK_DEV_ERROR_MASK))
+      atomicOr(d_local, GTK_DEV_PEER_FAILED);
+    return;
+  }
   const uint64_t tot = (uint64_t)P * (uint64_t)stride;
   for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < tot; q += (uint64_t)gridDim.x * blockDim.x) {
     const int32_t r = (int32_t)(q / (uint64_t)stride);
@@ -323,15 +350,19 @@ extern "C" int gtk_topk_accumulate(const int32_t* idx, const float* val, const i
 }
 
 extern "C" int gtk_topk_apply(const int32_t* idx, const float* val, const int32_t* d_n, int32_t P, int64_t stride,
-                              int64_t m, float* acc, float* w, float lr, int32_t divide, void* stream) {
-  if (!idx || !val || !d_n || !acc || !w || P < 1 || m < 1 || m >= (int64_t(1) << 31) || stride < 0)
+                              int64_t m, float* acc, float* w, float lr, int32_t divide, const int32_t* d_status,
+                              int64_t status_stride, int32_t* d_local_status, void* stream) {
+  if (!idx || !val || !d_n || !acc || !w || P < 1 || m < 1 || m >= (int64_t(1) << 31) || stride < 0 ||
+      status_stride < 0)
     return GTK_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   for (int r = 0; r < P; ++r) {  // rank order 0..P-1 (collectives.py:162-163), into the all-+0 acc
-    scatter_add_kernel<<<num_sms() * 2, 256, 0, st>>>(idx + r * stride, val + r * stride, d_n + r, acc);
+    scatter_add_guarded_kernel<<<num_sms() * 2, 256, 0, st>>>(idx + r * stride, val + r * stride, d_n + r, acc,
+                                                             d_status, P, status_stride);
     GTK_CHECK_LAUNCH();
   }
-  apply_touched_kernel<<<num_sms() * 2, 256, 0, st>>>(idx, d_n, P, stride, acc, w, lr, (float)P, divide);
+  apply_touched_kernel<<<num_sms() * 2, 256, 0, st>>>(idx, d_n, P, stride, acc, w, lr, (float)P, divide, d_status,
+                                                      status_stride, d_local_status);
   GTK_CHECK_LAUNCH();
   return GTK_OK;
 }

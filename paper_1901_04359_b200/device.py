@@ -331,12 +331,14 @@ def topk_accumulate(idx: torch.Tensor, val: torch.Tensor, counts: torch.Tensor, 
 
 
 def topk_apply(idx: torch.Tensor, val: torch.Tensor, counts: torch.Tensor, P_: int, stride: int, m: int,
-               acc: torch.Tensor, w: torch.Tensor, lr: float, divide: bool = True) -> None:
+               acc: torch.Tensor, w: torch.Tensor, lr: float, divide: bool = True, statuses=None,
+               status_stride: int = 1, local_status=None) -> None:
     """gtk_topk_apply: the topk baseline's momentum-0 update from the P
     gathered lists, at the touched entries only (acc: all-+0 f32[m] scratch,
-    left all +0)."""
+    left all +0).  statuses: the P ranks' status words (status_stride apart);
+    any error bit voids the update and flags local_status PEER_FAILED."""
     _lib.call("gtk_topk_apply", P(idx), P(val), P(counts), P_, stride, m, P(acc), P(w), ctypes.c_float(lr),
-              1 if divide else 0, stream_of(w.device))
+              1 if divide else 0, P(statuses), ctypes.c_int64(status_stride), P(local_status), stream_of(w.device))
 
 
 def dense_sum(srcs, m: int, out: torch.Tensor, ring: bool = False) -> None:

@@ -123,6 +123,7 @@ class DistDeviceGroup:
         self.dim_hint = 0
         self._plans: dict[int, _ExchangePlan] = {}
         self.aborted = False
+        self.topk_status_in_band = True  # topk(apply=...) carries the select's status (optimizer.topk_step)
         # abort word: pinned host memory mapped into the device; the exchange
         # kernel polls it while it waits for a partner (transport.py:210-214)
         lib = _lib.load()
@@ -214,23 +215,27 @@ class DistDeviceGroup:
         entries only)."""
         W = self.world
         if apply is not None:
-            # topk_step (w, lr, acc): every rank's list has the same capacity
+            # topk_step (w, lr, acc, status): every rank's list has the same capacity
             # (k), so one all-gather of [count | idx | value bits] per rank
             # carries the counts too -- no host read of the sizes -- and the
             # momentum-0 update runs at the touched entries only.  (Callers
             # pass the same k on every rank, like every step of the job.)
-            w, lr, acc = apply
+            # The select's status word travels in the same gather: any
+            # rank's error voids the update everywhere (PEER_FAILED on the
+            # healthy ranks) -- no host sync before the collective.
+            w, lr, acc, status = apply
             cap = lst.cap
-            stride = 2 * cap + 1
+            stride = 2 * cap + 2
             mine = torch.empty(stride, dtype=torch.int32, device=self.device)
             mine[0:1].copy_(lst.n)
-            mine[1:1 + cap].copy_(lst.idx)
-            mine[1 + cap:].copy_(lst.val.view(torch.int32))
+            mine[1:2].copy_(status[0:1])
+            mine[2:2 + cap].copy_(lst.idx)
+            mine[2 + cap:].copy_(lst.val.view(torch.int32))
             allv = torch.empty(W * stride, dtype=torch.int32, device=self.device)
             dist.all_gather_into_tensor(allv, mine)
             cnts = allv.view(W, stride)[:, 0].contiguous()
-            _dev.topk_apply(allv[1:], allv[1 + cap:].view(torch.float32), cnts, W, stride, lst.dim, acc, w, lr,
-                            divide)
+            _dev.topk_apply(allv[2:], allv[2 + cap:].view(torch.float32), cnts, W, stride, lst.dim, acc, w, lr,
+                            divide, statuses=allv[1:], status_stride=stride, local_status=status[0:1])
             self._topk_stats(ep, cnts)
             return None
         cnts = torch.empty(W, dtype=torch.int32, device=self.device)

@@ -419,9 +419,14 @@ def topk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float = 
     tm.mark(0)
     _select_checked(state, g, k, sel, status)
     tm.mark(1)
-    word = int(status[0].item())
-    _dev.raise_status(word)
-    if _dev.sparse_update_fusable(state.lr, state.momentum) and (P == 1 or hasattr(ep.group, "topk")):
+    sparse = _dev.sparse_update_fusable(state.lr, state.momentum) and (P == 1 or hasattr(ep.group, "topk"))
+    if not (sparse and (P == 1 or getattr(ep.group, "topk_status_in_band", False))):
+        # surface a local FloatingPointError before the collective (the
+        # in-band forms carry the status through it instead: a failed select
+        # voids the update on every rank and raises at the status read below)
+        word = int(status[0].item())
+        _dev.raise_status(word)
+    if sparse:
         # momentum 0, finite lr >= +0: the update touches only the gathered
         # lists' indices (w - lr * +0 leaves every other weight bitwise unchanged), so the
         # rank-ordered sums go to a persistent all-+0 scratch and the update
@@ -431,9 +436,10 @@ def topk_step(state: OptimizerState, ep, grad, k: int, P: int, *, loss: float = 
             acc = torch.zeros(state.m, dtype=torch.float32, device=dev)
         lr = float(np.float32(state.lr))
         if P == 1:
-            _dev.topk_apply(sel.idx, sel.val, sel.n, 1, sel.cap, state.m, acc, state._w, lr, divide=True)
+            _dev.topk_apply(sel.idx, sel.val, sel.n, 1, sel.cap, state.m, acc, state._w, lr, divide=True,
+                            statuses=status[0:1])
         else:
-            ep.group.topk(ep, sel, divide=True, apply=(state._w, lr, acc))
+            ep.group.topk(ep, sel, divide=True, apply=(state._w, lr, acc, status[0:1]))
         state._bufs["topk_acc"] = acc  # (dropped above if the collective raised)
         tm.mark(2)
     else:

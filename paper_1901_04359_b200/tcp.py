@@ -523,7 +523,7 @@ class HostStagedGroup:
         d = self.device
         ti, tv, tc = torch.from_numpy(idx).to(d), torch.from_numpy(val).to(d), torch.from_numpy(cnt).to(d)
         if apply is not None:  # (w, lr, acc): topk_step's momentum-0 update, touched entries only
-            w, lr, acc = apply
+            w, lr, acc = apply[:3]  # (the status was checked before the collective)
             _dev.topk_apply(ti, tv, tc, P, cap, lst.dim, acc, w, lr, divide)
             return None
         out = torch.empty(lst.dim, dtype=torch.float32, device=d)

@@ -115,6 +115,33 @@ def main():
         check(np.array_equal(bits(stt.weights), bits(reft[r].weights)), f"topk_step weights mom={mom}")
         check(np.array_equal(bits(stt.residual), bits(reft[r].residual)), f"topk_step residual mom={mom}")
 
+    # 2b'. a non-finite gradient on rank 0 in topk_step (status carried in
+    # the all-gather): rank 0 raises FloatingPointError, the others
+    # TransportError, nobody's state moves, and the next step is exact
+    from paper_1901_04359_b200.transport import TransportError as _TE
+
+    stp = opt.make_state(np.zeros(m, F32), lr=0.1)
+    opt.topk_step(stp, ep, grads[0][r], k, P)
+    w_before, res_before = stp.weights.copy(), stp.residual.copy()
+    badg = grads[1][r].copy()
+    if r == 0:
+        badg[17] = np.nan
+    try:
+        opt.topk_step(stp, ep, badg, k, P)
+        check(False, "poisoned topk_step did not raise")
+    except FloatingPointError:
+        check(r == 0, "FloatingPointError on a healthy rank")
+    except _TE:
+        check(r != 0, "TransportError on the failing rank")
+    check(np.array_equal(bits(stp.weights), bits(w_before)), "poisoned topk_step moved the weights")
+    check(np.array_equal(bits(stp.residual), bits(res_before)), "poisoned topk_step moved the residual")
+    opt.topk_step(stp, ep, grads[2][r], k, P)
+    refp = [orc.State(np.zeros(m, F32), 0.1) for _ in range(P)]
+    orc.topk_step_all(refp, [grads[0][q] for q in range(P)], k)
+    orc.topk_step_all(refp, [grads[2][q] for q in range(P)], k)
+    check(np.array_equal(bits(stp.weights), bits(refp[r].weights)), "topk_step after a poisoned step")
+    check(np.array_equal(bits(stp.residual), bits(refp[r].residual)), "topk_step residual after a poisoned step")
+
     # 2c. mismatched dense lengths raise ProtocolError on every rank
     # (collectives.py:113-117), and the group stays usable
     from paper_1901_04359_b200.transport import ProtocolError

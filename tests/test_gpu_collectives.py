@@ -500,3 +500,30 @@ def test_topk_step_touched_update_bitwise(gk, opt):
         orc.topk_step_all(ref, [grads[it]], k)
     assert np.array_equal(bits(st.weights), bits(ref[0].weights))
     assert np.array_equal(bits(st.residual), bits(ref[0].residual))
+
+
+def test_topk_step_nonfinite_voids_update_then_recovers(gk, opt):
+    """P = 1 topk_step with the select's status checked in the update kernel
+    (no host sync before it): FloatingPointError, state untouched, and the
+    next step exact against the oracle (the scratch stayed all +0)."""
+    from oracle import gtopk_oracle as orc
+
+    m, k = 50_000, 50
+    rng = np.random.default_rng(3)
+    g0, g2 = rng.standard_normal(m).astype(F32), rng.standard_normal(m).astype(F32)
+    bad = rng.standard_normal(m).astype(F32)
+    bad[123] = np.inf
+    (ep,) = gk.create_local_cluster(1)
+    st = opt.make_state(np.zeros(m, F32), lr=0.1)
+    opt.topk_step(st, ep, g0, k, 1)
+    w, r, it = st.weights.copy(), st.residual.copy(), st.iteration
+    with pytest.raises(FloatingPointError):
+        opt.topk_step(st, ep, bad, k, 1)
+    assert np.array_equal(bits(st.weights), bits(w)) and np.array_equal(bits(st.residual), bits(r))
+    assert st.iteration == it
+    opt.topk_step(st, ep, g2, k, 1)
+    ref = [orc.State(np.zeros(m, F32), 0.1)]
+    orc.topk_step_all(ref, [g0], k)
+    orc.topk_step_all(ref, [g2], k)
+    assert np.array_equal(bits(st.weights), bits(ref[0].weights))
+    assert np.array_equal(bits(st.residual), bits(ref[0].residual))
